@@ -1,0 +1,173 @@
+/*
+ * sweptnet_b200.h — C-ABI of the B200-native swept-volume proxy (arXiv 2402.15281).
+ *
+ * The drop-in boundary for the reference's inference hot path.  Every entry
+ * point takes plain pointers and sizes; no C++, Eigen or torch types cross it.
+ * Each function cites the reference interface it replaces (paths under
+ * /root/reference/proj):
+ *
+ *   svn_model_create          MlpT<float> construction  include/sweptnet/nn.hpp:16-44
+ *   svn_init_params           init_model<float>         include/sweptnet/nn.hpp:80-81, src/nn.cpp:57-93
+ *   svn_model_load_checkpoint load_checkpoint           include/sweptnet/nn.hpp:168, src/nn.cpp:524-576
+ *   svn_forward_eval          forward_eval<float>       include/sweptnet/nn.hpp:92-93, src/nn.cpp:95-130
+ *   svn_predict_min_distance  predict_min_distance      include/sweptnet/nn.hpp:162-163, src/nn.cpp:460-480
+ *   svn_query_min             ProxyEvaluator batch for gcc_nn_search_impl (collision.hpp:45,54-55;
+ *                             collision.cpp:63-69) and eval_classification (bench.cpp:98-124):
+ *                             predict_min_distance over M motions + `proxy > margin` in one call
+ *   svn_query_min_keys_device point-sharded partial of the above (new)
+ *   svn_keys_finalize_device  decode + margin classification of reduced keys (new)
+ *   svn_last_error            std::invalid_argument / IoError what() strings (nn.cpp:98-99,462,465;
+ *                             errors.hpp:8-27)
+ *
+ * Error convention: every function returns an svn_status; 0 = OK.  On failure the
+ * thread-local svn_last_error() holds the message.  Messages for the argument
+ * errors are the reference's own exception texts, so a C++ shim can rethrow
+ * std::invalid_argument(svn_last_error()) unchanged.
+ *
+ * Threading: all entry points are re-entrant.  Models are immutable after
+ * creation (nn.hpp:84-87) and may be shared by any number of threads; each call
+ * runs on the caller's stream (device entry points) or on a per-thread stream
+ * (host entry points).  run_box_world calls predict_min_distance from
+ * parallel_for workers (bench.cpp:156,193), and that pattern is supported.
+ */
+#ifndef SWEPTNET_B200_H
+#define SWEPTNET_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SVN_API __attribute__((visibility("default")))
+
+typedef enum {
+    SVN_OK = 0,
+    SVN_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    SVN_ERR_CUDA = 2,
+    SVN_ERR_OUT_OF_MEMORY = 3,
+    SVN_ERR_UNSUPPORTED = 4, /* shape/program the device kernels do not implement */
+    SVN_ERR_IO = 5,          /* IoError          errors.hpp:8  */
+    SVN_ERR_FORMAT = 6,      /* FormatError      errors.hpp:13 */
+    SVN_ERR_TRUNCATION = 7,  /* TruncationError  errors.hpp:18 */
+    SVN_ERR_VERSION = 8      /* VersionError     errors.hpp:23 */
+} svn_status;
+
+/* Arithmetic of the fused MLP kernel.
+ *  BF16        tcgen05 tensor cores, bf16 weights/activations, fp32 accumulate
+ *              in TMEM; per-point delta within the bound stated per config.
+ *  FP32        SIMT fp32 FMA with the per-motion q-fold (|d delta| <= 1e-5).
+ *  FP32_EXACT  SIMT fp32 FMA in the reference's exact accumulation order
+ *              (bias, h part, x, q0, q1 — nn.cpp:118-124): bit-identical to the
+ *              reference float path up to the documented dot-product order. */
+typedef enum { SVN_PREC_BF16 = 0, SVN_PREC_FP32 = 1, SVN_PREC_FP32_EXACT = 2 } svn_precision;
+
+/* One hidden layer of a layer program.  Layer 0 reads the
+ * normalised input z only; layer l>0 reads [h_{l-1}; z] when concat != 0.
+ *   a = W.in + b ; r = act ? max(a,0) : a ; p = affine ? r*s + t : r ;
+ *   h = residual ? h_{l-1} + p : p
+ * The reference's Fig. 2 network (nn.hpp:11-15) is layer 0 {1,0,0,0} followed
+ * by n_blocks layers {1,1,1,1}. */
+typedef struct {
+    int32_t concat;
+    int32_t act;
+    int32_t affine;
+    int32_t residual;
+} svn_layer;
+
+typedef struct {
+    int32_t n_layers;        /* hidden layers incl. the input layer, 1..32   */
+    int32_t width;           /* N (block_dim); 128, 256 or 512 on device     */
+    int32_t dof;             /* input_dim = 3 + 2*dof                        */
+    const svn_layer* layers; /* [n_layers]                                    */
+} svn_model_desc;
+
+typedef struct svn_model svn_model;
+
+/* Number of floats in the parameter buffer for `desc`:
+ *   norm_shift[in], norm_scale[in],
+ *   per layer l: W_l column-major [N x K_l] (K_0 = in; K_l = N + concat*in),
+ *                b_l[N], if affine: gamma[N], beta[N], running_mean[N], running_var[N],
+ *   output_weight[N], output_bias.
+ * For the Fig. 2 program this equals the SVCKPT01 body (nn.cpp:507-520). */
+SVN_API int64_t svn_param_count(const svn_model_desc* desc);
+
+/* Trainable parameter count as MlpT::param_count (nn.cpp:19-24). */
+SVN_API int64_t svn_trainable_param_count(const svn_model_desc* desc);
+
+/* Seeded weights as init_model (nn.cpp:57-93) on std::mt19937_64(seed):
+ * bound_mode 0 = uniform(+-1/sqrt(fan_in)) (init_model), 1 = uniform(+-sqrt(6/fan_in))
+ * (He-uniform, the BASELINE.json configs).  Writes svn_param_count floats. */
+SVN_API svn_status svn_init_params(const svn_model_desc* desc, uint64_t seed, int32_t bound_mode,
+                                   float* params_out);
+
+/* Upload a model to `device` and build every device layout (folded BN, bf16
+ * pre-swizzled tcgen05 weight stream, fp32 transposed weights). */
+SVN_API svn_status svn_model_create(const svn_model_desc* desc, const float* params, int64_t n_params,
+                                    int32_t device, svn_model** out);
+
+/* Read a reference SVCKPT01 checkpoint (nn.cpp:499-576) as a Fig. 2 program. */
+SVN_API svn_status svn_model_load_checkpoint(const char* path, int32_t device, svn_model** out);
+
+SVN_API svn_status svn_model_destroy(svn_model* model);
+
+/* Batched proxy, device-resident inputs (pointers are device memory):
+ *   points  float [P x 3]            (x, y, z)
+ *   q01     float [M x 2*dof]        (q0 | q1 per motion)
+ * outputs per motion m:
+ *   min_out    float [M]   min over points of delta(x_p, q0_m, q1_m)
+ *   argmin_out int32 [M]   lowest index attaining it (nn.cpp:476-478)
+ *   free_out   uint8 [M]   double(min) > margin (collision.cpp:68)
+ *   per_point  float [M x P] or NULL: every delta (only written when non-NULL)
+ * `stream` is a cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+SVN_API svn_status svn_query_min_device(const svn_model* model, svn_precision prec, const float* points,
+                                        int64_t P, const float* q01, int64_t M, double margin,
+                                        float* min_out, int32_t* argmin_out, uint8_t* free_out,
+                                        float* per_point, void* stream);
+
+/* Same with HOST buffers; copies in and out, synchronous. */
+SVN_API svn_status svn_query_min(const svn_model* model, svn_precision prec, const float* points, int64_t P,
+                                 const float* q01, int64_t M, double margin, float* min_out,
+                                 int32_t* argmin_out, uint8_t* free_out, float* per_point);
+
+/* Point-sharded partial (device pointers): folds min over this shard's points
+ * into keys[M] with atomicMin.  key = (orderable(delta) << 32) | (index_offset + p);
+ * the caller initialises keys to UINT64_MAX (svn_keys_init_device) and reduces
+ * shards with a u64 MIN all-reduce before svn_keys_finalize_device. */
+SVN_API svn_status svn_keys_init_device(uint64_t* keys, int64_t M, void* stream);
+SVN_API svn_status svn_query_min_keys_device(const svn_model* model, svn_precision prec, const float* points,
+                                             int64_t P, int64_t index_offset, const float* q01, int64_t M,
+                                             uint64_t* keys, void* stream);
+SVN_API svn_status svn_keys_finalize_device(const uint64_t* keys, int64_t M, double margin, float* min_out,
+                                            int32_t* argmin_out, uint8_t* free_out, void* stream);
+
+/* forward_eval<float> (nn.cpp:95-130): raw row-major [B x cols], row = [x, q0, q1];
+ * rows may mix motions (consecutive rows with equal q share a motion). HOST buffers. */
+SVN_API svn_status svn_forward_eval(const svn_model* model, svn_precision prec, const float* raw, int64_t B,
+                                    int64_t cols, float* out);
+SVN_API svn_status svn_forward_eval_device(const svn_model* model, svn_precision prec, const float* raw,
+                                           int64_t B, int64_t cols, float* out, void* stream);
+
+/* predict_min_distance (nn.cpp:460-480) with the reference's argument types:
+ * cloud double [P x 3], q0/q1 double [dof].  HOST buffers. */
+SVN_API svn_status svn_predict_min_distance(const svn_model* model, svn_precision prec, const double* cloud,
+                                            int64_t P, const double* q0, const double* q1, int32_t dof,
+                                            double* min_out, int32_t* argmin_out);
+
+/* Kernel launches issued by this thread since the last reset (evidence for bench.py). */
+SVN_API int64_t svn_launch_count(void);
+SVN_API void svn_launch_count_reset(void);
+
+/* Kernel timing for the roofline: between begin and end, every fused-MLP kernel
+ * launched by this thread is bracketed by CUDA events on its own stream.  end
+ * synchronises those events and returns the summed device time and the count. */
+SVN_API void svn_kernel_timing_begin(void);
+SVN_API svn_status svn_kernel_timing_end(double* total_ms, int64_t* launches);
+
+SVN_API const char* svn_last_error(void);
+SVN_API const char* svn_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SWEPTNET_B200_H */

@@ -1,0 +1,143 @@
+// fused.cuh — launch parameters shared by the host ABI and the device kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace svn {
+
+constexpr int kMaxLayers = 32;
+constexpr int kMaxIn = 32;  // input_dim = 3 + 2*dof <= 32
+
+enum : int { kConcat = 1, kAct = 2, kAffine = 4, kResidual = 8 };
+
+struct LayerDev {
+    const float* bias;  // [N] layer bias (used when the layer has no folded motion bias)
+    const float* s;     // [N] folded BN scale (affine layers)
+    const float* t;     // [N] folded BN shift
+    const float* wx;    // [3][N] fp32 x-part columns (concat layers), SoA
+    int flags;          // kConcat | kAct | kAffine | kResidual
+    int mb_slot;        // slot in the per-motion bias buffer, -1 if none
+};
+
+// One unit of work: `nrows` consecutive rows of one motion.
+struct TileDesc {
+    int64_t point_base;  // first point (row) index
+    int64_t out_base;    // first per-point output index
+    int32_t motion;
+    int32_t nrows;
+};
+
+struct FusedArgs {
+    // model
+    int L, N, dof, in;
+    LayerDev layer[kMaxLayers];
+    const float* wo;  // [N]
+    float bo;
+    float shift[kMaxIn], scale[kMaxIn];  // input normaliser
+    // weights
+    const void* wstream;        // bf16: pre-swizzled tcgen05 weight stream for layers 1..L-1
+    const float* wt[kMaxLayers];  // fp32: [K_l][N] transposed weights, rows (h | x | q)
+    int wt_rows[kMaxLayers];      // rows in wt[l]
+    // inputs
+    const float* points;  // row r -> points[r * point_stride + 0..2]
+    int64_t point_stride;
+    int64_t P;            // points per motion (dense mode)
+    const float* q01;     // [M][2*dof]
+    int64_t M;
+    const float* motion_bias;  // [M][n_mb][N]
+    int n_mb;
+    // work decomposition
+    int64_t tiles_per_motion;  // dense mode
+    int64_t n_tiles;
+    const TileDesc* tiles;     // non-null: explicit tile table (forward_eval segments)
+    int exact;                 // fp32 exact order (no q fold)
+    // outputs
+    unsigned long long* keys;  // [M] packed (orderable(delta) << 32 | index), or null
+    unsigned int* counters;    // [M] tiles done, for the fused finaliser, or null
+    int64_t index_offset;      // added to point indices in keys
+    float* min_out;
+    int32_t* argmin_out;
+    uint8_t* free_out;
+    double margin;
+    float* per_point;          // [.. out_base + row], or null
+};
+
+// Orderable-u32 map of a float: unsigned compare == float compare; NaN -> max.
+__device__ __forceinline__ uint32_t orderable(float f) {
+    uint32_t u = __float_as_uint(f);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0xffffffffu;  // NaN: never the min
+    if (u == 0x80000000u) u = 0u;  // -0 == +0 under '<' (ties then go to the lowest index)
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+__device__ __forceinline__ float from_orderable(uint32_t o) {
+    const uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+    return __uint_as_float(u);
+}
+
+// Key of one row.  A NaN at point index 0 sticks (nn.cpp:476-478: best starts at
+// 0 and `pred[i] < NaN` is always false), so it gets key 0, the global minimum.
+__device__ __forceinline__ unsigned long long row_key(float delta, int64_t point_index) {
+    const bool nan = isnan(delta);
+    if (nan && point_index == 0) return 0ull;
+    return (static_cast<unsigned long long>(orderable(delta)) << 32) | static_cast<uint32_t>(point_index);
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// Decode a reduced key into the reference's (min, argmin) and the margin class.
+__device__ __forceinline__ void decode_key(unsigned long long key, double margin, float* min_out,
+                                           int32_t* argmin_out, uint8_t* free_out) {
+    const uint32_t hi = static_cast<uint32_t>(key >> 32);
+    float v;
+    int32_t idx = static_cast<int32_t>(static_cast<uint32_t>(key));
+    if (key == 0ull) {
+        v = __uint_as_float(0x7fc00000u);  // NaN at index 0
+        idx = 0;
+    } else if (hi == 0xffffffffu) {
+        v = __uint_as_float(0x7fc00000u);  // every row NaN (index 0 handled above)
+    } else {
+        v = from_orderable(hi);
+    }
+    *min_out = v;
+    *argmin_out = idx;
+    *free_out = static_cast<double>(v) > margin ? 1 : 0;  // strict, in double (collision.cpp:68)
+}
+
+// Work item t -> (motion, first point, first output index, valid rows).
+__device__ __forceinline__ void tile_decode(const FusedArgs& a, int64_t t, int64_t TM, int32_t& motion,
+                                            int64_t& pbase, int64_t& obase, int32_t& nrows) {
+    if (a.tiles) {
+        const TileDesc d = a.tiles[t];
+        motion = d.motion;
+        pbase = d.point_base;
+        obase = d.out_base;
+        nrows = d.nrows;
+    } else {
+        motion = static_cast<int32_t>(t / a.tiles_per_motion);
+        pbase = (t % a.tiles_per_motion) * TM;
+        obase = static_cast<int64_t>(motion) * a.P + pbase;
+        const int64_t rem = a.P - pbase;
+        nrows = static_cast<int32_t>(rem < TM ? rem : TM);
+    }
+}
+
+// Launchers (kernels_*.cu).
+cudaError_t launch_motion_bias(const FusedArgs& a, const float* wq /*[n_mb][2dof][N]*/,
+                               const float* mb_base_bias /*[n_mb][N]*/, float* motion_bias,
+                               unsigned long long* keys_init, unsigned int* counters_init, int64_t n_keys,
+                               cudaStream_t st);
+cudaError_t launch_keys_init(unsigned long long* keys, int64_t M, cudaStream_t st);
+cudaError_t launch_keys_finalize(const unsigned long long* keys, int64_t M, double margin, float* min_out,
+                                 int32_t* argmin_out, uint8_t* free_out, cudaStream_t st);
+cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_fused_bf16(const FusedArgs& a, int num_sms, cudaStream_t st);
+
+}  // namespace svn

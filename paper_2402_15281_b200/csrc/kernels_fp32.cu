@@ -1,0 +1,323 @@
+// kernels_fp32.cu — K0 (per-motion q-fold), key init/finalise, and K1f: the fused
+// fp32 SIMT MLP + min/argmin + margin kernel.
+//
+// K1f replaces the row loop of forward_eval (/root/reference/proj/src/nn.cpp:116-128)
+// plus the argmin of predict_min_distance (nn.cpp:476-478) and the margin test
+// (collision.cpp:68).  Each CTA owns a 64-row tile of one motion.  Activations stay
+// in shared memory, transposed (actT[k][row]), between layers; weight rows stream
+// through a 4-stage ring of 16 KiB bulk copies (cp.async.bulk, TMA engine).  Each
+// output is one sequential fmaf chain over k ascending — the same order as the
+// reference's column axpy — so with `exact` set (no q-fold: bias, h part, x, q0,
+// q1) the per-point delta matches the CPU restatement bit for bit.
+#include <cuda_runtime.h>
+
+#include "fused.cuh"
+#include "ptx.cuh"
+
+namespace svn {
+
+// ------------------------------------------------------------------ K0 ------
+struct QNorm {
+    float shift[kMaxIn], scale[kMaxIn];
+};
+
+// motion_bias[m][slot][c] = b[c] + sum_k Wq[slot][k][c] * zq_m[k]   (k ascending:
+// q0 then q1), zq = (q - shift) * scale.  Block (m, slot), one thread per column.
+// Also resets the per-motion keys/counters used by the fused finaliser.
+__global__ void motion_bias_kernel(const float* __restrict__ q01, int64_t M, int dof, int N, int n_mb,
+                                   const float* __restrict__ wq, const float* __restrict__ base_bias,
+                                   float* __restrict__ motion_bias, const QNorm qn, unsigned long long* keys,
+                                   unsigned int* counters, int64_t n_keys) {
+    const int64_t m = blockIdx.x;
+    const int slot = blockIdx.y;
+    if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
+        keys[m] = ~0ull;
+        counters[m] = 0u;
+    }
+    if (slot >= n_mb) return;
+    __shared__ float zq[kMaxIn];
+    const int nq = 2 * dof;
+    if (threadIdx.x < nq) {
+        const float q = q01[m * nq + threadIdx.x];
+        zq[threadIdx.x] = __fmul_rn(__fsub_rn(q, qn.shift[threadIdx.x]), qn.scale[threadIdx.x]);
+    }
+    __syncthreads();
+    const float* w = wq + static_cast<int64_t>(slot) * nq * N;
+    for (int c = threadIdx.x; c < N; c += blockDim.x) {
+        float acc = base_bias[slot * N + c];
+        for (int k = 0; k < nq; ++k) acc = __fmaf_rn(zq[k], w[k * N + c], acc);
+        motion_bias[(m * n_mb + slot) * N + c] = acc;
+    }
+}
+
+cudaError_t launch_motion_bias(const FusedArgs& a, const float* wq, const float* mb_base_bias,
+                               float* motion_bias, unsigned long long* keys_init, unsigned int* counters_init,
+                               int64_t n_keys, cudaStream_t st) {
+    if (a.M <= 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
+    const int threads = a.N >= 256 ? 256 : 128;
+    QNorm qn;
+    for (int k = 0; k < 2 * a.dof && k < kMaxIn; ++k) {
+        qn.shift[k] = a.shift[3 + k];
+        qn.scale[k] = a.scale[3 + k];
+    }
+    motion_bias_kernel<<<grid, threads, 0, st>>>(a.q01, a.M, a.dof, a.N, a.n_mb, wq, mb_base_bias, motion_bias,
+                                                 qn, keys_init, counters_init, n_keys);
+    return cudaGetLastError();
+}
+
+__global__ void keys_init_kernel(unsigned long long* keys, int64_t M) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < M) keys[i] = ~0ull;
+}
+
+cudaError_t launch_keys_init(unsigned long long* keys, int64_t M, cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    keys_init_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, st>>>(keys, M);
+    return cudaGetLastError();
+}
+
+__global__ void keys_finalize_kernel(const unsigned long long* keys, int64_t M, double margin, float* min_out,
+                                     int32_t* argmin_out, uint8_t* free_out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i < M) decode_key(keys[i], margin, min_out + i, argmin_out + i, free_out + i);
+}
+
+cudaError_t launch_keys_finalize(const unsigned long long* keys, int64_t M, double margin, float* min_out,
+                                 int32_t* argmin_out, uint8_t* free_out, cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    keys_finalize_kernel<<<static_cast<unsigned>((M + 255) / 256), 256, 0, st>>>(keys, M, margin, min_out,
+                                                                                 argmin_out, free_out);
+    return cudaGetLastError();
+}
+
+// Called by one thread after this CTA's atomicMin for `motion` is done.
+__device__ __forceinline__ void tile_done(const FusedArgs& a, int32_t motion) {
+    if (!a.counters) return;
+    __threadfence();
+    const unsigned int prev = atomicAdd(a.counters + motion, 1u);
+    if (prev + 1 == static_cast<unsigned int>(a.tiles_per_motion)) {
+        __threadfence();
+        const unsigned long long key = atomicOr(a.keys + motion, 0ull);
+        decode_key(key, a.margin, a.min_out + motion, a.argmin_out + motion, a.free_out + motion);
+    }
+}
+
+// ------------------------------------------------------------------ K1f -----
+template <int N>
+struct Fp32Cfg {
+    static constexpr int TM = 64;                 // rows per tile
+    static constexpr int THREADS = 256;           // 8 row groups x 32 column groups
+    static constexpr int NC = N / 32;             // columns per thread
+    static constexpr int KS = 4096 / N;           // weight rows per 16 KiB chunk
+    static constexpr int STAGES = 4;
+    static constexpr int ACT_ROWS = N + kMaxIn;   // h rows then z rows
+    static constexpr size_t ACT_BYTES = static_cast<size_t>(ACT_ROWS) * TM * 4;
+    static constexpr size_t STAGE_BYTES = static_cast<size_t>(KS) * N * 4;
+    static constexpr size_t SMEM = ACT_BYTES + STAGES * STAGE_BYTES + 64;
+};
+
+struct ChunkIter {
+    int layer, chunk;
+};
+
+template <int N>
+__device__ __forceinline__ int layer_rows(const FusedArgs& a, int l) {
+    // exact: every row of wt[l]; folded: drop the q rows of concat layers.
+    const bool concat = (l == 0) || (a.layer[l].flags & kConcat);
+    return (a.exact || !concat) ? a.wt_rows[l] : a.wt_rows[l] - 2 * a.dof;
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, 1) fused_fp32_kernel(const __grid_constant__ FusedArgs a) {
+    using C = Fp32Cfg<N>;
+    extern __shared__ __align__(128) uint8_t smem[];
+    float* actT = reinterpret_cast<float*>(smem);
+    float* wst = reinterpret_cast<float*>(smem + C::ACT_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::ACT_BYTES + C::STAGES * C::STAGE_BYTES);
+
+    const int tid = threadIdx.x;
+    const int cg = tid & 31, rg = tid >> 5;
+    const int L = a.L;
+
+    // chunks per tile
+    int chunks_per_tile = 0;
+    for (int l = 0; l < L; ++l) chunks_per_tile += (layer_rows<N>(a, l) + C::KS - 1) / C::KS;
+    int64_t my_tiles = 0;
+    if (blockIdx.x < a.n_tiles) my_tiles = (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1;
+    const int64_t total_chunks = my_tiles * chunks_per_tile;
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    // producer state (thread 0): issues chunk g_prod into stage g_prod % STAGES
+    ChunkIter prod{0, 0};
+    int64_t g_prod = 0;
+    const uint64_t pol = policy_evict_last();
+    auto issue = [&]() {
+        const int rows = layer_rows<N>(a, prod.layer);
+        const int r0 = prod.chunk * C::KS;
+        const int nr = rows - r0 < C::KS ? rows - r0 : C::KS;
+        const int s = static_cast<int>(g_prod % C::STAGES);
+        const uint32_t bytes = static_cast<uint32_t>(nr) * N * 4u;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(wst + static_cast<size_t>(s) * C::KS * N, a.wt[prod.layer] + static_cast<size_t>(r0) * N, bytes,
+                 &full[s], pol);
+        ++g_prod;
+        if (r0 + C::KS >= rows) {
+            prod.chunk = 0;
+            prod.layer = prod.layer + 1 == L ? 0 : prod.layer + 1;
+        } else {
+            ++prod.chunk;
+        }
+    };
+    if (tid == 0)
+        while (g_prod < total_chunks && g_prod < C::STAGES) issue();
+
+    int64_t g = 0;  // consumer chunk counter
+    for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
+        int32_t motion, nrows;
+        int64_t pbase, obase;
+        tile_decode(a, t, C::TM, motion, pbase, obase, nrows);
+
+        // z rows: actT[N + k][row] = (raw_k - shift_k) * scale_k
+        if (tid < C::TM) {
+            const int64_t pr = pbase + (tid < nrows ? tid : 0);
+            const float* xp = a.points + pr * a.point_stride;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                actT[(N + k) * C::TM + tid] = __fmul_rn(__fsub_rn(xp[k], a.shift[k]), a.scale[k]);
+            if (a.exact) {
+                const float* q = a.q01 + static_cast<int64_t>(motion) * 2 * a.dof;
+                for (int k = 0; k < 2 * a.dof; ++k)
+                    actT[(N + 3 + k) * C::TM + tid] = __fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]);
+            }
+        }
+        __syncthreads();
+
+        for (int l = 0; l < L; ++l) {
+            const LayerDev& ld = a.layer[l];
+            const bool concat = (l == 0) || (ld.flags & kConcat);
+            const float* bias = (!a.exact && concat && ld.mb_slot >= 0)
+                                    ? a.motion_bias + (static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * N
+                                    : ld.bias;
+            float acc[8][C::NC];
+#pragma unroll
+            for (int j4 = 0; j4 < C::NC / 4; ++j4) {
+                const float4 b4 = *reinterpret_cast<const float4*>(bias + cg * 4 + j4 * 128);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    acc[i][j4 * 4 + 0] = b4.x;
+                    acc[i][j4 * 4 + 1] = b4.y;
+                    acc[i][j4 * 4 + 2] = b4.z;
+                    acc[i][j4 * 4 + 3] = b4.w;
+                }
+            }
+            const int rows = layer_rows<N>(a, l);
+            const int a_off = (l == 0) ? N : 0;
+            for (int r0 = 0; r0 < rows; r0 += C::KS) {
+                const int s = static_cast<int>(g % C::STAGES);
+                mbar_wait(&full[s], static_cast<uint32_t>((g / C::STAGES) & 1));
+                const float* w = wst + static_cast<size_t>(s) * C::KS * N;
+                const int nk = rows - r0 < C::KS ? rows - r0 : C::KS;
+                for (int kk = 0; kk < nk; ++kk) {
+                    const float* arow = actT + (a_off + r0 + kk) * C::TM + rg * 8;
+                    const float4 a0 = *reinterpret_cast<const float4*>(arow);
+                    const float4 a1 = *reinterpret_cast<const float4*>(arow + 4);
+                    const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    float wv[C::NC];
+#pragma unroll
+                    for (int j4 = 0; j4 < C::NC / 4; ++j4) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(w + kk * N + cg * 4 + j4 * 128);
+                        wv[j4 * 4 + 0] = w4.x;
+                        wv[j4 * 4 + 1] = w4.y;
+                        wv[j4 * 4 + 2] = w4.z;
+                        wv[j4 * 4 + 3] = w4.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < C::NC; ++j) acc[i][j] = __fmaf_rn(av[i], wv[j], acc[i][j]);
+                }
+                __syncthreads();  // every thread is done with stage s
+                if (tid == 0 && g_prod < total_chunks) issue();
+                ++g;
+            }
+            // epilogue: activation / folded BN / residual, written back in place
+            const int fl = ld.flags;
+            const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+#pragma unroll
+            for (int j4 = 0; j4 < C::NC / 4; ++j4) {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int col = cg * 4 + j4 * 128 + jj;
+                    const float sv = aff ? ld.s[col] : 0.f, tv = aff ? ld.t[col] : 0.f;
+                    float* hrow = actT + col * C::TM + rg * 8;
+                    float hv[8];
+                    if (res) {
+                        const float4 h0 = *reinterpret_cast<const float4*>(hrow);
+                        const float4 h1 = *reinterpret_cast<const float4*>(hrow + 4);
+                        hv[0] = h0.x, hv[1] = h0.y, hv[2] = h0.z, hv[3] = h0.w;
+                        hv[4] = h1.x, hv[5] = h1.y, hv[6] = h1.z, hv[7] = h1.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float r = acc[i][j4 * 4 + jj];
+                        if (act) r = r > 0.f ? r : 0.f;
+                        if (aff) r = __fmaf_rn(r, sv, tv);
+                        hv[i] = res ? __fadd_rn(hv[i], r) : r;
+                    }
+                    *reinterpret_cast<float4*>(hrow) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                    *reinterpret_cast<float4*>(hrow + 4) = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                }
+            }
+            __syncthreads();
+        }
+
+        // output layer: delta = sum_k w_o[k] h[k] (sequential fmaf) + b_o; min/argmin
+        if (tid < C::TM) {
+            float acc = 0.f;
+            for (int k = 0; k < N; ++k) acc = __fmaf_rn(a.wo[k], actT[k * C::TM + tid], acc);
+            const float delta = __fadd_rn(acc, a.bo);
+            const bool valid = tid < nrows;
+            if (valid && a.per_point) a.per_point[obase + tid] = delta;
+            if (a.keys) {
+                unsigned long long key = valid ? row_key(delta, a.index_offset + pbase + tid) : ~0ull;
+                key = warp_min_u64(key);
+                if ((tid & 31) == 0) atomicMin(a.keys + motion, key);
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && a.keys) tile_done(a, motion);
+    }
+}
+
+template <int N>
+static cudaError_t launch_fp32_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    using C = Fp32Cfg<N>;
+    static bool attr_set = false;  // benign race: idempotent attribute set
+    if (!attr_set) {
+        cudaError_t e =
+            cudaFuncSetAttribute(fused_fp32_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
+    if (grid < 1) return cudaSuccess;
+    fused_fp32_kernel<N><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    switch (a.N) {
+        case 128: return launch_fp32_n<128>(a, num_sms, st);
+        case 256: return launch_fp32_n<256>(a, num_sms, st);
+        case 512: return launch_fp32_n<512>(a, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace svn

@@ -1,0 +1,704 @@
+// svn_abi.cu — implementation of the C-ABI declared in include/sweptnet_b200.h.
+//
+// Host-side model preparation (layer program parse, BN fold, per-layer device
+// layouts, bf16 tcgen05 weight stream), argument validation with the reference's
+// exception texts, stream-ordered scratch, kernel sequencing (K0 -> K1), the
+// host-buffer convenience entry points that mirror the reference signatures, and
+// the SVCKPT01 checkpoint reader.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/sweptnet_b200.h"
+#include "fused.cuh"
+#include "ptx.cuh"
+
+using namespace svn;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+thread_local bool g_timing = false;
+thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+
+svn_status fail(svn_status code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+svn_status cuda_fail(cudaError_t e, const char* what) {
+    const svn_status code = (e == cudaErrorMemoryAllocation) ? SVN_ERR_OUT_OF_MEMORY : SVN_ERR_CUDA;
+    return fail(code, std::string("CUDA error in ") + what + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e));
+}
+
+#define SVN_CUDA(call, what)                       \
+    do {                                           \
+        cudaError_t e_ = (call);                   \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int layer_k(const svn_layer* layers, int l, int N, int in) {
+    if (l == 0) return in;
+    return N + (layers[l].concat ? in : 0);
+}
+
+svn_status validate_desc(const svn_model_desc* d) {
+    if (!d || !d->layers) return fail(SVN_ERR_INVALID_ARGUMENT, "model: null descriptor");
+    if (d->n_layers < 1 || d->n_layers > kMaxLayers)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "model: n_layers must be in 1..32");
+    if (d->width < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "init_model: n_blocks, block_dim and dof must be >= 1");
+    if (d->dof < 1 || 3 + 2 * d->dof > kMaxIn)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "model: dof must be in 1..14");
+    return SVN_OK;
+}
+
+}  // namespace
+
+struct svn_model {
+    int device = 0;
+    int L = 0, N = 0, dof = 0, in = 0;
+    int num_sms = 148;
+    int n_mb = 0;
+    std::vector<svn_layer> layers;
+    std::vector<void*> allocs;
+    FusedArgs base{};        // model part of the kernel arguments
+    float* d_wq = nullptr;     // [n_mb][2dof][N]
+    float* d_mbbase = nullptr; // [n_mb][N]
+    bool has_bf16 = false;
+
+    template <class T>
+    svn_status upload(const T* host, size_t count, T** out) {
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, sizeof(T) * (count ? count : 1));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(model)");
+        allocs.push_back(p);
+        if (count) {
+            e = cudaMemcpy(p, host, sizeof(T) * count, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(model)");
+        }
+        *out = static_cast<T*>(p);
+        return SVN_OK;
+    }
+    ~svn_model() {
+        DeviceGuard g(device);
+        for (void* p : allocs) cudaFree(p);
+    }
+};
+
+extern "C" {
+
+SVN_API const char* svn_last_error(void) { return g_err.c_str(); }
+SVN_API const char* svn_version(void) { return "sweptnet_b200 0.1 (sm_100a)"; }
+SVN_API int64_t svn_launch_count(void) { return g_launches; }
+SVN_API void svn_launch_count_reset(void) { g_launches = 0; }
+
+SVN_API void svn_kernel_timing_begin(void) {
+    for (auto& ev : g_events) {
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    g_events.clear();
+    g_timing = true;
+}
+
+SVN_API svn_status svn_kernel_timing_end(double* total_ms, int64_t* launches) {
+    g_timing = false;
+    double sum = 0.0;
+    for (auto& ev : g_events) {
+        SVN_CUDA(cudaEventSynchronize(ev.second), "cudaEventSynchronize");
+        float ms = 0.f;
+        SVN_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second), "cudaEventElapsedTime");
+        sum += ms;
+        cudaEventDestroy(ev.first);
+        cudaEventDestroy(ev.second);
+    }
+    if (total_ms) *total_ms = sum;
+    if (launches) *launches = static_cast<int64_t>(g_events.size());
+    g_events.clear();
+    return SVN_OK;
+}
+
+SVN_API int64_t svn_param_count(const svn_model_desc* d) {
+    if (validate_desc(d) != SVN_OK) return -1;
+    const int N = d->width, in = 3 + 2 * d->dof;
+    int64_t n = 2 * static_cast<int64_t>(in);
+    for (int l = 0; l < d->n_layers; ++l) {
+        n += static_cast<int64_t>(N) * layer_k(d->layers, l, N, in) + N;
+        if (d->layers[l].affine) n += 4 * static_cast<int64_t>(N);
+    }
+    return n + N + 1;
+}
+
+SVN_API int64_t svn_trainable_param_count(const svn_model_desc* d) {
+    if (validate_desc(d) != SVN_OK) return -1;
+    const int N = d->width, in = 3 + 2 * d->dof;
+    int64_t n = 0;
+    for (int l = 0; l < d->n_layers; ++l) {
+        n += static_cast<int64_t>(N) * layer_k(d->layers, l, N, in) + N;
+        if (d->layers[l].affine) n += 2 * static_cast<int64_t>(N);
+    }
+    return n + N + 1;
+}
+
+// init_model (nn.cpp:57-93): one std::mt19937_64 stream; tensors in order layer 0 W,
+// hidden W's, output W; each drawn row-major over [out x in] (nn.cpp:70-71) with
+// Rng::uniform (rng.hpp:21-23) and stored column-major.
+SVN_API svn_status svn_init_params(const svn_model_desc* d, uint64_t seed, int32_t bound_mode, float* p) {
+    svn_status st = validate_desc(d);
+    if (st != SVN_OK) return st;
+    if (!p) return fail(SVN_ERR_INVALID_ARGUMENT, "init_params: null output");
+    const int N = d->width, in = 3 + 2 * d->dof;
+    std::mt19937_64 eng(seed);
+    auto uniform = [&](double lo, double hi) {
+        const double u = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+        return std::fma(hi - lo, u, lo);
+    };
+    float* q = p;
+    for (int i = 0; i < in; ++i) *q++ = 0.0f;
+    for (int i = 0; i < in; ++i) *q++ = 1.0f;
+    for (int l = 0; l < d->n_layers; ++l) {
+        const int K = layer_k(d->layers, l, N, in);
+        const double bound = bound_mode ? std::sqrt(6.0 / K) : 1.0 / std::sqrt(static_cast<double>(K));
+        for (int r = 0; r < N; ++r)
+            for (int c = 0; c < K; ++c) q[static_cast<int64_t>(c) * N + r] = static_cast<float>(uniform(-bound, bound));
+        q += static_cast<int64_t>(N) * K;
+        for (int i = 0; i < N; ++i) *q++ = 0.0f;
+        if (d->layers[l].affine) {
+            for (int i = 0; i < N; ++i) *q++ = 1.0f;
+            for (int i = 0; i < N; ++i) *q++ = 0.0f;
+            for (int i = 0; i < N; ++i) *q++ = 0.0f;
+            for (int i = 0; i < N; ++i) *q++ = 1.0f;
+        }
+    }
+    const double bound = bound_mode ? std::sqrt(6.0 / N) : 1.0 / std::sqrt(static_cast<double>(N));
+    for (int c = 0; c < N; ++c) *q++ = static_cast<float>(uniform(-bound, bound));
+    *q = 0.0f;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params, int64_t n_params, int32_t device,
+                                    svn_model** out) {
+    svn_status st = validate_desc(d);
+    if (st != SVN_OK) return st;
+    if (!params || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "model: null params/out");
+    if (n_params != svn_param_count(d)) return fail(SVN_ERR_INVALID_ARGUMENT, "model: parameter count mismatch");
+    int ndev = 0;
+    SVN_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(SVN_ERR_INVALID_ARGUMENT, "model: no such CUDA device");
+    DeviceGuard guard(device);
+
+    auto m = new svn_model();
+    m->device = device;
+    m->L = d->n_layers;
+    m->N = d->width;
+    m->dof = d->dof;
+    m->in = 3 + 2 * d->dof;
+    m->layers.assign(d->layers, d->layers + d->n_layers);
+    cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
+    const int N = m->N, in = m->in, L = m->L, nq = 2 * m->dof;
+    FusedArgs& a = m->base;
+    a.L = L;
+    a.N = N;
+    a.dof = m->dof;
+    a.in = in;
+
+    // parse the parameter buffer (layout: include/sweptnet_b200.h)
+    const float* q = params;
+    for (int k = 0; k < in; ++k) a.shift[k] = q[k];
+    q += in;
+    for (int k = 0; k < in; ++k) a.scale[k] = q[k];
+    q += in;
+    std::vector<float> wq_host, mbbase_host;
+    auto cleanup_fail = [&](svn_status s) {
+        delete m;
+        return s;
+    };
+    for (int l = 0; l < L; ++l) {
+        const svn_layer& ly = m->layers[l];
+        const int K = layer_k(d->layers, l, N, in);
+        const float* W = q;  // column-major [N x K]: column k contiguous == row k of W^T
+        q += static_cast<int64_t>(N) * K;
+        const float* b = q;
+        q += N;
+        LayerDev& ld = a.layer[l];
+        ld.flags = (ly.concat || l == 0 ? kConcat : 0) | (ly.act ? kAct : 0) | (ly.affine ? kAffine : 0) |
+                   (ly.residual && l > 0 ? kResidual : 0);
+        float* dW = nullptr;
+        if ((st = m->upload(W, static_cast<size_t>(N) * K, &dW)) != SVN_OK) return cleanup_fail(st);
+        a.wt[l] = dW;
+        a.wt_rows[l] = K;
+        float* db = nullptr;
+        if ((st = m->upload(b, N, &db)) != SVN_OK) return cleanup_fail(st);
+        ld.bias = db;
+        ld.mb_slot = -1;
+        ld.wx = nullptr;
+        if (ld.flags & kConcat) {
+            const int xoff = (l == 0) ? 0 : N;
+            ld.wx = dW + static_cast<int64_t>(xoff) * N;  // rows x0, x1, x2 of W^T
+            ld.mb_slot = m->n_mb++;
+            wq_host.insert(wq_host.end(), W + static_cast<int64_t>(xoff + 3) * N,
+                           W + static_cast<int64_t>(xoff + 3 + nq) * N);
+            mbbase_host.insert(mbbase_host.end(), b, b + N);
+        }
+        ld.s = ld.t = nullptr;
+        if (ly.affine) {
+            const float *gamma = q, *beta = q + N, *mean = q + 2 * N, *var = q + 3 * N;
+            q += 4 * N;
+            // nn.cpp:108-110 in float: s = gamma / sqrt(var + eps); t = beta - mean * s
+            std::vector<float> s(N), t(N);
+            for (int i = 0; i < N; ++i) {
+                s[i] = gamma[i] / std::sqrt(var[i] + 1e-5f);
+                t[i] = std::fma(-mean[i], s[i], beta[i]);
+            }
+            float *ds = nullptr, *dt = nullptr;
+            if ((st = m->upload(s.data(), N, &ds)) != SVN_OK) return cleanup_fail(st);
+            if ((st = m->upload(t.data(), N, &dt)) != SVN_OK) return cleanup_fail(st);
+            ld.s = ds;
+            ld.t = dt;
+        }
+    }
+    {
+        float* dwo = nullptr;
+        if ((st = m->upload(q, N, &dwo)) != SVN_OK) return cleanup_fail(st);
+        a.wo = dwo;
+        a.bo = q[N];
+    }
+    if ((st = m->upload(wq_host.data(), wq_host.size(), &m->d_wq)) != SVN_OK) return cleanup_fail(st);
+    if ((st = m->upload(mbbase_host.data(), mbbase_host.size(), &m->d_mbbase)) != SVN_OK) return cleanup_fail(st);
+    a.n_mb = m->n_mb;
+
+    // bf16 tcgen05 weight stream for layers 1..L-1: h part only, per layer the
+    // quarter-steps (n-half, k-half) = (0,0) (1,0) (0,1) (1,1), each as K/2/64 chunks
+    // of (N/2 rows x 64 k) in the SW128 K-major image the MMA descriptors expect.
+    if (N == 256 || N == 512) {
+        const int NH = N / 2, KSL = NH / 64;
+        const size_t chunk_elems = static_cast<size_t>(NH) * 64;
+        std::vector<__nv_bfloat16> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * N * N);
+        const float* Wl = params + 2 * in;
+        size_t pos = 0;
+        for (int l = 0; l < L; ++l) {
+            const int K = layer_k(d->layers, l, N, in);
+            if (l > 0) {
+                for (int step = 0; step < 4; ++step) {
+                    const int nh = step & 1, kh = step >> 1;
+                    for (int ks = 0; ks < KSL; ++ks) {
+                        uint8_t* chunk = reinterpret_cast<uint8_t*>(ws.data() + pos);
+                        for (int nr = 0; nr < NH; ++nr)
+                            for (int kc = 0; kc < 64; ++kc) {
+                                const int n = nh * NH + nr, k = (kh * KSL + ks) * 64 + kc;
+                                const float w = Wl[static_cast<int64_t>(k) * N + n];
+                                *reinterpret_cast<__nv_bfloat16*>(chunk + sw128_offset(nr, kc, NH)) =
+                                    __float2bfloat16_rn(w);
+                            }
+                        pos += chunk_elems;
+                    }
+                }
+            }
+            Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+        }
+        __nv_bfloat16* dws = nullptr;
+        if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return cleanup_fail(st);
+        a.wstream = dws;
+        m->has_bf16 = true;
+    }
+    *out = m;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_model_destroy(svn_model* m) {
+    delete m;
+    return SVN_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+svn_status check_prec(const svn_model* m, svn_precision prec) {
+    if (prec == SVN_PREC_BF16) {
+        if (!m->has_bf16) return fail(SVN_ERR_UNSUPPORTED, "bf16 path needs width 256 or 512");
+    } else if (prec == SVN_PREC_FP32 || prec == SVN_PREC_FP32_EXACT) {
+        if (m->N != 128 && m->N != 256 && m->N != 512)
+            return fail(SVN_ERR_UNSUPPORTED, "fp32 path needs width 128, 256 or 512");
+    } else {
+        return fail(SVN_ERR_INVALID_ARGUMENT, "unknown precision");
+    }
+    return SVN_OK;
+}
+
+int tile_rows(svn_precision prec) { return prec == SVN_PREC_BF16 ? 128 : 64; }
+
+// Scratch buffers freed on the stream when the call's kernels are done.
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    cudaError_t alloc(void** p, size_t bytes) {
+        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+
+void ensure_pool(int device) {
+    static std::once_flag flags[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(flags[device], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t threshold = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+        }
+    });
+}
+
+cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaStream_t st) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_timing) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    cudaError_t e = prec == SVN_PREC_BF16 ? launch_fused_bf16(a, num_sms, st) : launch_fused_fp32(a, num_sms, st);
+    ++g_launches;
+    if (g_timing) {
+        cudaEventRecord(e1, st);
+        g_events.emplace_back(e0, e1);
+    }
+    return e;
+}
+
+// Shared body of the dense query (full result or keys-only partial).
+svn_status query_dense(const svn_model* m, svn_precision prec, const float* points, int64_t P, int64_t index_offset,
+                       const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
+                       uint8_t* free_out, float* per_point, uint64_t* keys_partial, cudaStream_t st) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    if (P + index_offset > 0xFFFFFFFFll) return fail(SVN_ERR_UNSUPPORTED, "query: more than 2^32 points");
+    svn_status s = check_prec(m, prec);
+    if (s != SVN_OK) return s;
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    FusedArgs a = m->base;
+    const bool exact = prec == SVN_PREC_FP32_EXACT;
+    a.exact = exact ? 1 : 0;
+    a.points = points;
+    a.point_stride = 3;
+    a.P = P;
+    a.q01 = q01;
+    a.M = M;
+    const int TM = tile_rows(prec);
+    a.tiles_per_motion = (P + TM - 1) / TM;
+    a.n_tiles = a.tiles_per_motion * M;
+    a.tiles = nullptr;
+    a.margin = margin;
+    a.per_point = per_point;
+    a.index_offset = index_offset;
+    Scratch sc(st);
+    float* mb = nullptr;
+    const int n_mb = exact ? 0 : m->n_mb;
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb), sizeof(float) * static_cast<size_t>(M) * (n_mb ? n_mb : 1) * m->N),
+             "cudaMallocAsync(motion_bias)");
+    a.motion_bias = mb;
+    a.n_mb = m->n_mb;  // slot stride stays the model's (exact mode never reads it)
+    unsigned long long* keys = nullptr;
+    unsigned int* counters = nullptr;
+    if (keys_partial) {
+        keys = reinterpret_cast<unsigned long long*>(keys_partial);
+    } else {
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&keys), sizeof(unsigned long long) * M), "cudaMallocAsync(keys)");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * M), "cudaMallocAsync(counters)");
+    }
+    a.keys = keys;
+    a.counters = counters;
+    a.min_out = min_out;
+    a.argmin_out = argmin_out;
+    a.free_out = free_out;
+    {
+        FusedArgs k0 = a;
+        k0.n_mb = n_mb;
+        SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, keys_partial ? nullptr : keys, counters,
+                                    keys_partial ? 0 : M, st),
+                 "motion_bias kernel");
+        ++g_launches;
+    }
+    SVN_CUDA(launch_k1(a, prec, m->num_sms, st), "fused MLP kernel");
+    return SVN_OK;
+}
+
+cudaStream_t thread_stream(int device) {
+    thread_local cudaStream_t streams[64] = {};
+    if (device < 0 || device >= 64) return nullptr;
+    if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
+    return streams[device];
+}
+
+}  // namespace
+
+extern "C" {
+
+SVN_API svn_status svn_query_min_device(const svn_model* m, svn_precision prec, const float* points, int64_t P,
+                                        const float* q01, int64_t M, double margin, float* min_out,
+                                        int32_t* argmin_out, uint8_t* free_out, float* per_point, void* stream) {
+    if (!min_out || !argmin_out || !free_out) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null output");
+    return query_dense(m, prec, points, P, 0, q01, M, margin, min_out, argmin_out, free_out, per_point, nullptr,
+                       static_cast<cudaStream_t>(stream));
+}
+
+SVN_API svn_status svn_keys_init_device(uint64_t* keys, int64_t M, void* stream) {
+    SVN_CUDA(launch_keys_init(reinterpret_cast<unsigned long long*>(keys), M, static_cast<cudaStream_t>(stream)),
+             "keys_init kernel");
+    ++g_launches;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_query_min_keys_device(const svn_model* m, svn_precision prec, const float* points, int64_t P,
+                                             int64_t index_offset, const float* q01, int64_t M, uint64_t* keys,
+                                             void* stream) {
+    if (!keys) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null keys");
+    return query_dense(m, prec, points, P, index_offset, q01, M, 0.0, nullptr, nullptr, nullptr, nullptr, keys,
+                       static_cast<cudaStream_t>(stream));
+}
+
+SVN_API svn_status svn_keys_finalize_device(const uint64_t* keys, int64_t M, double margin, float* min_out,
+                                            int32_t* argmin_out, uint8_t* free_out, void* stream) {
+    SVN_CUDA(launch_keys_finalize(reinterpret_cast<const unsigned long long*>(keys), M, margin, min_out, argmin_out,
+                                  free_out, static_cast<cudaStream_t>(stream)),
+             "keys_finalize kernel");
+    ++g_launches;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const float* points, int64_t P,
+                                 const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
+                                 uint8_t* free_out, float* per_point) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    if (!points || !q01 || !min_out || !argmin_out || !free_out)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    const int nq = 2 * m->dof;
+    svn_status s;
+    {
+        Scratch sc(st);
+        float *dp = nullptr, *dq = nullptr, *dmin = nullptr, *dpp = nullptr;
+        int32_t* darg = nullptr;
+        uint8_t* dfree = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * P), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * nq * M), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dmin), sizeof(float) * M), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&darg), sizeof(int32_t) * M), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dfree), M), "cudaMallocAsync");
+        if (per_point)
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(dp, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
+        SVN_CUDA(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions");
+        s = query_dense(m, prec, dp, P, 0, dq, M, margin, dmin, darg, dfree, dpp, nullptr, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(min_out, dmin, sizeof(float) * M, cudaMemcpyDeviceToHost, st), "D2H min");
+        SVN_CUDA(cudaMemcpyAsync(argmin_out, darg, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st), "D2H argmin");
+        SVN_CUDA(cudaMemcpyAsync(free_out, dfree, M, cudaMemcpyDeviceToHost, st), "D2H free");
+        if (per_point)
+            SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
+    }
+    SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+    return SVN_OK;
+}
+
+// forward_eval (nn.cpp:95-130).  Consecutive rows with identical (q0, q1) form one
+// motion segment; each segment is cut into tiles of one motion.
+static svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw_host, const float* raw_dev,
+                               int64_t B, int64_t cols, float* out_dev, cudaStream_t st) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+    svn_status s = check_prec(m, prec);
+    if (s != SVN_OK) return s;
+    const int nq = 2 * m->dof, TM = tile_rows(prec);
+    std::vector<float> qseg;
+    std::vector<TileDesc> tiles;
+    int64_t seg_start = 0;
+    int32_t nseg = 0;
+    for (int64_t r = 1; r <= B; ++r) {
+        const bool cut = (r == B) || std::memcmp(raw_host + r * cols + 3, raw_host + (r - 1) * cols + 3,
+                                                 sizeof(float) * nq) != 0;
+        if (!cut) continue;
+        qseg.insert(qseg.end(), raw_host + seg_start * cols + 3, raw_host + seg_start * cols + 3 + nq);
+        for (int64_t t0 = seg_start; t0 < r; t0 += TM) {
+            const int64_t n = (r - t0) < TM ? (r - t0) : TM;
+            tiles.push_back(TileDesc{t0, t0, nseg, static_cast<int32_t>(n)});
+        }
+        ++nseg;
+        seg_start = r;
+    }
+    FusedArgs a = m->base;
+    a.exact = prec == SVN_PREC_FP32_EXACT ? 1 : 0;
+    a.points = raw_dev;
+    a.point_stride = cols;
+    a.P = B;
+    a.M = nseg;
+    a.n_tiles = static_cast<int64_t>(tiles.size());
+    a.tiles_per_motion = 1;
+    a.per_point = out_dev;
+    a.keys = nullptr;
+    a.counters = nullptr;
+    Scratch sc(st);
+    float *dq = nullptr, *mb = nullptr;
+    TileDesc* dt = nullptr;
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * qseg.size()), "cudaMallocAsync");
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dt), sizeof(TileDesc) * tiles.size()), "cudaMallocAsync");
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb), sizeof(float) * static_cast<size_t>(nseg) * (m->n_mb ? m->n_mb : 1) * m->N),
+             "cudaMallocAsync");
+    SVN_CUDA(cudaMemcpyAsync(dq, qseg.data(), sizeof(float) * qseg.size(), cudaMemcpyHostToDevice, st), "H2D q");
+    SVN_CUDA(cudaMemcpyAsync(dt, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice, st), "H2D tiles");
+    a.q01 = dq;
+    a.tiles = dt;
+    a.motion_bias = mb;
+    {
+        FusedArgs k0 = a;
+        k0.n_mb = a.exact ? 0 : m->n_mb;
+        SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, nullptr, nullptr, 0, st), "motion_bias kernel");
+        ++g_launches;
+    }
+    SVN_CUDA(launch_k1(a, prec, m->num_sms, st), "fused MLP kernel");
+    // keep the host tile/q vectors alive until the async copies have consumed them
+    SVN_CUDA(cudaStreamSynchronize(st), "forward kernels");
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_forward_eval(const svn_model* m, svn_precision prec, const float* raw, int64_t B, int64_t cols,
+                                    float* out) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+    if (!raw || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null buffer");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    float *draw = nullptr, *dout = nullptr;
+    {
+        Scratch sc(st);
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&draw), sizeof(float) * B * cols), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dout), sizeof(float) * B), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(draw, raw, sizeof(float) * B * cols, cudaMemcpyHostToDevice, st), "H2D raw");
+        svn_status s = forward_rows(m, prec, raw, draw, B, cols, dout, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * B, cudaMemcpyDeviceToHost, st), "D2H out");
+    }
+    SVN_CUDA(cudaStreamSynchronize(st), "forward");
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_forward_eval_device(const svn_model* m, svn_precision prec, const float* raw, int64_t B,
+                                           int64_t cols, float* out, void* stream) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // segmenting needs the q columns on the host
+    std::vector<float> host(static_cast<size_t>(B * cols));
+    SVN_CUDA(cudaMemcpyAsync(host.data(), raw, sizeof(float) * B * cols, cudaMemcpyDeviceToHost, st), "D2H raw");
+    SVN_CUDA(cudaStreamSynchronize(st), "D2H raw");
+    return forward_rows(m, prec, host.data(), raw, B, cols, out, st);
+}
+
+SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision prec, const double* cloud, int64_t P,
+                                            const double* q0, const double* q1, int32_t dof, double* min_out,
+                                            int32_t* argmin_out) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (3 + 2 * dof != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: motion dof does not match model");
+    if (!cloud || !q0 || !q1 || !min_out || !argmin_out)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null buffer");
+    // nn.cpp:469-473: every coordinate and joint value is cast to float
+    std::vector<float> pts(static_cast<size_t>(3 * P)), q(static_cast<size_t>(2 * dof));
+    for (int64_t i = 0; i < 3 * P; ++i) pts[i] = static_cast<float>(cloud[i]);
+    for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
+    for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+    float mn = 0.f;
+    int32_t idx = 0;
+    uint8_t fr = 0;
+    svn_status s = svn_query_min(m, prec, pts.data(), P, q.data(), 1, 0.0, &mn, &idx, &fr, nullptr);
+    if (s != SVN_OK) return s;
+    *min_out = static_cast<double>(mn);
+    *argmin_out = idx;
+    return SVN_OK;
+}
+
+// SVCKPT01 (nn.cpp:482-576): magic, u32 {version, n_blocks, block_dim, input_dim},
+// then the Fig. 2 parameter body; strict trailing-byte check.
+SVN_API svn_status svn_model_load_checkpoint(const char* path, int32_t device, svn_model** out) {
+    if (!path || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "load_checkpoint: null argument");
+    const std::string p(path);
+    FILE* f = std::fopen(path, "rb");
+    if (!f) return fail(SVN_ERR_IO, "cannot open checkpoint: " + p);
+    char magic[8];
+    if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, "SVCKPT01", 8) != 0) {
+        std::fclose(f);
+        return fail(SVN_ERR_FORMAT, p + ": not a sweptnet checkpoint");
+    }
+    uint32_t hdr[4];
+    if (std::fread(hdr, sizeof(uint32_t), 4, f) != 4) {
+        std::fclose(f);
+        return fail(SVN_ERR_TRUNCATION, p + ": file ends inside header");
+    }
+    if (hdr[0] != 1u) {
+        std::fclose(f);
+        return fail(SVN_ERR_VERSION, p + ": checkpoint version " + std::to_string(hdr[0]) +
+                                         " not supported (expected 1)");
+    }
+    const int n_blocks = static_cast<int>(hdr[1]), block_dim = static_cast<int>(hdr[2]),
+              input_dim = static_cast<int>(hdr[3]);
+    if (n_blocks < 1 || block_dim < 1 || input_dim < 5 || (input_dim - 3) % 2 != 0 || n_blocks + 1 > kMaxLayers ||
+        input_dim > kMaxIn) {
+        std::fclose(f);
+        return fail(SVN_ERR_FORMAT, p + ": implausible architecture header");
+    }
+    std::vector<svn_layer> layers(static_cast<size_t>(n_blocks + 1), svn_layer{1, 1, 1, 1});
+    layers[0] = svn_layer{1, 0, 0, 0};
+    svn_model_desc d{n_blocks + 1, block_dim, (input_dim - 3) / 2, layers.data()};
+    const int64_t n = svn_param_count(&d);
+    std::vector<float> params(static_cast<size_t>(n));
+    if (std::fread(params.data(), sizeof(float), static_cast<size_t>(n), f) != static_cast<size_t>(n)) {
+        std::fclose(f);
+        return fail(SVN_ERR_TRUNCATION, p + ": file ends inside tensor data");
+    }
+    char extra;
+    const bool trailing = std::fread(&extra, 1, 1, f) == 1;
+    std::fclose(f);
+    if (trailing) return fail(SVN_ERR_FORMAT, p + ": trailing bytes after parameters");
+    return svn_model_create(&d, params.data(), n, device, out);
+}
+
+}  // extern "C"
