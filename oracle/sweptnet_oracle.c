@@ -394,18 +394,20 @@ OR_API int oracle_predict_min_distance(const int* flags, int L, int N, int dof, 
 /* ---------------------------------------------- batched query (baseline) -- */
 /* Every (point x motion) pair, per-motion min/argmin and `double(min) > margin`
  * (collision.cpp:68).  points: float [P x 3]; q01: float [M x 2dof] = [q0 | q1].
- * per_point (nullable): float [M x P].  Motions are split over `threads`
- * workers with the contiguous partition of parallel.cpp:33-41. */
+ * per_point (nullable): float [M x P].  Work items are (motion, point chunk); a
+ * motion is cut into chunks only when there are fewer motions than threads.  Items
+ * are split over `threads` workers with the contiguous partition of
+ * parallel.cpp:33-41; chunk results are merged in ascending chunk order with the
+ * same strict '<' as nn.cpp:476-478, so the answer does not depend on `threads`. */
 typedef struct {
     const model_f32* m;
     const float* pts;
     int64_t P;
     const float* q01;
-    int64_t m0, m1;
-    double margin;
-    float* min_out;
-    int32_t* argmin_out;
-    uint8_t* free_out;
+    int64_t nchunk, chunk_len;
+    int64_t i0, i1; /* item range */
+    float* best_v;  /* [items] */
+    int32_t* best;  /* [items] */
     float* per_point;
 } qjob_t;
 
@@ -415,27 +417,26 @@ static void* query_worker(void* arg) {
     const int in = m->in, dof = (in - 3) / 2, N = m->N;
     float* raw = (float*)malloc(sizeof(float) * (size_t)in);
     float* scratch = (float*)malloc(sizeof(float) * (size_t)(in + 2 * N));
-    for (int64_t mi = j->m0; mi < j->m1; ++mi) {
+    for (int64_t it = j->i0; it < j->i1; ++it) {
+        const int64_t mi = it / j->nchunk, c = it % j->nchunk;
+        const int64_t r0 = c * j->chunk_len;
+        const int64_t r1 = r0 + j->chunk_len < j->P ? r0 + j->chunk_len : j->P;
         memcpy(raw + 3, j->q01 + mi * 2 * dof, sizeof(float) * 2 * (size_t)dof);
         float best_v = 0.0f;
-        int32_t best = 0;
-        for (int64_t r = 0; r < j->P; ++r) {
+        int32_t best = -1;
+        for (int64_t r = r0; r < r1; ++r) {
             raw[0] = j->pts[3 * r];
             raw[1] = j->pts[3 * r + 1];
             raw[2] = j->pts[3 * r + 2];
             const float v = forward_row_f32(m, raw, scratch, scratch + in, scratch + in + N);
             if (j->per_point) j->per_point[mi * j->P + r] = v;
-            if (r == 0) {
-                best_v = v;
-                best = 0;
-            } else if (v < best_v) {
+            if (best < 0 || v < best_v) {
                 best_v = v;
                 best = (int32_t)r;
             }
         }
-        j->min_out[mi] = best_v;
-        j->argmin_out[mi] = best;
-        j->free_out[mi] = (double)best_v > j->margin ? 1 : 0;
+        j->best_v[it] = best_v;
+        j->best[it] = best;
     }
     free(raw);
     free(scratch);
@@ -448,25 +449,45 @@ OR_API int oracle_query_min(const int* flags, int L, int N, int dof, const float
     if (P < 1 || M < 1) return 1;
     model_f32 m;
     if (model_bind_f32(&m, flags, L, N, dof, params)) return 1;
-    int64_t workers = threads < 1 ? 1 : threads;
-    if (workers > M) workers = M;
-    const int64_t chunk = (M + workers - 1) / workers;
+    const int64_t T = threads < 1 ? 1 : threads;
+    int64_t nchunk = M >= T ? 1 : (T + M - 1) / M;
+    if (nchunk > P) nchunk = P;
+    const int64_t chunk_len = (P + nchunk - 1) / nchunk;
+    nchunk = (P + chunk_len - 1) / chunk_len;
+    const int64_t items = M * nchunk;
+    float* bv = (float*)malloc(sizeof(float) * (size_t)items);
+    int32_t* bi = (int32_t*)malloc(sizeof(int32_t) * (size_t)items);
+    int64_t workers = T < items ? T : items;
+    const int64_t per = (items + workers - 1) / workers;
     qjob_t* jobs = (qjob_t*)calloc((size_t)workers, sizeof(qjob_t));
     pthread_t* tid = (pthread_t*)calloc((size_t)workers, sizeof(pthread_t));
     int64_t launched = 0;
     for (int64_t w = 0; w < workers; ++w) {
-        const int64_t b = w * chunk, e = b + chunk < M ? b + chunk : M;
+        const int64_t b = w * per, e = b + per < items ? b + per : items;
         if (b >= e) break;
-        jobs[w] = (qjob_t){&m, pts, P, q01, b, e, margin, min_out, argmin_out, free_out, per_point};
-        if (workers == 1) {
+        jobs[w] = (qjob_t){&m, pts, P, q01, nchunk, chunk_len, b, e, bv, bi, per_point};
+        if (workers == 1)
             query_worker(&jobs[w]);
-        } else {
+        else
             pthread_create(&tid[w], NULL, query_worker, &jobs[w]);
-        }
         ++launched;
     }
     if (workers > 1)
         for (int64_t w = 0; w < launched; ++w) pthread_join(tid[w], NULL);
+    for (int64_t mi = 0; mi < M; ++mi) {
+        float best_v = bv[mi * nchunk];
+        int32_t best = bi[mi * nchunk];
+        for (int64_t c = 1; c < nchunk; ++c)
+            if (bv[mi * nchunk + c] < best_v) {
+                best_v = bv[mi * nchunk + c];
+                best = bi[mi * nchunk + c];
+            }
+        min_out[mi] = best_v;
+        argmin_out[mi] = best;
+        free_out[mi] = (double)best_v > margin ? 1 : 0;
+    }
+    free(bv);
+    free(bi);
     free(jobs);
     free(tid);
     free(m.fold);

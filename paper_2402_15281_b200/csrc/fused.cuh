@@ -17,6 +17,7 @@ struct LayerDev {
     const float* wx;    // [3][N] fp32 x-part columns (concat layers), SoA
     int flags;          // kConcat | kAct | kAffine | kResidual
     int mb_slot;        // slot in the per-motion bias buffer, -1 if none
+    int bias_zero;      // 1: every b_l == 0 and no folded motion bias (the add is skipped)
 };
 
 // One unit of work: `nrows` consecutive rows of one motion.

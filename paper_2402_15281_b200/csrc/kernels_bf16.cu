@@ -61,6 +61,37 @@ __device__ __forceinline__ void epi_chunk(const FusedArgs& a, const LayerDev& ld
     const bool concat = (l == 0) || (ld.flags & kConcat);
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (!concat && !aff && !res && !last) {
+        // fast path (plain hidden layer): [+ bias] -> ReLU fused into the bf16 pack -> smem
+        if (!ld.bias_zero) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
+                v[i + 0] += b.x;
+                v[i + 1] += b.y;
+                v[i + 2] += b.z;
+                v[i + 3] += b.w;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4 p;
+            if (act) {
+                p.x = pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]);
+                p.y = pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]);
+                p.z = pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]);
+                p.w = pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]);
+            } else {
+                p.x = pack_bf16(v[8 * u + 0], v[8 * u + 1]);
+                p.y = pack_bf16(v[8 * u + 2], v[8 * u + 3]);
+                p.z = pack_bf16(v[8 * u + 4], v[8 * u + 5]);
+                p.w = pack_bf16(v[8 * u + 6], v[8 * u + 7]);
+            }
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, 128)) = p;
+        }
+        return;
+    }
+    if (!ld.bias_zero) {
 #pragma unroll
     for (int i = 0; i < 32; i += 4) {
         const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c0 + i));
@@ -68,6 +99,7 @@ __device__ __forceinline__ void epi_chunk(const FusedArgs& a, const LayerDev& ld
         v[i + 1] += b.y;
         v[i + 2] += b.z;
         v[i + 3] += b.w;
+    }
     }
     if (concat) {
         const float* wx = ld.wx;
@@ -258,16 +290,19 @@ __global__ void __launch_bounds__(Bf16Cfg<N>::THREADS, 1) fused_bf16_kernel(cons
                         tc_fence_after();
                     }
 #pragma unroll 1
-                    for (int cc = 0; cc < C::CPT; ++cc) {
+                    for (int cc = 0; cc < C::CPT; cc += 2) {
                         const int c0 = j * C::NH + ch * (C::NH / 2) + cc * 32;
-                        float v[32];
+                        float v[64];
                         if (l > 0) {
-                            tmem_ld32(tmem + t_lane + static_cast<uint32_t>(c0), v);
+                            tmem_ld64(tmem + t_lane + static_cast<uint32_t>(c0), v);
                         } else {
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+                            for (int i = 0; i < 64; ++i) v[i] = 0.f;
                         }
-                        epi_chunk<N>(a, ld, l, last, bias, v, c0, row, z0, z1, z2, A, dot);
+                        epi_chunk<N>(a, ld, l, last, bias, *reinterpret_cast<float(*)[32]>(&v[0]), c0, row, z0,
+                                     z1, z2, A, dot);
+                        epi_chunk<N>(a, ld, l, last, bias, *reinterpret_cast<float(*)[32]>(&v[32]), c0 + 32, row,
+                                     z0, z1, z2, A, dot);
                     }
                     if (!last) {
                         tc_fence_before();

@@ -253,11 +253,15 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         if ((st = m->upload(b, N, &db)) != SVN_OK) return cleanup_fail(st);
         ld.bias = db;
         ld.mb_slot = -1;
+        ld.bias_zero = 1;
+        for (int i = 0; i < N; ++i)
+            if (b[i] != 0.0f) ld.bias_zero = 0;
         ld.wx = nullptr;
         if (ld.flags & kConcat) {
             const int xoff = (l == 0) ? 0 : N;
             ld.wx = dW + static_cast<int64_t>(xoff) * N;  // rows x0, x1, x2 of W^T
             ld.mb_slot = m->n_mb++;
+            ld.bias_zero = 0;
             wq_host.insert(wq_host.end(), W + static_cast<int64_t>(xoff + 3) * N,
                            W + static_cast<int64_t>(xoff + 3 + nq) * N);
             mbbase_host.insert(mbbase_host.end(), b, b + N);
