@@ -1,6 +1,7 @@
 // fused.cuh — launch parameters shared by the host ABI and the device kernels.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace svn {
@@ -18,6 +19,8 @@ struct LayerDev {
     int flags;          // kConcat | kAct | kAffine | kResidual
     int mb_slot;        // slot in the per-motion bias buffer, -1 if none
     int bias_zero;      // 1: every b_l == 0 and no folded motion bias (the add is skipped)
+    int ext;            // bf16 pair kernel: K=16 extension slab 0 none, 1 model-constant, 2 per-motion
+    int64_t ext_row;    // ext == 1: first 32-byte row of this layer in the model extension stream
 };
 
 // One unit of work: `nrows` consecutive rows of one motion.
@@ -29,6 +32,10 @@ struct TileDesc {
 };
 
 struct FusedArgs {
+    // TMA descriptors (bf16 CTA-pair kernel): blobs of pre-arranged smem images
+    alignas(64) CUtensorMap tmap_w;   // weight stream viewed as [rows][128 B]
+    alignas(64) CUtensorMap tmap_xm;  // model extension stream [rows][32 B]
+    alignas(64) CUtensorMap tmap_xq;  // per-motion extension stream [rows][32 B]
     // model
     int L, N, dof, in;
     LayerDev layer[kMaxLayers];
@@ -140,5 +147,9 @@ cudaError_t launch_keys_finalize(const unsigned long long* keys, int64_t M, doub
                                  int32_t* argmin_out, uint8_t* free_out, cudaStream_t st);
 cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_fused_bf16(const FusedArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
+                              uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,
+                              int64_t n_keys, cudaStream_t st);
 
 }  // namespace svn

@@ -1,0 +1,497 @@
+// kernels_bf16_pair.cu — K1 (bf16): the fused swept-volume MLP on a CTA pair.
+//
+// Replaces, for a 256-point tile of one motion, the row loop of forward_eval
+// (/root/reference/proj/src/nn.cpp:116-128), the argmin of predict_min_distance
+// (nn.cpp:476-478) and the margin predicate (collision.cpp:68).
+//
+// Layout of the work: a cluster of 2 CTAs on one TPC issues tcgen05.mma.cta_group::2
+// with M = 256 (128 rows per CTA), N = width/2 (one output half), K = 16.  Each CTA
+// holds its 128 activation rows (bf16, SW128 K-major, the A operand) and half of each
+// weight chunk (B operand); both are fed by TMA (cp.async.bulk.tensor ... cta_group::2)
+// whose completion is counted on the leader CTA's mbarrier.  The accumulator for a
+// whole layer (128 x width fp32 per CTA) lives in TMEM.
+//
+// Every affine term of a layer that is not the width x width product is computed by
+// the tensor core too, as one extra K=16 "extension" slab: A_ext row = (1, 1, z_x in
+// bf16 hi/lo splits), B_ext row = (b_hi, b_lo, W_x in bf16 hi/lo splits), giving the
+// (per-motion folded) bias and the x-part to ~2^-16 relative.  Layer 0 is the extension
+// alone.  The epilogue therefore only does ReLU (fused into the bf16 pack) and the
+// store of the next layer's A operand — or, on the last layer, the output dot.
+//
+// Warps (per CTA): 0 TMA producer, 1 TMEM owner + MMA issuer (leader CTA only),
+// 2..9 epilogue (two warps per TMEM lane quadrant, each owning half of every
+// output half).  A layer runs as quarter steps (n-half, k-half) in the order
+// (0,0) (1,0) (0,1) (1,1); the epilogue of output half 0 overlaps step (1,1), that
+// of half 1 overlaps step (0,0) of the next layer.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "fused.cuh"
+#include "ptx.cuh"
+
+namespace svn {
+
+template <int N>
+struct PairCfg {
+    static constexpr int TM = 128;                   // rows per CTA (pair tile = 256)
+    static constexpr int NH = N / 2;                 // MMA N = one output half
+    static constexpr int BR = NH / 2;                // B rows per CTA per chunk
+    static constexpr int KSL = NH / 64;              // 64-wide K slabs per k-half
+    static constexpr uint32_t A_SLAB = TM * 128;     // 16 KiB
+    static constexpr uint32_t A_BYTES = TM * N * 2;
+    static constexpr uint32_t AX_BYTES = TM * 32;    // K=16 extension of A (4 KiB)
+    static constexpr uint32_t CHUNK = BR * 128;      // per-CTA main weight chunk
+    static constexpr uint32_t XCHUNK = BR * 32;      // per-CTA extension chunk
+    static constexpr int STAGES = N >= 512 ? 4 : 8;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int THREADS = 64 + EPI_WARPS * 32;
+    static constexpr int COLS = NH / 2;              // columns per epilogue thread per half
+    static constexpr uint32_t OFF_AX = A_BYTES;
+    static constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
+    static constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * CHUNK;
+    static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
+    static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
+    static constexpr uint32_t SMEM = OFF_BAR + 256;
+    static_assert(SMEM <= 232448, "shared memory budget");
+    static_assert(COLS % 64 == 0, "epilogue works in 64-column TMEM loads");
+};
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&p);
+}
+
+__device__ __forceinline__ float bflo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bfhi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+// bf16 hi/lo split of x: hi = bf16(x), lo = bf16(x - hi).
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(x);
+    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+// Write this row's A extension: (1, 1, z0h, z0h, z0l, z1h, z1h, z1l, z2h, z2h, z2l, 0...).
+__device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, float z1, float z2) {
+    __nv_bfloat16 h0, l0, h1, l1, h2, l2;
+    split_bf16(z0, h0, l0);
+    split_bf16(z1, h1, l1);
+    split_bf16(z2, h2, l2);
+    const __nv_bfloat16 one = __float2bfloat16_rn(1.0f), zero = __float2bfloat16_rn(0.0f);
+    __align__(16) __nv_bfloat16 v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
+    *reinterpret_cast<uint4*>(ax + ext_offset(row, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
+    *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+}
+
+// Epilogue of 32 columns of one row (the MMA already added bias and x-part).
+template <int N>
+__device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
+                                           uint8_t* A, const float* wo_s, float& dot) {
+    const int fl = ld.flags;
+    const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (!aff && !res && !last) {  // hidden layer: ReLU fused into the bf16 pack
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4 p;
+            if (act) {
+                p.x = pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]);
+                p.y = pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]);
+                p.z = pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]);
+                p.w = pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]);
+            } else {
+                p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
+                p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
+                p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
+                p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+            }
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, 128)) = p;
+        }
+        return;
+    }
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+    }
+    if (aff) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 s = __ldg(reinterpret_cast<const float4*>(ld.s + c0 + i));
+            const float4 t = __ldg(reinterpret_cast<const float4*>(ld.t + c0 + i));
+            v[i + 0] = fmaf(v[i + 0], s.x, t.x);
+            v[i + 1] = fmaf(v[i + 1], s.y, t.y);
+            v[i + 2] = fmaf(v[i + 2], s.z, t.z);
+            v[i + 3] = fmaf(v[i + 3], s.w, t.w);
+        }
+    }
+    if (res) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint4 o = *reinterpret_cast<const uint4*>(A + sw128_offset(row, c0 + 8 * u, 128));
+            v[8 * u + 0] += bflo(o.x);
+            v[8 * u + 1] += bfhi(o.x);
+            v[8 * u + 2] += bflo(o.y);
+            v[8 * u + 3] += bfhi(o.y);
+            v[8 * u + 4] += bflo(o.z);
+            v[8 * u + 5] += bfhi(o.z);
+            v[8 * u + 6] += bflo(o.w);
+            v[8 * u + 7] += bfhi(o.w);
+        }
+    }
+    if (last) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+            dot = fmaf(w.x, v[i + 0], dot);
+            dot = fmaf(w.y, v[i + 1], dot);
+            dot = fmaf(w.z, v[i + 2], dot);
+            dot = fmaf(w.w, v[i + 3], dot);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4 p;
+            p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
+            p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
+            p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
+            p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, 128)) = p;
+        }
+    }
+}
+
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS, 1)
+    fused_bf16_pair_kernel(const __grid_constant__ FusedArgs a) {
+    using C = PairCfg<N>;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* A = smem;
+    uint8_t* AX = smem + C::OFF_AX;  // [2][AX_BYTES]
+    uint8_t* stages = smem + C::OFF_STAGE;
+    float* wo_s = reinterpret_cast<float*>(smem + C::OFF_WO);
+    float* dotbuf = reinterpret_cast<float*>(smem + C::OFF_DOT);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+    uint64_t* full = bars;                      // [STAGES] leader: TMA bytes of both CTAs
+    uint64_t* empty = full + C::STAGES;         // [STAGES] each CTA: slot consumed (MMA commit)
+    uint64_t* d_full = empty + C::STAGES;       // [2] each CTA: output half j in TMEM
+    uint64_t* a_ready = d_full + 2;             // [2] leader: epilogues of half j done (16 warps)
+    uint64_t* ax_full = a_ready + 2;            // [2] leader: A extension buffer b written (16 warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ax_full + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int L = a.L;
+    const int64_t pair = blockIdx.x >> 1;
+    const int64_t npairs = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(&d_full[j], 1);
+            mbar_init(&a_ready[j], 2 * C::EPI_WARPS);
+            mbar_init(&ax_full[j], 2 * C::EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) wo_s[i] = a.wo[i];
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&a.tmap_w);
+        prefetch_tmap(&a.tmap_xm);
+        prefetch_tmap(&a.tmap_xq);
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, N);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- producer --
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            const uint32_t full0 = mapa_shared(smem_u32(full), 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            auto slot = [&](uint32_t bytes_one_cta) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                if (rank == 0) mbar_arrive_expect_tx_local(&full[stage], 2 * bytes_one_cta);
+            };
+            auto advance = [&]() {
+                if (++stage == C::STAGES) stage = 0, phase ^= 1u;
+            };
+            for (int64_t t = pair; t < a.n_tiles; t += npairs) {
+                int32_t motion, nrows;
+                int64_t pbase, obase;
+                tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+                int64_t wrow = 0;  // 128-byte row of the weight stream
+                for (int l = 0; l < L; ++l) {
+                    const LayerDev& ld = a.layer[l];
+                    const int steps = l == 0 ? 2 : 4;
+                    for (int step = 0; step < steps; ++step) {
+                        const int nh = step & 1, kh = step >> 1;
+                        if (kh == 0 && ld.ext) {
+                            slot(C::XCHUNK);
+                            const uint32_t fb = full0 + stage * 8u;
+                            uint8_t* dst = stages + stage * C::CHUNK;
+                            if (ld.ext == 2) {
+                                const int64_t blob = ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
+                                tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * C::BR), fb, pol);
+                            } else {
+                                const int64_t r0 = ld.ext_row + (nh * 2 + rank) * C::BR;
+                                tma_load_2d_pair(dst, &a.tmap_xm, 0, static_cast<int32_t>(r0), fb, pol);
+                            }
+                            advance();
+                        }
+                        if (l > 0) {
+                            for (int ks = 0; ks < C::KSL; ++ks) {
+                                slot(C::CHUNK);
+                                tma_load_2d_pair(stages + stage * C::CHUNK, &a.tmap_w, 0,
+                                                 static_cast<int32_t>(wrow + rank * C::BR), full0 + stage * 8u, pol);
+                                wrow += C::NH;
+                                advance();
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------------- MMA issuer --
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_bf16(2 * C::TM, C::NH);
+            const uint32_t a_base = smem_u32(A), s_base = smem_u32(stages), ax_base = smem_u32(AX);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
+            int64_t k = 0;  // local tile counter
+            for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+                const int b = static_cast<int>(k & 1);
+                mbar_wait_cluster(&ax_full[b], ax_ph[b]);
+                ax_ph[b] ^= 1u;
+                for (int l = 0; l < L; ++l) {
+                    const LayerDev& ld = a.layer[l];
+                    const int steps = l == 0 ? 2 : 4;
+                    for (int step = 0; step < steps; ++step) {
+                        const int nh = step & 1, kh = step >> 1;
+                        if (kh == 0 && (k > 0 || l > 0)) {  // D[nh] drained / A[k-half nh] written
+                            mbar_wait_cluster(&a_ready[nh], ar_ph[nh]);
+                            ar_ph[nh] ^= 1u;
+                        }
+                        tc_fence_after();
+                        const uint32_t d_addr = tmem + static_cast<uint32_t>(nh * C::NH);
+                        bool acc = false;
+                        if (kh == 0 && ld.ext) {
+                            mbar_wait(&full[stage], phase);
+                            tc_fence_after();
+                            mma_bf16_pair(d_addr, noswz_desc(ax_base + b * C::AX_BYTES, 128, 256),
+                                          noswz_desc(s_base + stage * C::CHUNK, 128, 256), idesc, 0u);
+                            mma_commit_pair(&empty[stage], 3);
+                            if (++stage == C::STAGES) stage = 0, phase ^= 1u;
+                            acc = true;
+                        }
+                        if (l > 0) {
+                            for (int ks = 0; ks < C::KSL; ++ks) {
+                                mbar_wait(&full[stage], phase);
+                                tc_fence_after();
+                                const uint32_t a_slab = a_base + static_cast<uint32_t>(kh * C::KSL + ks) * C::A_SLAB;
+                                const uint32_t b_stage = s_base + static_cast<uint32_t>(stage) * C::CHUNK;
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk) {
+                                    mma_bf16_pair(d_addr, sw128_desc(a_slab + kk * 32), sw128_desc(b_stage + kk * 32),
+                                                  idesc, (acc || kh || ks || kk) ? 1u : 0u);
+                                }
+                                mma_commit_pair(&empty[stage], 3);
+                                if (++stage == C::STAGES) stage = 0, phase ^= 1u;
+                            }
+                        }
+                        if (l == 0) mma_commit_pair(&d_full[nh], 3);
+                        else if (step >= 2) mma_commit_pair(&d_full[step - 2], 3);
+                    }
+                }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue --
+        const int e = warp - 2;
+        const uint32_t quad = static_cast<uint32_t>(warp & 3);
+        const int ch = e >> 2;
+        const uint32_t row = quad * 32 + lane;  // row within this CTA's 128
+        const uint32_t t_lane = (quad * 32u) << 16;
+        const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
+        const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
+        uint32_t dp[2] = {0u, 0u};
+        auto write_ax_tile = [&](int64_t t, int b) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+            const int32_t r = static_cast<int32_t>(rank * C::TM + row);
+            const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
+            if (ch == 0) {
+                const float z0 = (xp[0] - a.shift[0]) * a.scale[0];
+                const float z1 = (xp[1] - a.shift[1]) * a.scale[1];
+                const float z2 = (xp[2] - a.shift[2]) * a.scale[2];
+                write_ax(AX + b * C::AX_BYTES, row, z0, z1, z2);
+                fence_proxy_async_smem();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(ax_full0 + b * 8u);
+        };
+        int64_t k = 0;
+        if (pair < a.n_tiles) write_ax_tile(pair, 0);
+        for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+            if (t + npairs < a.n_tiles) write_ax_tile(t + npairs, static_cast<int>((k + 1) & 1));
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+            const int32_t rr = static_cast<int32_t>(rank * C::TM + row);
+            const bool valid = rr < nrows;
+            float dot = 0.f;
+            for (int l = 0; l < L; ++l) {
+                const LayerDev& ld = a.layer[l];
+                const bool last = (l == L - 1);
+                for (int j = 0; j < 2; ++j) {
+                    mbar_wait(&d_full[j], dp[j]);
+                    dp[j] ^= 1u;
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int cc = 0; cc < C::COLS; cc += 64) {
+                        const int c0 = j * C::NH + ch * C::COLS + cc;
+                        float v[64];
+                        tmem_ld64(tmem + t_lane + static_cast<uint32_t>(c0), v);
+                        pair_epi32<N>(ld, l, last, v, c0, row, A, wo_s, dot);
+                        pair_epi32<N>(ld, l, last, v + 32, c0 + 32, row, A, wo_s, dot);
+                    }
+                    tc_fence_before();
+                    if (!last) fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(a_ready0 + j * 8u);
+                }
+            }
+            const int par = static_cast<int>(k & 1);
+            dotbuf[(par * 2 + ch) * C::TM + row] = dot;
+            named_bar_sync(1, C::EPI_WARPS * 32);
+            if (ch == 0) {
+                const float delta = (dotbuf[(par * 2) * C::TM + row] + dotbuf[(par * 2 + 1) * C::TM + row]) + a.bo;
+                if (valid && a.per_point) a.per_point[obase + rr] = delta;
+                if (a.keys) {
+                    unsigned long long key = valid ? row_key(delta, a.index_offset + pbase + rr) : ~0ull;
+                    key = warp_min_u64(key);
+                    if (lane == 0) atomicMin(a.keys + motion, key);
+                    named_bar_sync(2, 4 * 32);
+                    if (e == 0 && lane == 0 && a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                            __threadfence();
+                            const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion, a.free_out + motion);
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_pair(tmem, N);
+}
+
+template <int N>
+static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    using C = PairCfg<N>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(fused_bf16_pair_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int64_t pairs = num_sms / 2;
+    if (a.n_tiles < pairs) pairs = a.n_tiles;
+    if (pairs < 1) return cudaSuccess;
+    fused_bf16_pair_kernel<N><<<static_cast<unsigned>(2 * pairs), C::THREADS, C::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    switch (a.N) {
+        case 256: return launch_pair_n<256>(a, num_sms, st);
+        case 512: return launch_pair_n<512>(a, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ------------------------------------------------------------- K0 (bf16) -----
+// Per motion m and concat slot s: b_m = b + Wq . zq (fp32, q0 then q1), then the
+// extension rows (b_hi, b_lo, W_x hi/lo splits) in the no-swizzle K=16 layout,
+// cut into (n-half, CTA-half) blobs of N/4 rows.  Also resets keys/counters.
+struct QNormX {
+    float shift[kMaxIn], scale[kMaxIn];
+};
+
+__global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N, int n_mb,
+                                  const float* __restrict__ wq, const float* __restrict__ base_bias,
+                                  const float* __restrict__ wx_slots, uint8_t* __restrict__ ext, const QNormX qn,
+                                  unsigned long long* keys, unsigned int* counters, int64_t n_keys) {
+    const int64_t m = blockIdx.x;
+    const int slot = blockIdx.y;
+    if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
+        keys[m] = ~0ull;
+        counters[m] = 0u;
+    }
+    if (slot >= n_mb) return;
+    __shared__ float zq[kMaxIn];
+    const int nq = 2 * dof;
+    if (threadIdx.x < nq) {
+        const float q = q01[m * nq + threadIdx.x];
+        zq[threadIdx.x] = __fmul_rn(__fsub_rn(q, qn.shift[threadIdx.x]), qn.scale[threadIdx.x]);
+    }
+    __syncthreads();
+    const float* w = wq + static_cast<int64_t>(slot) * nq * N;
+    const float* wx = wx_slots + static_cast<int64_t>(slot) * 3 * N;
+    const int NH = N / 2, BR = N / 4;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        float acc = base_bias[slot * N + n];
+        for (int k = 0; k < nq; ++k) acc = __fmaf_rn(zq[k], w[k * N + n], acc);
+        __nv_bfloat16 bh, bl, h0, l0, h1, l1, h2, l2;
+        split_bf16(acc, bh, bl);
+        split_bf16(wx[n], h0, l0);
+        split_bf16(wx[N + n], h1, l1);
+        split_bf16(wx[2 * N + n], h2, l2);
+        const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
+        __align__(16) __nv_bfloat16 v[16] = {bh, bl, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
+        const int nh = n / NH, wi = n % NH, r = wi / BR, rr = wi % BR;
+        const int64_t blob = ((m * n_mb + slot) * 2 + nh) * 2 + r;
+        uint8_t* base = ext + blob * BR * 32;
+        *reinterpret_cast<uint4*>(base + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
+        *reinterpret_cast<uint4*>(base + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+    }
+}
+
+}  // namespace svn
+
+namespace svn {
+
+cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
+                              uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,
+                              int64_t n_keys, cudaStream_t st) {
+    if (a.M <= 0) return cudaSuccess;
+    QNormX qn;
+    for (int k = 0; k < 2 * a.dof && k < kMaxIn; ++k) {
+        qn.shift[k] = a.shift[3 + k];
+        qn.scale[k] = a.scale[3 + k];
+    }
+    dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
+    motion_ext_kernel<<<grid, 256, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn,
+                                             keys_init, counters_init, n_keys);
+    return cudaGetLastError();
+}
+
+}  // namespace svn

@@ -5,6 +5,8 @@
 // exception texts, stream-ordered scratch, kernel sequencing (K0 -> K1), the
 // host-buffer convenience entry points that mirror the reference signatures, and
 // the SVCKPT01 checkpoint reader.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -74,6 +76,41 @@ svn_status validate_desc(const svn_model_desc* d) {
     return SVN_OK;
 }
 
+// cuTensorMapEncodeTiled from the driver, fetched through the runtime (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// A byte blob seen as a 2-D tensor [rows][row_bytes]; one TMA box = box_rows rows.
+svn_status encode_blob_map(CUtensorMap* map, const void* base, uint64_t row_bytes, uint64_t rows, uint32_t box_rows) {
+    auto fn = tmap_encoder();
+    if (!fn) return fail(SVN_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {row_bytes, rows > 0 ? rows : 1};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(row_bytes), box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SVN_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    return SVN_OK;
+}
+
+// bf16 hi/lo split (host), matching split_bf16 on the device.
+void split_bf16_host(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(x);
+    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
 }  // namespace
 
 struct svn_model {
@@ -86,6 +123,7 @@ struct svn_model {
     FusedArgs base{};        // model part of the kernel arguments
     float* d_wq = nullptr;     // [n_mb][2dof][N]
     float* d_mbbase = nullptr; // [n_mb][N]
+    float* d_wxslots = nullptr; // [n_mb][3][N] x-part columns of the concat layers
     bool has_bf16 = false;
 
     template <class T>
@@ -230,7 +268,7 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
     q += in;
     for (int k = 0; k < in; ++k) a.scale[k] = q[k];
     q += in;
-    std::vector<float> wq_host, mbbase_host;
+    std::vector<float> wq_host, mbbase_host, wx_host;
     auto cleanup_fail = [&](svn_status s) {
         delete m;
         return s;
@@ -264,6 +302,7 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
             ld.bias_zero = 0;
             wq_host.insert(wq_host.end(), W + static_cast<int64_t>(xoff + 3) * N,
                            W + static_cast<int64_t>(xoff + 3 + nq) * N);
+            wx_host.insert(wx_host.end(), W + static_cast<int64_t>(xoff) * N, W + static_cast<int64_t>(xoff + 3) * N);
             mbbase_host.insert(mbbase_host.end(), b, b + N);
         }
         ld.s = ld.t = nullptr;
@@ -291,6 +330,7 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
     }
     if ((st = m->upload(wq_host.data(), wq_host.size(), &m->d_wq)) != SVN_OK) return cleanup_fail(st);
     if ((st = m->upload(mbbase_host.data(), mbbase_host.size(), &m->d_mbbase)) != SVN_OK) return cleanup_fail(st);
+    if ((st = m->upload(wx_host.data(), wx_host.size(), &m->d_wxslots)) != SVN_OK) return cleanup_fail(st);
     a.n_mb = m->n_mb;
 
     // bf16 tcgen05 weight stream for layers 1..L-1: h part only, per layer the
@@ -325,6 +365,40 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         __nv_bfloat16* dws = nullptr;
         if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return cleanup_fail(st);
         a.wstream = dws;
+        // CTA-pair kernel: TMA views of the weight stream and of the model-constant
+        // K=16 extension rows (bias hi/lo of non-concat layers with a nonzero bias).
+        const int BR = N / 4;
+        if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return cleanup_fail(st);
+        std::vector<uint8_t> xm;
+        const float* Wb = params + 2 * in;
+        for (int l = 0; l < L; ++l) {
+            const int K = layer_k(d->layers, l, N, in);
+            const float* b = Wb + static_cast<int64_t>(N) * K;
+            LayerDev& ld = a.layer[l];
+            ld.ext = 0;
+            ld.ext_row = 0;
+            if (ld.mb_slot >= 0) {
+                ld.ext = 2;
+            } else if (!ld.bias_zero) {
+                ld.ext = 1;
+                ld.ext_row = static_cast<int64_t>(xm.size() / 32);
+                const size_t base = xm.size();
+                xm.resize(base + static_cast<size_t>(N) * 32, 0);
+                for (int n = 0; n < N; ++n) {
+                    const int nh = n / (N / 2), wi = n % (N / 2), r = wi / BR, rr = wi % BR;
+                    uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * BR) * 32;
+                    __nv_bfloat16 hi, lo;
+                    split_bf16_host(b[n], hi, lo);
+                    *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 0)) = hi;
+                    *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 1)) = lo;
+                }
+            }
+            Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+        }
+        if (xm.empty()) xm.resize(static_cast<size_t>(BR) * 32, 0);
+        uint8_t* dxm = nullptr;
+        if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
+        if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return cleanup_fail(st);
         m->has_bf16 = true;
     }
     *out = m;
@@ -352,7 +426,7 @@ svn_status check_prec(const svn_model* m, svn_precision prec) {
     return SVN_OK;
 }
 
-int tile_rows(svn_precision prec) { return prec == SVN_PREC_BF16 ? 128 : 64; }
+int tile_rows(svn_precision prec) { return prec == SVN_PREC_BF16 ? 256 : 64; }
 
 // Scratch buffers freed on the stream when the call's kernels are done.
 struct Scratch {
@@ -388,13 +462,27 @@ cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaS
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
     }
-    cudaError_t e = prec == SVN_PREC_BF16 ? launch_fused_bf16(a, num_sms, st) : launch_fused_fp32(a, num_sms, st);
+    cudaError_t e = prec == SVN_PREC_BF16 ? launch_fused_bf16_pair(a, num_sms, st) : launch_fused_fp32(a, num_sms, st);
     ++g_launches;
     if (g_timing) {
         cudaEventRecord(e1, st);
         g_events.emplace_back(e0, e1);
     }
     return e;
+}
+
+// bf16: per-motion K=16 extension rows (folded bias + x-part splits) and their TMA view.
+svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long long* keys, unsigned int* counters,
+                      int64_t n_keys, Scratch& sc, cudaStream_t st) {
+    uint8_t* ext = nullptr;
+    const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * m->N;
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
+    svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N / 4));
+    if (s != SVN_OK) return s;
+    SVN_CUDA(launch_motion_ext(a, m->d_wq, m->d_mbbase, m->d_wxslots, ext, keys, counters, n_keys, st),
+             "motion_ext kernel");
+    ++g_launches;
+    return SVN_OK;
 }
 
 // Shared body of the dense query (full result or keys-only partial).
@@ -427,8 +515,10 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     Scratch sc(st);
     float* mb = nullptr;
     const int n_mb = exact ? 0 : m->n_mb;
-    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb), sizeof(float) * static_cast<size_t>(M) * (n_mb ? n_mb : 1) * m->N),
-             "cudaMallocAsync(motion_bias)");
+    if (prec != SVN_PREC_BF16)
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb),
+                          sizeof(float) * static_cast<size_t>(M) * (n_mb ? n_mb : 1) * m->N),
+                 "cudaMallocAsync(motion_bias)");
     a.motion_bias = mb;
     a.n_mb = m->n_mb;  // slot stride stays the model's (exact mode never reads it)
     unsigned long long* keys = nullptr;
@@ -444,7 +534,10 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.min_out = min_out;
     a.argmin_out = argmin_out;
     a.free_out = free_out;
-    {
+    if (prec == SVN_PREC_BF16) {
+        s = motion_ext(m, a, M, keys_partial ? nullptr : keys, counters, keys_partial ? 0 : M, sc, st);
+        if (s != SVN_OK) return s;
+    } else {
         FusedArgs k0 = a;
         k0.n_mb = n_mb;
         SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, keys_partial ? nullptr : keys, counters,
@@ -587,7 +680,10 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
     a.q01 = dq;
     a.tiles = dt;
     a.motion_bias = mb;
-    {
+    if (prec == SVN_PREC_BF16) {
+        s = motion_ext(m, a, nseg, nullptr, nullptr, 0, sc, st);
+        if (s != SVN_OK) return s;
+    } else {
         FusedArgs k0 = a;
         k0.n_mb = a.exact ? 0 : m->n_mb;
         SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, nullptr, nullptr, 0, st), "motion_bias kernel");
