@@ -68,6 +68,22 @@ struct FusedArgs {
     uint8_t* free_out;
     double margin;
     float* per_point;          // [.. out_base + row], or null
+    unsigned long long* prof;  // optional wait-time counters (clock64 cycles), see kProf*
+};
+
+// Instrumentation slots (summed over CTAs) when FusedArgs::prof is set.
+enum : int {
+    kProfMmaWaitA = 0,   // MMA issuer waiting for epilogue (a_ready)
+    kProfMmaWaitFull,    // MMA issuer waiting for TMA (full)
+    kProfMmaWaitAx,      // MMA issuer waiting for the A extension
+    kProfMmaTotal,       // MMA issuer loop
+    kProfEpiWaitD,       // epilogue waiting for the accumulator (d_full)
+    kProfEpiWork,        // epilogue TMEM load + math + smem store
+    kProfEpiArrive,      // epilogue fences + arrive
+    kProfEpiOut,         // output dot exchange + keys
+    kProfEpiAx,          // A extension writes
+    kProfProdWaitEmpty,  // producer waiting for free slots
+    kProfSlots = 16
 };
 
 // Orderable-u32 map of a float: unsigned compare == float compare; NaN -> max.

@@ -42,7 +42,7 @@ struct PairCfg {
     static constexpr uint32_t AX_BYTES = TM * 32;    // K=16 extension of A (4 KiB)
     static constexpr uint32_t CHUNK = BR * 128;      // per-CTA main weight chunk
     static constexpr uint32_t XCHUNK = BR * 32;      // per-CTA extension chunk
-    static constexpr int STAGES = N >= 512 ? 4 : 8;
+    static constexpr int STAGES = N >= 512 ? 5 : 8;
     static constexpr int EPI_WARPS = 8;
     static constexpr int THREADS = 64 + EPI_WARPS * 32;
     static constexpr int COLS = NH / 2;              // columns per epilogue thread per half
@@ -53,7 +53,7 @@ struct PairCfg {
     static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
     static constexpr uint32_t SMEM = OFF_BAR + 256;
     static_assert(SMEM <= 232448, "shared memory budget");
-    static_assert(COLS % 64 == 0, "epilogue works in 64-column TMEM loads");
+    static_assert(COLS % 32 == 0, "epilogue works in 32-column TMEM loads");
 };
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
@@ -216,8 +216,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             const uint32_t full0 = mapa_shared(smem_u32(full), 0);
             int stage = 0;
             uint32_t phase = 0;
+            unsigned long long pw_e = 0;
             auto slot = [&](uint32_t bytes_one_cta) {
+                const unsigned long long c0 = clock64();
                 mbar_wait(&empty[stage], phase ^ 1u);
+                pw_e += clock64() - c0;
                 if (rank == 0) mbar_arrive_expect_tx_local(&full[stage], 2 * bytes_one_cta);
             };
             auto advance = [&]() {
@@ -258,6 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     }
                 }
             }
+            if (a.prof && rank == 0) atomicAdd(a.prof + kProfProdWaitEmpty, pw_e);
         }
     } else if (warp == 1) {
         // -------------------------------------------------------------- MMA issuer --
@@ -267,10 +271,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             int stage = 0;
             uint32_t phase = 0;
             uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
+            unsigned long long pw_a = 0, pw_f = 0, pw_x = 0;
+            const unsigned long long p_start = clock64();
             int64_t k = 0;  // local tile counter
             for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
                 const int b = static_cast<int>(k & 1);
-                mbar_wait_cluster(&ax_full[b], ax_ph[b]);
+                {
+                    const unsigned long long c0 = clock64();
+                    mbar_wait(&ax_full[b], ax_ph[b]);
+                    pw_x += clock64() - c0;
+                }
                 ax_ph[b] ^= 1u;
                 for (int l = 0; l < L; ++l) {
                     const LayerDev& ld = a.layer[l];
@@ -278,14 +288,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     for (int step = 0; step < steps; ++step) {
                         const int nh = step & 1, kh = step >> 1;
                         if (kh == 0 && (k > 0 || l > 0)) {  // D[nh] drained / A[k-half nh] written
-                            mbar_wait_cluster(&a_ready[nh], ar_ph[nh]);
+                            const unsigned long long c0 = clock64();
+                            mbar_wait(&a_ready[nh], ar_ph[nh]);
+                            pw_a += clock64() - c0;
                             ar_ph[nh] ^= 1u;
                         }
                         tc_fence_after();
                         const uint32_t d_addr = tmem + static_cast<uint32_t>(nh * C::NH);
                         bool acc = false;
                         if (kh == 0 && ld.ext) {
-                            mbar_wait(&full[stage], phase);
+                            {
+                                const unsigned long long c0 = clock64();
+                                mbar_wait(&full[stage], phase);
+                                pw_f += clock64() - c0;
+                            }
                             tc_fence_after();
                             mma_bf16_pair(d_addr, noswz_desc(ax_base + b * C::AX_BYTES, 128, 256),
                                           noswz_desc(s_base + stage * C::CHUNK, 128, 256), idesc, 0u);
@@ -295,7 +311,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                         }
                         if (l > 0) {
                             for (int ks = 0; ks < C::KSL; ++ks) {
-                                mbar_wait(&full[stage], phase);
+                                {
+                                    const unsigned long long c0 = clock64();
+                                    mbar_wait(&full[stage], phase);
+                                    pw_f += clock64() - c0;
+                                }
                                 tc_fence_after();
                                 const uint32_t a_slab = a_base + static_cast<uint32_t>(kh * C::KSL + ks) * C::A_SLAB;
                                 const uint32_t b_stage = s_base + static_cast<uint32_t>(stage) * C::CHUNK;
@@ -312,6 +332,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                         else if (step >= 2) mma_commit_pair(&d_full[step - 2], 3);
                     }
                 }
+            }
+            if (a.prof) {
+                atomicAdd(a.prof + kProfMmaWaitA, pw_a);
+                atomicAdd(a.prof + kProfMmaWaitFull, pw_f);
+                atomicAdd(a.prof + kProfMmaWaitAx, pw_x);
+                atomicAdd(a.prof + kProfMmaTotal, clock64() - p_start);
             }
         }
     } else {
@@ -338,12 +364,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 fence_proxy_async_smem();
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(ax_full0 + b * 8u);
+            if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
         };
+        unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0, pe_x = 0;
         int64_t k = 0;
         if (pair < a.n_tiles) write_ax_tile(pair, 0);
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
-            if (t + npairs < a.n_tiles) write_ax_tile(t + npairs, static_cast<int>((k + 1) & 1));
+            {
+                const unsigned long long c0 = clock64();
+                if (t + npairs < a.n_tiles) write_ax_tile(t + npairs, static_cast<int>((k + 1) & 1));
+                pe_x += clock64() - c0;
+            }
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
@@ -354,23 +385,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
                 for (int j = 0; j < 2; ++j) {
+                    const unsigned long long c0 = clock64();
                     mbar_wait(&d_full[j], dp[j]);
+                    const unsigned long long c1 = clock64();
+                    pe_d += c1 - c0;
                     dp[j] ^= 1u;
                     tc_fence_after();
-#pragma unroll 1
-                    for (int cc = 0; cc < C::COLS; cc += 64) {
-                        const int c0 = j * C::NH + ch * C::COLS + cc;
-                        float v[64];
-                        tmem_ld64(tmem + t_lane + static_cast<uint32_t>(c0), v);
-                        pair_epi32<N>(ld, l, last, v, c0, row, A, wo_s, dot);
-                        pair_epi32<N>(ld, l, last, v + 32, c0 + 32, row, A, wo_s, dot);
+                    {
+                        // rolling pipeline over 32-column chunks: the next TMEM load is in
+                        // flight while the current chunk is packed and stored
+                        const int c0 = j * C::NH + ch * C::COLS;
+                        constexpr int NCH = C::COLS / 32;
+                        uint32_t ra[32], rb[32];
+                        tmem_ld32_async(tmem + t_lane + static_cast<uint32_t>(c0), ra);
+                        tmem_wait_tied(ra);
+#pragma unroll
+                        for (int q = 0; q < NCH; ++q) {
+                            uint32_t(&cur)[32] = (q & 1) ? rb : ra;
+                            uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
+                            if (q + 1 < NCH) tmem_ld32_async(tmem + t_lane + static_cast<uint32_t>(c0 + 32 * (q + 1)), nxt);
+                            pair_epi32<N>(ld, l, last, reinterpret_cast<float*>(cur), c0 + 32 * q, row, A, wo_s, dot);
+                            if (q + 1 < NCH) tmem_wait_tied(nxt);
+                        }
                     }
+                    const unsigned long long c2 = clock64();
+                    pe_w += c2 - c1;
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive_cluster(a_ready0 + j * 8u);
+                    if (lane == 0) mbar_arrive_remote(a_ready0 + j * 8u);
+                    pe_a += clock64() - c2;
                 }
             }
+            const unsigned long long c3 = clock64();
             const int par = static_cast<int>(k & 1);
             dotbuf[(par * 2 + ch) * C::TM + row] = dot;
             named_bar_sync(1, C::EPI_WARPS * 32);
@@ -393,6 +440,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     }
                 }
             }
+            pe_o += clock64() - c3;
+        }
+        if (a.prof && e == 0 && lane == 0 && rank == 0) {
+            atomicAdd(a.prof + kProfEpiWaitD, pe_d);
+            atomicAdd(a.prof + kProfEpiWork, pe_w);
+            atomicAdd(a.prof + kProfEpiArrive, pe_a);
+            atomicAdd(a.prof + kProfEpiOut, pe_o);
+            atomicAdd(a.prof + kProfEpiAx, pe_x);
         }
     }
 

@@ -12,6 +12,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -31,6 +32,14 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 thread_local bool g_timing = false;
 thread_local std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_events;
+thread_local unsigned long long g_prof[kProfSlots] = {};
+bool prof_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVN_PROF");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
 
 svn_status fail(svn_status code, const std::string& msg) {
     g_err = msg;
@@ -462,8 +471,23 @@ cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaS
         cudaEventCreate(&e1);
         cudaEventRecord(e0, st);
     }
-    cudaError_t e = prec == SVN_PREC_BF16 ? launch_fused_bf16_pair(a, num_sms, st) : launch_fused_fp32(a, num_sms, st);
+    unsigned long long* dprof = nullptr;
+    FusedArgs ap = a;
+    if (prof_enabled()) {
+        cudaMalloc(&dprof, sizeof(unsigned long long) * kProfSlots);
+        cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * kProfSlots, st);
+        ap.prof = dprof;
+    }
+    cudaError_t e = prec == SVN_PREC_BF16 ? launch_fused_bf16_pair(ap, num_sms, st) : launch_fused_fp32(ap, num_sms, st);
     ++g_launches;
+    if (dprof) {
+        cudaMemcpyAsync(g_prof, dprof, sizeof(g_prof), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(dprof);
+        std::fprintf(stderr, "[svn prof]");
+        for (int i = 0; i < kProfSlots; ++i) std::fprintf(stderr, " %llu", g_prof[i]);
+        std::fprintf(stderr, "\n");
+    }
     if (g_timing) {
         cudaEventRecord(e1, st);
         g_events.emplace_back(e0, e1);
