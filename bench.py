@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default=None, choices=["motion", "point"],
+                    help="multi-GPU sharding: motion (default) or point (single-motion workloads)")
     return ap.parse_args()
 
 
@@ -145,9 +147,10 @@ def cpu_sample(w, threads):
     """Bounded sample of the workload for the CPU path: `threads` motions x a point
     count sized for ~10-20 s of CPU work at ~2 ns/FLOP-per-core."""
     fq = w.program.flops_per_query()
-    budget = 4e10 * max(1, threads)  # FLOPs
-    per_motion = int(max(256, min(w.points, budget / max(1, threads) / fq)))
-    return max(1, min(w.motions, threads)), per_motion
+    budget = 4e10 * max(1, threads)  # FLOPs for the whole sample
+    M = max(1, min(w.motions, threads))
+    per_motion = int(max(256, min(w.points, budget / M / fq)))
+    return M, per_motion
 
 
 def run_cpu(w, params, seed, threads, lib, steps, warmup):
@@ -201,21 +204,40 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    # ---- workload: this rank's motion shard, resident in HBM -----------------
+    # ---- workload, resident in HBM ------------------------------------------
+    # motion mode (weak scaling): rank r evaluates its own shard of the c5 motion
+    #   stream (motions [r*M, (r+1)*M)) against the full cloud; no collective.
+    # point mode (strong scaling, single-motion workloads): the cloud is split into
+    #   rank chunks; one NCCL MIN all-reduce of 8 B per motion per step.
+    mode = args.mode or ("point" if w.motions == 1 and world > 1 else "motion")
+    from paper_2402_15281_b200.parallel import allreduce_keys_min, shard_range
     M, P = w.motions, w.points
-    pts_np, q_np = w.make(seed=args.seed, motions=M, motion_offset=rank * M)
+    if mode == "motion":
+        pts_np, q_np = w.make(seed=args.seed, motions=M, motion_offset=rank * M)
+        pb, pe = 0, P
+    else:
+        pts_np, q_np = w.make(seed=args.seed, motions=M)
+        pb, pe = shard_range(P, world, rank)
     params = S.init_params(w.program, args.seed, w.bound)
     model = S.Model(w.program, params, device=local)
-    pts = torch.from_numpy(pts_np).to(dev)
+    pts = torch.from_numpy(np.ascontiguousarray(pts_np[pb:pe])).to(dev)
     q = torch.from_numpy(q_np).to(dev)
     mn = torch.empty(M, dtype=torch.float32, device=dev)
     am = torch.empty(M, dtype=torch.int32, device=dev)
     fr = torch.empty(M, dtype=torch.uint8, device=dev)
+    keys = torch.empty(M, dtype=torch.int64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        model.query_min_device(pts, q, w.margin, mn, am, fr, None, precision=prec, stream=stream)
+        if mode == "motion":
+            model.query_min_device(pts, q, w.margin, mn, am, fr, None, precision=prec, stream=stream)
+        else:
+            S.keys_init_device(keys, stream=stream)
+            model.query_keys_device(pts, pb, q, keys, precision=prec, stream=stream)
+            if world > 1:
+                allreduce_keys_min(keys)
+            S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -245,12 +267,12 @@ def main():
         t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kernel_ms = float(t[0]), float(t[1])
-    total_queries = M * P * world
+    total_queries = M * P * world if mode == "motion" else M * P
     value = total_queries / (ms * 1e-3)
 
     # ---- roofline of the dominant kernel (the fused MLP) ----------------------
     flop_q = w.program.flops_per_query()
-    achieved_tf = M * P * flop_q / (kernel_ms * 1e-3) / 1e12
+    achieved_tf = M * (pe - pb) * flop_q / (kernel_ms * 1e-3) / 1e12
     if prec == "bf16":
         peak = float(peaks["bf16_tflops"])
         roof = {"bound": "tensor", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
@@ -275,7 +297,7 @@ def main():
 
     # ---- e2e through the public host API (host buffers, copies inside) --------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and mode == "motion":
         hp = torch.from_numpy(pts_np).pin_memory().numpy()
         hq = torch.from_numpy(q_np).pin_memory().numpy()
         model.query_min(hp, hq, w.margin, precision=prec)  # warm the host path
@@ -307,11 +329,12 @@ def main():
     if rank == 0:
         cl = clocks.summary()
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "weak" if mode == "motion" else "strong",
                 "vs_baseline": None, "dtype": prec, "data": "synthetic (seeded; see workloads.py)",
                 "config": {"workload": w.key, "description": w.description, "network": w.program.name,
                            "motions_per_gpu": M, "points": P, "queries_per_step": total_queries,
-                           "margin": w.margin, "parallelism": f"motion-shard x{world}",
+                           "margin": w.margin, "parallelism": f"{mode}-shard x{world}",
                            "l2": "flushed (256 MiB write) before every timed step, outside the step events"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": cl, "free_fraction": float(fr.float().mean().item())}

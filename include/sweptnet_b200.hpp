@@ -1,0 +1,168 @@
+// sweptnet_b200.hpp — header-only C++ host API over the C-ABI (include/sweptnet_b200.h).
+//
+// Mirrors the reference's inference interface (/root/reference/proj/include/sweptnet/nn.hpp
+// and collision.hpp) with std containers instead of Eigen, so it compiles anywhere the
+// C-ABI library does:
+//   init_model            nn.hpp:80-81     -> Model::init
+//   load_checkpoint       nn.hpp:168       -> Model::load_checkpoint
+//   forward_eval<float>   nn.hpp:92-93     -> forward_eval
+//   predict_min_distance  nn.hpp:162-163   -> predict_min_distance
+//   ProxyEvaluator        collision.hpp:45 -> batched_proxy (one GPU call for all motions)
+// Errors are rethrown with the reference's exception types and messages:
+// std::invalid_argument for argument errors (nn.cpp:98-99, 462, 465), and IoError /
+// FormatError / TruncationError / VersionError (errors.hpp:8-27) for checkpoints.
+#pragma once
+
+#include <array>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sweptnet_b200.h"
+
+namespace sweptnet_b200 {
+
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct FormatError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct TruncationError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct VersionError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(svn_status s) {
+    if (s == SVN_OK) return;
+    const std::string msg = svn_last_error();
+    switch (s) {
+        case SVN_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+        case SVN_ERR_IO: throw IoError(msg);
+        case SVN_ERR_FORMAT: throw FormatError(msg);
+        case SVN_ERR_TRUNCATION: throw TruncationError(msg);
+        case SVN_ERR_VERSION: throw VersionError(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+using Vec3 = std::array<double, 3>;
+
+// Motion (sweptvol.hpp:14-18): start and goal joint configurations.
+struct Motion {
+    std::vector<double> q0, q1;
+};
+
+enum class Precision { BF16 = SVN_PREC_BF16, FP32 = SVN_PREC_FP32, FP32_EXACT = SVN_PREC_FP32_EXACT };
+
+// A layer program; fig2() is the reference network (nn.hpp:11-15).
+struct Program {
+    int width = 0, dof = 0;
+    std::vector<svn_layer> layers;
+    svn_model_desc desc() const { return svn_model_desc{static_cast<int32_t>(layers.size()), width, dof, layers.data()}; }
+    static Program fig2(int n_blocks, int width, int dof) {
+        Program p{width, dof, {}};
+        p.layers.push_back(svn_layer{1, 0, 0, 0});
+        for (int i = 0; i < n_blocks; ++i) p.layers.push_back(svn_layer{1, 1, 1, 1});
+        return p;
+    }
+    static Program plain(int hidden, int width, int dof) {
+        Program p{width, dof, {}};
+        p.layers.push_back(svn_layer{1, 1, 0, 0});
+        for (int i = 1; i < hidden; ++i) p.layers.push_back(svn_layer{0, 1, 0, 0});
+        return p;
+    }
+    static Program deepsdf(int hidden, int width, int dof, int skip_at = 4) {
+        Program p{width, dof, {}};
+        p.layers.push_back(svn_layer{1, 1, 0, 0});
+        for (int i = 1; i < hidden; ++i) p.layers.push_back(svn_layer{i == skip_at ? 1 : 0, 1, 0, 0});
+        return p;
+    }
+};
+
+class Model {
+public:
+    Model(const Program& prog, const std::vector<float>& params, int device = 0) : prog_(prog) {
+        const svn_model_desc d = prog_.desc();
+        svn_model* h = nullptr;
+        check(svn_model_create(&d, params.data(), static_cast<int64_t>(params.size()), device, &h));
+        h_.reset(h, svn_model_destroy);
+    }
+    // init_model (nn.cpp:57-93); bound_mode 0 = +-1/sqrt(fan_in), 1 = He-uniform.
+    static Model init(const Program& prog, uint64_t seed, int bound_mode = 0, int device = 0) {
+        const svn_model_desc d = prog.desc();
+        std::vector<float> p(static_cast<size_t>(svn_param_count(&d)));
+        check(svn_init_params(&d, seed, bound_mode, p.data()));
+        return Model(prog, p, device);
+    }
+    static Model load_checkpoint(const std::string& path, int device = 0) {
+        svn_model* h = nullptr;
+        check(svn_model_load_checkpoint(path.c_str(), device, &h));
+        Model m;
+        m.h_.reset(h, svn_model_destroy);
+        return m;
+    }
+    const svn_model* handle() const { return h_.get(); }
+    int dof() const { return prog_.dof; }
+
+private:
+    Model() = default;
+    Program prog_;
+    std::shared_ptr<svn_model> h_;
+};
+
+// forward_eval<float> (nn.cpp:95-130): raw row-major [rows x (3 + 2*dof)].
+inline std::vector<float> forward_eval(const Model& m, const std::vector<float>& raw, long rows, long cols,
+                                       Precision prec = Precision::FP32_EXACT) {
+    std::vector<float> out(static_cast<size_t>(rows > 0 ? rows : 0));
+    check(svn_forward_eval(m.handle(), static_cast<svn_precision>(prec), raw.data(), rows, cols, out.data()));
+    return out;
+}
+
+// predict_min_distance (nn.cpp:460-480): (double(min delta), argmin point index).
+inline std::pair<double, int> predict_min_distance(const Model& m, const std::vector<Vec3>& cloud, const Motion& mo,
+                                                   Precision prec = Precision::FP32_EXACT) {
+    if (mo.q0.size() != mo.q1.size()) throw std::invalid_argument("predict_min_distance: motion dof does not match model");
+    double mn = 0.0;
+    int32_t idx = 0;
+    check(svn_predict_min_distance(m.handle(), static_cast<svn_precision>(prec),
+                                   cloud.empty() ? nullptr : cloud.front().data(), static_cast<int64_t>(cloud.size()),
+                                   mo.q0.data(), mo.q1.data(), static_cast<int32_t>(mo.q0.size()), &mn, &idx));
+    return {mn, idx};
+}
+
+// Batched proxy for gcc_nn_search_impl (collision.cpp:55-107): every motion of a scene in
+// one GPU call; proxy(j) then returns the cached predict_min_distance(...).first.
+inline std::function<double(int)> batched_proxy(const Model& m, const std::vector<Vec3>& cloud,
+                                                const std::vector<Motion>& motions,
+                                                Precision prec = Precision::BF16) {
+    if (cloud.empty()) throw std::invalid_argument("predict_min_distance: empty point cloud");
+    std::vector<float> pts;
+    pts.reserve(cloud.size() * 3);
+    for (const Vec3& p : cloud)
+        for (double c : p) pts.push_back(static_cast<float>(c));
+    const size_t dof = motions.empty() ? 0 : motions.front().q0.size();
+    std::vector<float> q;
+    for (const Motion& mo : motions) {
+        if (mo.q0.size() != dof || mo.q1.size() != dof)
+            throw std::invalid_argument("predict_min_distance: motion dof does not match model");
+        for (double v : mo.q0) q.push_back(static_cast<float>(v));
+        for (double v : mo.q1) q.push_back(static_cast<float>(v));
+    }
+    const size_t M = motions.size();
+    auto mins = std::make_shared<std::vector<float>>(M);
+    if (M) {
+        std::vector<int32_t> am(M);
+        std::vector<uint8_t> fr(M);
+        check(svn_query_min(m.handle(), static_cast<svn_precision>(prec), pts.data(), static_cast<int64_t>(cloud.size()),
+                            q.data(), static_cast<int64_t>(M), 0.0, mins->data(), am.data(), fr.data(), nullptr));
+    }
+    return [mins](int j) { return static_cast<double>((*mins)[static_cast<size_t>(j)]); };
+}
+
+}  // namespace sweptnet_b200

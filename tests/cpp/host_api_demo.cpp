@@ -1,0 +1,37 @@
+// Compiles the C++ host API against the C-ABI library and runs the reference-shaped
+// calls.  Built and run by tests/test_cpp_host_api.py (GPU); compiled-only on CPU.
+#include <cstdio>
+#include <stdexcept>
+
+#include "sweptnet_b200.hpp"
+
+using namespace sweptnet_b200;
+
+int main() {
+    const Program prog = Program::fig2(3, 256, 6);
+    Model m = Model::init(prog, 7, 0);
+    std::vector<Vec3> cloud;
+    for (int i = 0; i < 300; ++i) cloud.push_back({0.004 * i, -0.2 + 0.001 * i, 0.1});
+    Motion mo{{0.1, -0.2, 0.3, 0.0, 0.5, -0.4}, {1.0, 0.5, -0.3, 0.2, 0.1, 0.0}};
+    auto [mn, idx] = predict_min_distance(m, cloud, mo);
+    std::vector<float> raw;
+    for (const Vec3& p : cloud) {
+        for (double c : p) raw.push_back(static_cast<float>(c));
+        for (double v : mo.q0) raw.push_back(static_cast<float>(v));
+        for (double v : mo.q1) raw.push_back(static_cast<float>(v));
+    }
+    const std::vector<float> d = forward_eval(m, raw, static_cast<long>(cloud.size()), 15);
+    int best = 0;
+    for (int i = 1; i < static_cast<int>(d.size()); ++i)
+        if (d[i] < d[best]) best = i;
+    auto proxy = batched_proxy(m, cloud, {mo, mo}, Precision::FP32_EXACT);
+    bool threw = false;
+    try {
+        predict_min_distance(m, {}, mo);
+    } catch (const std::invalid_argument& e) {
+        threw = std::string(e.what()) == "predict_min_distance: empty point cloud";
+    }
+    std::printf("min %.9g idx %d | forward argmin %d %.9g | proxy %.9g | empty-cloud error %d\n", mn, idx, best,
+                static_cast<double>(d[best]), proxy(1), threw ? 1 : 0);
+    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw) ? 0 : 1;
+}
