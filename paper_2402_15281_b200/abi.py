@@ -65,6 +65,10 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    override = os.environ.get("SVN_LIB")  # A/B experiments: load another build of the same ABI
+    if override:
+        L = C.CDLL(override)
+        return _finish(L)
     if os.environ.get("SVN_NO_BUILD") != "1":
         try:
             _build.build()
@@ -73,7 +77,11 @@ def lib() -> C.CDLL:
                 raise RuntimeError(f"sweptnet_b200 native library missing and build failed: {e}") from e
     if not LIB_PATH.exists():
         raise RuntimeError(f"sweptnet_b200 native library not found at {LIB_PATH}")
-    L = C.CDLL(str(LIB_PATH))
+    return _finish(C.CDLL(str(LIB_PATH)))
+
+
+def _finish(L):
+    global _lib
     P, I64, I32, D, VP = C.c_void_p, C.c_int64, C.c_int32, C.c_double, C.c_void_p
     desc_p = C.POINTER(SvnModelDesc)
     sig = {

@@ -162,7 +162,6 @@ cudaError_t launch_keys_init(unsigned long long* keys, int64_t M, cudaStream_t s
 cudaError_t launch_keys_finalize(const unsigned long long* keys, int64_t M, double margin, float* min_out,
                                  int32_t* argmin_out, uint8_t* free_out, cudaStream_t st);
 cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st);
-cudaError_t launch_fused_bf16(const FusedArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
                               uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,
