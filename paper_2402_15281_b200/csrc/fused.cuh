@@ -59,6 +59,7 @@ struct FusedArgs {
     int64_t n_tiles;
     const TileDesc* tiles;     // non-null: explicit tile table (forward_eval segments)
     int exact;                 // fp32 exact order (no q fold)
+    unsigned sleep_hint;       // bf16 kernel: try_wait suspend hint (ns) for idle-warp waits, 0 = poll
     // outputs
     unsigned long long* keys;  // [M] packed (orderable(delta) << 32 | index), or null
     unsigned int* counters;    // [M] tiles done, for the fused finaliser, or null

@@ -219,7 +219,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             unsigned long long pw_e = 0;
             auto slot = [&](uint32_t bytes_one_cta) {
                 const unsigned long long c0 = clock64();
-                mbar_wait(&empty[stage], phase ^ 1u);
+                if (a.sleep_hint) mbar_wait_sleep(&empty[stage], phase ^ 1u, a.sleep_hint);
+                else mbar_wait(&empty[stage], phase ^ 1u);
                 pw_e += clock64() - c0;
                 if (rank == 0) mbar_arrive_expect_tx_local(&full[stage], 2 * bytes_one_cta);
             };
@@ -367,6 +368,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
         };
         unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0, pe_x = 0;
+        struct Pending {
+            bool live;
+            int par;
+            int32_t motion;
+            int64_t pbase, obase;
+            int32_t rr;
+            bool valid;
+        } pend{false, 0, 0, 0, 0, 0, false};
+        auto flush_output = [&]() {
+            if (!pend.live) return;
+            const unsigned long long c3 = clock64();
+            named_bar_sync(1, C::EPI_WARPS * 32);
+            if (ch == 0) {
+                const int par = pend.par;
+                const float delta = (dotbuf[(par * 2) * C::TM + row] + dotbuf[(par * 2 + 1) * C::TM + row]) + a.bo;
+                if (pend.valid && a.per_point) a.per_point[pend.obase + pend.rr] = delta;
+                if (a.keys) {
+                    unsigned long long key = pend.valid ? row_key(delta, a.index_offset + pend.pbase + pend.rr) : ~0ull;
+                    key = warp_min_u64(key);
+                    if (lane == 0) atomicMin(a.keys + pend.motion, key);
+                    named_bar_sync(2, 4 * 32);
+                    if (e == 0 && lane == 0 && a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + pend.motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                            __threadfence();
+                            const unsigned long long kk = atomicOr(a.keys + pend.motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + pend.motion, a.argmin_out + pend.motion,
+                                       a.free_out + pend.motion);
+                        }
+                    }
+                }
+            }
+            pend.live = false;
+            pe_o += clock64() - c3;
+        };
         int64_t k = 0;
         if (pair < a.n_tiles) write_ax_tile(pair, 0);
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
@@ -386,7 +423,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 const bool last = (l == L - 1);
                 for (int j = 0; j < 2; ++j) {
                     const unsigned long long c0 = clock64();
-                    mbar_wait(&d_full[j], dp[j]);
+                    if (a.sleep_hint) mbar_wait_sleep(&d_full[j], dp[j], a.sleep_hint);
+                    else mbar_wait(&d_full[j], dp[j]);
                     const unsigned long long c1 = clock64();
                     pe_d += c1 - c0;
                     dp[j] ^= 1u;
@@ -416,31 +454,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     if (lane == 0) mbar_arrive_remote(a_ready0 + j * 8u);
                     pe_a += clock64() - c2;
                 }
+                if (l == 0) flush_output();  // previous tile's outputs
             }
-            const unsigned long long c3 = clock64();
-            const int par = static_cast<int>(k & 1);
-            dotbuf[(par * 2 + ch) * C::TM + row] = dot;
-            named_bar_sync(1, C::EPI_WARPS * 32);
-            if (ch == 0) {
-                const float delta = (dotbuf[(par * 2) * C::TM + row] + dotbuf[(par * 2 + 1) * C::TM + row]) + a.bo;
-                if (valid && a.per_point) a.per_point[obase + rr] = delta;
-                if (a.keys) {
-                    unsigned long long key = valid ? row_key(delta, a.index_offset + pbase + rr) : ~0ull;
-                    key = warp_min_u64(key);
-                    if (lane == 0) atomicMin(a.keys + motion, key);
-                    named_bar_sync(2, 4 * 32);
-                    if (e == 0 && lane == 0 && a.counters) {
-                        __threadfence();
-                        const unsigned int prev = atomicAdd(a.counters + motion, 1u);
-                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
-                            __threadfence();
-                            const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
-                            decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion, a.free_out + motion);
-                        }
-                    }
-                }
-            }
-            pe_o += clock64() - c3;
+            // the output phase of this tile runs after the next tile's layer-0 epilogue
+            // (off the MMA critical path); dotbuf is double-buffered by tile parity
+            dotbuf[((k & 1) * 2 + ch) * C::TM + row] = dot;
+            pend = Pending{true, static_cast<int>(k & 1), motion, pbase, obase, rr, valid};
+            if (t + npairs >= a.n_tiles) flush_output();
         }
         if (a.prof && e == 0 && lane == 0 && rank == 0) {
             atomicAdd(a.prof + kProfEpiWaitD, pe_d);

@@ -473,6 +473,13 @@ cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaS
     }
     unsigned long long* dprof = nullptr;
     FusedArgs ap = a;
+    {
+        static const unsigned hint = [] {
+            const char* e = std::getenv("SVN_SLEEP_NS");
+            return e ? static_cast<unsigned>(std::atoi(e)) : 0u;
+        }();
+        ap.sleep_hint = hint;
+    }
     if (prof_enabled()) {
         cudaMalloc(&dprof, sizeof(unsigned long long) * kProfSlots);
         cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * kProfSlots, st);
