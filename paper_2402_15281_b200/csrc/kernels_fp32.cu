@@ -106,8 +106,8 @@ __device__ __forceinline__ void tile_done(const FusedArgs& a, int32_t motion) {
 // ------------------------------------------------------------------ K1f -----
 template <int N>
 struct Fp32Cfg {
-    static constexpr int TM = 64;                 // rows per tile
-    static constexpr int THREADS = 256;           // 8 row groups x 32 column groups
+    static constexpr int TM = N >= 512 ? 64 : 128;  // rows per tile (activations must fit in smem)
+    static constexpr int THREADS = TM * 4;          // TM/8 row groups x 32 column groups
     static constexpr int NC = N / 32;             // columns per thread
     static constexpr int KS = 4096 / N;           // weight rows per 16 KiB chunk
     static constexpr int STAGES = 4;
@@ -129,7 +129,7 @@ __device__ __forceinline__ int layer_rows(const FusedArgs& a, int l) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(256, 1) fused_fp32_kernel(const __grid_constant__ FusedArgs a) {
+__global__ void __launch_bounds__(Fp32Cfg<N>::THREADS, 1) fused_fp32_kernel(const __grid_constant__ FusedArgs a) {
     using C = Fp32Cfg<N>;
     extern __shared__ __align__(128) uint8_t smem[];
     float* actT = reinterpret_cast<float*>(smem);

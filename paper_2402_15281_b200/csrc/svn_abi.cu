@@ -435,7 +435,7 @@ svn_status check_prec(const svn_model* m, svn_precision prec) {
     return SVN_OK;
 }
 
-int tile_rows(svn_precision prec) { return prec == SVN_PREC_BF16 ? 256 : 64; }
+int tile_rows(svn_precision prec, int N) { return prec == SVN_PREC_BF16 ? 256 : (N >= 512 ? 64 : 128); }
 
 // Scratch buffers freed on the stream when the call's kernels are done.
 struct Scratch {
@@ -536,7 +536,7 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.P = P;
     a.q01 = q01;
     a.M = M;
-    const int TM = tile_rows(prec);
+    const int TM = tile_rows(prec, m->N);
     a.tiles_per_motion = (P + TM - 1) / TM;
     a.n_tiles = a.tiles_per_motion * M;
     a.tiles = nullptr;
@@ -671,7 +671,7 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
     if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
     svn_status s = check_prec(m, prec);
     if (s != SVN_OK) return s;
-    const int nq = 2 * m->dof, TM = tile_rows(prec);
+    const int nq = 2 * m->dof, TM = tile_rows(prec, m->N);
     std::vector<float> qseg;
     std::vector<TileDesc> tiles;
     int64_t seg_start = 0;
