@@ -1,0 +1,138 @@
+"""GPU edge cases: ragged tiles, tiny inputs, NaN inputs, heavy motion mixing, concurrent
+host callers (run_box_world calls predict_min_distance from parallel_for workers,
+bench.cpp:156,193), and the device entry points."""
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2402_15281_b200 as S
+from oracle import oracle as O
+from paper_2402_15281_b200.workloads import WORKLOADS
+from test_gpu_parity import BF16_BOUND
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32_exact": 0.0, "fp32": 1e-5}
+
+
+def _tol(prec, prog):
+    return TOL.get(prec, BF16_BOUND.get(prog.name, 0.1))
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32", "fp32_exact"])
+@pytest.mark.parametrize("P", [1, 2, 127, 129, 255, 257, 511, 1000])
+def test_ragged_point_counts(prec, P):
+    w = WORKLOADS["c3"] if prec == "bf16" else WORKLOADS["c2"]
+    params = S.init_params(w.program, 17, w.bound)
+    pts, q = w.make(seed=17, motions=3, points=P)
+    r = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec, per_point=True)
+    omin, oarg, ofree, opp = O.query_min(w.program, params, pts, q, w.margin, per_point=True, threads=8)
+    tol = _tol(prec, w.program)
+    assert np.abs(r.per_point.astype(np.float64) - opp).max() <= tol
+    assert np.array_equal(r.min, r.per_point.min(axis=1))
+    assert np.array_equal(r.argmin, r.per_point.argmin(axis=1))
+    if prec == "fp32_exact":
+        assert np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32_exact"])
+def test_many_motions_few_points(prec):
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 3, w.bound)
+    pts, q = w.make(seed=3, motions=700, points=5)
+    r = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec, per_point=True)
+    omin, oarg, ofree, opp = O.query_min(w.program, params, pts, q, w.margin, per_point=True, threads=8)
+    assert np.abs(r.per_point.astype(np.float64) - opp).max() <= _tol(prec, w.program)
+    assert np.array_equal(r.argmin, r.per_point.argmin(axis=1))
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32", "fp32_exact"])
+def test_nan_point_at_index_zero_sticks(prec):
+    """nn.cpp:476-478: a NaN prediction at row 0 is returned; NaN elsewhere is skipped.
+    The Fig. 2 network propagates NaN (its input layer has no ReLU and blocks are residual)."""
+    prog = S.fig2(2, 256, 6)
+    params = S.init_params(prog, 5, "ref")
+    pts, q = WORKLOADS["c2"].make(seed=5, motions=2, points=300)
+    bad = pts.copy()
+    bad[7] = np.nan
+    m = S.Model(prog, params)
+    r = m.query_min(bad, q, 0.0, precision=prec, per_point=True)
+    assert np.all(np.isnan(r.per_point[:, 7]))
+    ok = np.delete(np.arange(300), 7)
+    assert np.array_equal(r.argmin, ok[np.argmin(r.per_point[:, ok], axis=1)])
+    bad[0] = np.nan
+    r = m.query_min(bad, q, 0.0, precision=prec)
+    assert np.all(np.isnan(r.min)) and np.all(r.argmin == 0) and not r.free.any()
+    o = O.query_min(prog, params, bad, q, 0.0)
+    assert np.all(np.isnan(o[0])) and np.all(o[1] == 0)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32_exact"])
+def test_forward_eval_every_row_its_own_motion(prec):
+    w = WORKLOADS["c3"]
+    params = S.init_params(w.program, 8, w.bound)
+    pts, q = w.make(seed=8, motions=300, points=300)
+    raw = np.concatenate([pts, q], axis=1).astype(np.float32)  # row i uses motion i
+    out = S.Model(w.program, params).forward_eval(raw, precision=prec)
+    ref = O.forward_eval(w.program, params, raw)
+    assert np.abs(out.astype(np.float64) - ref).max() <= _tol(prec, w.program)
+
+
+def test_concurrent_host_callers_share_one_model():
+    w = WORKLOADS["c1"]
+    params = S.init_params(w.program, 9, w.bound)
+    model = S.Model(w.program, params)
+    pts, q = w.make(seed=9, motions=8, points=500)
+    ref = [O.predict_min_distance(w.program, params, pts.astype(np.float64), q[m, :6], q[m, 6:]) for m in range(8)]
+    out = [None] * 8
+    errs = []
+
+    def work(m):
+        try:
+            for _ in range(3):
+                out[m] = model.predict_min_distance(pts.astype(np.float64), q[m, :6], q[m, 6:],
+                                                    precision="fp32_exact")
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(m,)) for m in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs
+    assert out == ref
+
+
+def test_device_entry_points_with_torch_stream():
+    import torch
+    w = WORKLOADS["c3"]
+    params = S.init_params(w.program, 10, w.bound)
+    pts, q = w.make(seed=10, motions=5, points=3000)
+    model = S.Model(w.program, params)
+    host = model.query_min(pts, q, w.margin, precision="bf16", per_point=True)
+    dev = torch.device("cuda:0")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        tp, tq = torch.from_numpy(pts).to(dev), torch.from_numpy(q).to(dev)
+        mn = torch.empty(5, dtype=torch.float32, device=dev)
+        am = torch.empty(5, dtype=torch.int32, device=dev)
+        fr = torch.empty(5, dtype=torch.uint8, device=dev)
+        pp = torch.empty((5, 3000), dtype=torch.float32, device=dev)
+        model.query_min_device(tp, tq, w.margin, mn, am, fr, pp, precision="bf16", stream=st)
+    st.synchronize()
+    assert np.array_equal(mn.cpu().numpy(), host.min)
+    assert np.array_equal(am.cpu().numpy(), host.argmin)
+    assert np.array_equal(pp.cpu().numpy(), host.per_point)
+
+
+def test_batched_proxy_matches_per_motion_calls():
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 12, w.bound)
+    model = S.Model(w.program, params)
+    pts, q = w.make(seed=12, motions=6, points=800)
+    proxy = S.batched_proxy(model, pts, q, precision="fp32_exact")
+    for m in range(6):
+        mn, _ = model.predict_min_distance(pts.astype(np.float64), q[m, :6], q[m, 6:], precision="fp32_exact")
+        assert proxy(m) == mn
