@@ -497,7 +497,7 @@ static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t s
 
 cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st) {
     switch (a.N) {
-        case 256: return launch_pair_n<256>(a, num_sms, st);
+        case 256: return launch_fused_bf16_pp(a, num_sms, st);  // two tiles in flight (kernels_bf16_pp.cu)
         case 512: return launch_pair_n<512>(a, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
@@ -514,7 +514,7 @@ struct QNormX {
 __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N, int n_mb,
                                   const float* __restrict__ wq, const float* __restrict__ base_bias,
                                   const float* __restrict__ wx_slots, uint8_t* __restrict__ ext, const QNormX qn,
-                                  unsigned long long* keys, unsigned int* counters, int64_t n_keys) {
+                                  unsigned long long* keys, unsigned int* counters, int64_t n_keys, int pp_layout) {
     const int64_t m = blockIdx.x;
     const int slot = blockIdx.y;
     if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
@@ -542,9 +542,17 @@ __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N,
         split_bf16(wx[2 * N + n], h2, l2);
         const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
         __align__(16) __nv_bfloat16 v[16] = {bh, bl, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
-        const int nh = n / NH, wi = n % NH, r = wi / BR, rr = wi % BR;
-        const int64_t blob = ((m * n_mb + slot) * 2 + nh) * 2 + r;
-        uint8_t* base = ext + blob * BR * 32;
+        uint8_t* base;
+        int rr;
+        if (pp_layout) {  // width-256 ping-pong kernel: blobs [r] of N/2 rows
+            const int r = n / NH;
+            rr = n % NH;
+            base = ext + ((m * n_mb + slot) * 2 + r) * NH * 32;
+        } else {          // pair kernel: blobs [n-half][r] of N/4 rows
+            const int nh = n / NH, wi = n % NH, r = wi / BR;
+            rr = wi % BR;
+            base = ext + (((m * n_mb + slot) * 2 + nh) * 2 + r) * BR * 32;
+        }
         *reinterpret_cast<uint4*>(base + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
         *reinterpret_cast<uint4*>(base + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
     }
@@ -565,7 +573,7 @@ cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* 
     }
     dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
     motion_ext_kernel<<<grid, 256, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn,
-                                             keys_init, counters_init, n_keys);
+                                             keys_init, counters_init, n_keys, a.N == 256 ? 1 : 0);
     return cudaGetLastError();
 }
 

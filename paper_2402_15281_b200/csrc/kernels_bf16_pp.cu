@@ -1,0 +1,435 @@
+// kernels_bf16_pp.cu — K1 (bf16) for width 256: two tiles ping-ponging on a CTA pair.
+//
+// Same math and operand formats as kernels_bf16_pair.cu (K=16 extension slab for bias and
+// x-part, ReLU fused into the bf16 pack, fp32 output dot, packed-key min), but at width 256
+// a whole layer fits one MMA chain (M=256 per pair, N=256, K=16) and TMEM holds two
+// 256-column accumulators.  So each CTA pair keeps two tiles in flight (slots 0/1, each
+// with its own activation tile and TMEM accumulator): the tensor core runs layer l of one
+// slot while the epilogue warps drain the other slot's layer, and every weight slab is
+// fetched once and used by both slots.
+//
+// Per CTA (width 256): A[2] 2 x 64 KiB, A-ext[2] 2 x 4 KiB, weight ring 4 x 16 KiB (one
+// 64-wide K slab of this CTA's 128 B-rows each), extension ring 2 x 4 KiB.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "fused.cuh"
+#include "ptx.cuh"
+
+namespace svn {
+
+namespace pp {
+
+constexpr int N = 256;
+constexpr int TM = 128;                    // rows per CTA (tile = 256 rows per pair)
+constexpr int BR = N / 2;                  // B rows per CTA (M=256 x N=256 MMA: CTA r holds rows r*128..)
+constexpr int KSL = N / 64;                // K slabs per layer
+constexpr uint32_t A_SLAB = TM * 128;      // 16 KiB
+constexpr uint32_t A_BYTES = TM * N * 2;   // 64 KiB
+constexpr uint32_t AX_BYTES = TM * 32;     // 4 KiB
+constexpr uint32_t SLAB_B = BR * 128;      // 16 KiB
+constexpr uint32_t XCHUNK = BR * 32;       // 4 KiB
+constexpr int WSTAGES = 4;
+constexpr int XSTAGES = 2;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int COLS = N / 2;                // columns per epilogue thread
+constexpr uint32_t OFF_AX = 2 * A_BYTES;
+constexpr uint32_t OFF_W = OFF_AX + 2 * AX_BYTES;
+constexpr uint32_t OFF_X = OFF_W + WSTAGES * SLAB_B;
+constexpr uint32_t OFF_WO = OFF_X + XSTAGES * XCHUNK;
+constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
+constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
+constexpr uint32_t SMEM = OFF_BAR + 256;
+static_assert(SMEM <= 232448, "shared memory budget");
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&p);
+}
+__device__ __forceinline__ float bflo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bfhi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+__device__ __forceinline__ void split(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(x);
+    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, float z1, float z2) {
+    __nv_bfloat16 h0, l0, h1, l1, h2, l2;
+    split(z0, h0, l0);
+    split(z1, h1, l1);
+    split(z2, h2, l2);
+    const __nv_bfloat16 one = __float2bfloat16_rn(1.0f), zero = __float2bfloat16_rn(0.0f);
+    __align__(16) __nv_bfloat16 v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
+    *reinterpret_cast<uint4*>(ax + ext_offset(row, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
+    *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+}
+
+// 32 columns of one row: activation (+ Fig. 2 affine/residual) then bf16 store or output dot.
+__device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
+                                      uint8_t* A, const float* wo_s, float& dot) {
+    const int fl = ld.flags;
+    const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (!aff && !res && !last) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4 p;
+            if (act) {
+                p.x = pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]);
+                p.y = pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]);
+                p.z = pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]);
+                p.w = pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]);
+            } else {
+                p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
+                p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
+                p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
+                p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+            }
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
+        }
+        return;
+    }
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+    }
+    if (aff) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 s = __ldg(reinterpret_cast<const float4*>(ld.s + c0 + i));
+            const float4 t = __ldg(reinterpret_cast<const float4*>(ld.t + c0 + i));
+            v[i + 0] = fmaf(v[i + 0], s.x, t.x);
+            v[i + 1] = fmaf(v[i + 1], s.y, t.y);
+            v[i + 2] = fmaf(v[i + 2], s.z, t.z);
+            v[i + 3] = fmaf(v[i + 3], s.w, t.w);
+        }
+    }
+    if (res) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint4 o = *reinterpret_cast<const uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
+            v[8 * u + 0] += bflo(o.x);
+            v[8 * u + 1] += bfhi(o.x);
+            v[8 * u + 2] += bflo(o.y);
+            v[8 * u + 3] += bfhi(o.y);
+            v[8 * u + 4] += bflo(o.z);
+            v[8 * u + 5] += bfhi(o.z);
+            v[8 * u + 6] += bflo(o.w);
+            v[8 * u + 7] += bfhi(o.w);
+        }
+    }
+    if (last) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+            dot = fmaf(w.x, v[i + 0], dot);
+            dot = fmaf(w.y, v[i + 1], dot);
+            dot = fmaf(w.z, v[i + 2], dot);
+            dot = fmaf(w.w, v[i + 3], dot);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4 p;
+            p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
+            p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
+            p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
+            p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
+        }
+    }
+}
+
+}  // namespace pp
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
+    fused_bf16_pp_kernel(const __grid_constant__ FusedArgs a) {
+    using namespace pp;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* Abuf = smem;                      // [2][A_BYTES]
+    uint8_t* AX = smem + OFF_AX;               // [2][AX_BYTES]
+    uint8_t* wring = smem + OFF_W;
+    uint8_t* xring = smem + OFF_X;
+    float* wo_s = reinterpret_cast<float*>(smem + OFF_WO);
+    float* dotbuf = reinterpret_cast<float*>(smem + OFF_DOT);  // [slot][ch][TM]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* wfull = bars;                     // [WSTAGES] leader
+    uint64_t* wempty = wfull + WSTAGES;         // [WSTAGES] each CTA
+    uint64_t* xfull = wempty + WSTAGES;         // [XSTAGES] leader
+    uint64_t* xempty = xfull + XSTAGES;         // [XSTAGES] each CTA
+    uint64_t* d_full = xempty + XSTAGES;        // [2] each CTA: slot s accumulator ready
+    uint64_t* a_ready = d_full + 2;             // [2] leader: slot s drained + A_s/AX_s written (16 warps)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int L = a.L;
+    const int64_t pair = blockIdx.x >> 1;
+    const int64_t npairs = gridDim.x >> 1;
+    const int64_t T = pair < a.n_tiles ? (a.n_tiles - 1 - pair) / npairs + 1 : 0;  // tiles of this pair
+    const int64_t R = (T + 1) / 2;                                                   // rounds
+    auto tile_of = [&](int64_t j, int s) { return pair + (2 * j + s) * npairs; };
+    auto has = [&](int64_t j, int s) { return 2 * j + s < T; };
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();
+        for (int s = 0; s < WSTAGES; ++s) {
+            mbar_init(&wfull[s], 1);
+            mbar_init(&wempty[s], 1);
+        }
+        for (int s = 0; s < XSTAGES; ++s) {
+            mbar_init(&xfull[s], 1);
+            mbar_init(&xempty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&d_full[s], 1);
+            mbar_init(&a_ready[s], 2 * EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) wo_s[i] = a.wo[i];
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&a.tmap_w);
+        prefetch_tmap(&a.tmap_xm);
+        prefetch_tmap(&a.tmap_xq);
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------------ producer --
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            const uint32_t wfull0 = mapa_shared(smem_u32(wfull), 0), xfull0 = mapa_shared(smem_u32(xfull), 0);
+            int ws = 0, xs = 0;
+            uint32_t wph = 0, xph = 0;
+            for (int64_t j = 0; j < R; ++j) {
+                int64_t wrow = 0;  // slab index in the stream
+                for (int l = 0; l < L; ++l) {
+                    const LayerDev& ld = a.layer[l];
+                    if (ld.ext) {
+                        for (int s = 0; s < 2; ++s) {
+                            if (!has(j, s)) continue;
+                            int32_t motion, nrows;
+                            int64_t pbase, obase;
+                            tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
+                            mbar_wait(&xempty[xs], xph ^ 1u);
+                            if (rank == 0) mbar_arrive_expect_tx_local(&xfull[xs], 2 * XCHUNK);
+                            uint8_t* dst = xring + xs * XCHUNK;
+                            if (ld.ext == 2) {
+                                const int64_t blob = (static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + rank;
+                                tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * BR), xfull0 + xs * 8u, pol);
+                            } else {
+                                tma_load_2d_pair(dst, &a.tmap_xm, 0, static_cast<int32_t>(ld.ext_row + rank * BR),
+                                                 xfull0 + xs * 8u, pol);
+                            }
+                            if (++xs == XSTAGES) xs = 0, xph ^= 1u;
+                        }
+                    }
+                    if (l > 0) {
+                        for (int ks = 0; ks < KSL; ++ks, ++wrow) {
+                            mbar_wait(&wempty[ws], wph ^ 1u);
+                            if (rank == 0) mbar_arrive_expect_tx_local(&wfull[ws], 2 * SLAB_B);
+                            tma_load_2d_pair(wring + ws * SLAB_B, &a.tmap_w, 0,
+                                             static_cast<int32_t>((wrow * 2 + rank) * BR), wfull0 + ws * 8u, pol);
+                            if (++ws == WSTAGES) ws = 0, wph ^= 1u;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer --
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_bf16(2 * TM, N);
+            const uint32_t a_base = smem_u32(Abuf), ax_base = smem_u32(AX), w_base = smem_u32(wring);
+            const uint32_t x_base = smem_u32(xring);
+            int ws = 0, xs = 0;
+            uint32_t wph = 0, xph = 0;
+            uint32_t ar_ph[2] = {0u, 0u};
+            for (int64_t j = 0; j < R; ++j) {
+                for (int l = 0; l < L; ++l) {
+                    const LayerDev& ld = a.layer[l];
+                    const int ws_layer = ws;  // ring slot of this layer's slab 0
+                    const uint32_t wph_layer = wph;
+                    const int nslots = has(j, 1) ? 2 : 1;
+                    for (int s = 0; s < nslots; ++s) {
+                        mbar_wait(&a_ready[s], ar_ph[s]);  // D_s drained, A_s / AX_s written
+                        ar_ph[s] ^= 1u;
+                        tc_fence_after();
+                        const uint32_t d_addr = tmem + static_cast<uint32_t>(s * N);
+                        bool acc = false;
+                        if (ld.ext) {
+                            mbar_wait(&xfull[xs], xph);
+                            tc_fence_after();
+                            mma_bf16_pair(d_addr, noswz_desc(ax_base + s * AX_BYTES, 128, 256),
+                                          noswz_desc(x_base + xs * XCHUNK, 128, 256), idesc, 0u);
+                            mma_commit_pair(&xempty[xs], 3);
+                            if (++xs == XSTAGES) xs = 0, xph ^= 1u;
+                            acc = true;
+                        }
+                        if (l > 0) {
+                            int st = ws_layer;
+                            uint32_t ph = wph_layer;
+                            for (int ks = 0; ks < KSL; ++ks) {
+                                if (s == 0) {
+                                    mbar_wait(&wfull[st], ph);
+                                    tc_fence_after();
+                                }
+                                const uint32_t a_slab = a_base + s * A_BYTES + ks * A_SLAB;
+                                const uint32_t b_slab = w_base + st * SLAB_B;
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk)
+                                    mma_bf16_pair(d_addr, sw128_desc(a_slab + kk * 32), sw128_desc(b_slab + kk * 32),
+                                                  idesc, (acc || ks || kk) ? 1u : 0u);
+                                if (s == nslots - 1) mma_commit_pair(&wempty[st], 3);  // last user frees the slab
+                                if (++st == WSTAGES) st = 0, ph ^= 1u;
+                            }
+                        }
+                        mma_commit_pair(&d_full[s], 3);
+                    }
+                    if (l > 0)
+                        for (int ks = 0; ks < KSL; ++ks)
+                            if (++ws == WSTAGES) ws = 0, wph ^= 1u;
+                }
+            }
+        }
+    } else {
+        // ------------------------------------------------------------------ epilogue --
+        const int e = warp - 2;
+        const uint32_t quad = static_cast<uint32_t>(warp & 3);
+        const int ch = e >> 2;
+        const uint32_t row = quad * 32 + lane;
+        const uint32_t t_lane = (quad * 32u) << 16;
+        const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
+        uint32_t dp[2] = {0u, 0u};
+        auto write_ax_for = [&](int64_t t, int s) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+            const int32_t r = static_cast<int32_t>(rank * TM + row);
+            const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
+            if (ch == 0) {
+                const float z0 = (xp[0] - a.shift[0]) * a.scale[0];
+                const float z1 = (xp[1] - a.shift[1]) * a.scale[1];
+                const float z2 = (xp[2] - a.shift[2]) * a.scale[2];
+                write_ax(AX + s * AX_BYTES, row, z0, z1, z2);
+            }
+        };
+        struct Pending {
+            bool live;
+            int32_t motion, rr;
+            int64_t pbase, obase;
+            bool valid;
+        } pend[2] = {{false, 0, 0, 0, 0, false}, {false, 0, 0, 0, 0, false}};
+        auto flush = [&](int s) {
+            if (!pend[s].live) return;
+            named_bar_sync(1 + s, EPI_WARPS * 32);
+            if (ch == 0) {
+                const Pending& p = pend[s];
+                const float delta = (dotbuf[(s * 2) * TM + row] + dotbuf[(s * 2 + 1) * TM + row]) + a.bo;
+                if (p.valid && a.per_point) a.per_point[p.obase + p.rr] = delta;
+                if (a.keys) {
+                    unsigned long long key = p.valid ? row_key(delta, a.index_offset + p.pbase + p.rr) : ~0ull;
+                    key = warp_min_u64(key);
+                    if (lane == 0) atomicMin(a.keys + p.motion, key);
+                    named_bar_sync(3 + s, 4 * 32);
+                    if (e == 0 && lane == 0 && a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + p.motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                            __threadfence();
+                            const unsigned long long kk = atomicOr(a.keys + p.motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + p.motion, a.argmin_out + p.motion,
+                                       a.free_out + p.motion);
+                        }
+                    }
+                }
+            }
+            pend[s].live = false;
+        };
+        // round 0: A extensions of both slots, then the initial "slot free" arrivals
+        for (int s = 0; s < 2; ++s) {
+            if (has(0, s)) write_ax_for(tile_of(0, s), s);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
+        }
+        float dot[2] = {0.f, 0.f};
+        for (int64_t j = 0; j < R; ++j) {
+            const int nslots = has(j, 1) ? 2 : 1;
+            for (int l = 0; l < L; ++l) {
+                const LayerDev& ld = a.layer[l];
+                const bool last = (l == L - 1);
+                for (int s = 0; s < nslots; ++s) {
+                    uint8_t* A = Abuf + s * A_BYTES;
+                    mbar_wait(&d_full[s], dp[s]);
+                    dp[s] ^= 1u;
+                    tc_fence_after();
+                    const int c0c = ch * COLS;
+                    constexpr int NCH = COLS / 32;
+                    uint32_t ra[32], rb[32];
+                    const uint32_t tbase = tmem + t_lane + static_cast<uint32_t>(s * N);
+                    tmem_ld32_async(tbase + static_cast<uint32_t>(c0c), ra);
+                    tmem_wait_tied(ra);
+#pragma unroll
+                    for (int q = 0; q < NCH; ++q) {
+                        uint32_t(&cur)[32] = (q & 1) ? rb : ra;
+                        uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
+                        if (q + 1 < NCH) tmem_ld32_async(tbase + static_cast<uint32_t>(c0c + 32 * (q + 1)), nxt);
+                        epi32(ld, l, last, reinterpret_cast<float*>(cur), c0c + 32 * q, row, A, wo_s, dot[s]);
+                        if (q + 1 < NCH) tmem_wait_tied(nxt);
+                    }
+                    if (last) {
+                        // this slot's tile is done: stash the dot, load the next tile's A extension
+                        dotbuf[(s * 2 + ch) * TM + row] = dot[s];
+                        dot[s] = 0.f;
+                        int32_t motion, nrows;
+                        int64_t pbase, obase;
+                        tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
+                        const int32_t rr = static_cast<int32_t>(rank * TM + row);
+                        pend[s] = Pending{true, motion, rr, pbase, obase, rr < nrows};
+                        if (has(j + 1, s)) write_ax_for(tile_of(j + 1, s), s);
+                    }
+                    tc_fence_before();
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
+                    if (l == 0 && j > 0) flush(s);  // previous round's outputs, off the critical path
+                }
+            }
+        }
+        flush(0);
+        flush(1);
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_pair(tmem, 512);
+}
+
+cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e =
+            cudaFuncSetAttribute(fused_bf16_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int64_t pairs = num_sms / 2;
+    const int64_t need = (a.n_tiles + 1) / 2;  // two tiles in flight per pair
+    if (need < pairs) pairs = need;
+    if (pairs < 1) return cudaSuccess;
+    fused_bf16_pp_kernel<<<static_cast<unsigned>(2 * pairs), pp::THREADS, pp::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace svn

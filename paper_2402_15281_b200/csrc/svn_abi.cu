@@ -353,7 +353,20 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         size_t pos = 0;
         for (int l = 0; l < L; ++l) {
             const int K = layer_k(d->layers, l, N, in);
-            if (l > 0) {
+            if (l > 0 && N == 256) {
+                // ping-pong kernel (width 256): per layer 4 K slabs, each [CTA r: 128 rows] x 64 k
+                for (int ks = 0; ks < N / 64; ++ks)
+                    for (int r = 0; r < 2; ++r) {
+                        uint8_t* blob = reinterpret_cast<uint8_t*>(ws.data() + pos);
+                        for (int nr = 0; nr < 128; ++nr)
+                            for (int kc = 0; kc < 64; ++kc) {
+                                const int n = r * 128 + nr, k = ks * 64 + kc;
+                                *reinterpret_cast<__nv_bfloat16*>(blob + sw128_offset(nr, kc, 128)) =
+                                    __float2bfloat16_rn(Wl[static_cast<int64_t>(k) * N + n]);
+                            }
+                        pos += 128 * 64;
+                    }
+            } else if (l > 0) {
                 for (int step = 0; step < 4; ++step) {
                     const int nh = step & 1, kh = step >> 1;
                     for (int ks = 0; ks < KSL; ++ks) {
@@ -376,7 +389,7 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         a.wstream = dws;
         // CTA-pair kernel: TMA views of the weight stream and of the model-constant
         // K=16 extension rows (bias hi/lo of non-concat layers with a nonzero bias).
-        const int BR = N / 4;
+        const int BR = N == 256 ? N / 2 : N / 4;  // B rows per CTA per TMA box (128 for both kernels)
         if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return cleanup_fail(st);
         std::vector<uint8_t> xm;
         const float* Wb = params + 2 * in;
@@ -394,8 +407,16 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
                 const size_t base = xm.size();
                 xm.resize(base + static_cast<size_t>(N) * 32, 0);
                 for (int n = 0; n < N; ++n) {
-                    const int nh = n / (N / 2), wi = n % (N / 2), r = wi / BR, rr = wi % BR;
-                    uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * BR) * 32;
+                    int blob_i, rr;
+                    if (N == 256) {  // ping-pong layout: blobs [r] of N/2 rows
+                        blob_i = n / BR;
+                        rr = n % BR;
+                    } else {         // pair layout: blobs [n-half][r] of N/4 rows
+                        const int nh = n / (N / 2), wi = n % (N / 2);
+                        blob_i = nh * 2 + wi / BR;
+                        rr = wi % BR;
+                    }
+                    uint8_t* blob = xm.data() + base + static_cast<size_t>(blob_i * BR) * 32;
                     __nv_bfloat16 hi, lo;
                     split_bf16_host(b[n], hi, lo);
                     *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 0)) = hi;
@@ -508,7 +529,7 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
     uint8_t* ext = nullptr;
     const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * m->N;
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
-    svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N / 4));
+    svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N == 256 ? m->N / 2 : m->N / 4));
     if (s != SVN_OK) return s;
     SVN_CUDA(launch_motion_ext(a, m->d_wq, m->d_mbbase, m->d_wxslots, ext, keys, counters, n_keys, st),
              "motion_ext kernel");
