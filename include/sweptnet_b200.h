@@ -15,6 +15,7 @@
  *                             collision.cpp:63-69) and eval_classification (bench.cpp:98-124):
  *                             predict_min_distance over M motions + `proxy > margin` in one call
  *   svn_query_min_keys_device point-sharded partial of the above (new)
+ *   svn_eval_grid             NN branch of cmd_reconstruct  src/cli.cpp:240-261
  *   svn_keys_finalize_device  decode + margin classification of reduced keys (new)
  *   svn_last_error            std::invalid_argument / IoError what() strings (nn.cpp:98-99,462,465;
  *                             errors.hpp:8-27)
@@ -153,6 +154,15 @@ SVN_API svn_status svn_forward_eval_device(const svn_model* model, svn_precision
 SVN_API svn_status svn_predict_min_distance(const svn_model* model, svn_precision prec, const double* cloud,
                                             int64_t P, const double* q0, const double* q1, int32_t dof,
                                             double* min_out, int32_t* argmin_out);
+
+/* Dense-grid evaluation for NN reconstruction (cmd_reconstruct, cli.cpp:240-261): voxel
+ * centres origin + voxel_size * (ix, iy, iz) (SdfGrid::voxel_center, sweptvol.hpp:73-75)
+ * are generated on the device in double, cast to float, and every centre is evaluated
+ * for the single motion (q0, q1).  values: HOST float [dims[0] * dims[1] * dims[2]] in
+ * (ix, iy, iz) row-major order, the order of SdfGrid::values. */
+SVN_API svn_status svn_eval_grid(const svn_model* model, svn_precision prec, const double* origin, double voxel_size,
+                                 const int32_t* dims, const double* q0, const double* q1, int32_t dof,
+                                 float* values);
 
 /* Kernel launches issued by this thread since the last reset (evidence for bench.py). */
 SVN_API int64_t svn_launch_count(void);

@@ -122,6 +122,18 @@ class Model:
                                                      C.byref(mn), C.byref(am)))
         return mn.value, am.value
 
+    def eval_grid(self, origin, voxel_size: float, dims, q0, q1, precision: str = "fp32_exact") -> np.ndarray:
+        """NN branch of cmd_reconstruct (cli.cpp:240-261): every voxel centre of the grid
+        for one motion; returns float32 [dx, dy, dz] (SdfGrid::values order)."""
+        o = np.ascontiguousarray(origin, np.float64).reshape(3)
+        d = np.ascontiguousarray(dims, np.int32).reshape(3)
+        q0 = np.ascontiguousarray(q0, np.float64).reshape(-1)
+        q1 = np.ascontiguousarray(q1, np.float64).reshape(-1)
+        out = np.empty(int(np.prod(d.astype(np.int64))), np.float32)
+        abi.check(abi.lib().svn_eval_grid(self._h, abi.PRECISIONS[precision], abi.ptr(o), float(voxel_size),
+                                          abi.ptr(d), abi.ptr(q0), abi.ptr(q1), q0.size, abi.ptr(out)))
+        return out.reshape(tuple(int(x) for x in d))
+
     # ---------------------------------------------------------- device entry --
     def query_min_device(self, points, q01, margin: float, min_out, argmin_out, free_out, per_point=None,
                          precision: str = "bf16", stream=None) -> None:

@@ -321,3 +321,28 @@ cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st) 
 }
 
 }  // namespace svn
+
+namespace svn {
+
+// Voxel centres for dense-grid evaluation (SdfGrid::voxel_center, sweptvol.hpp:73-75):
+// c = origin + voxel_size * i per axis, in double (contracted to one fma, as GCC emits for
+// the reference's -march=native build), then cast to float like nn.cpp:469-471.
+__global__ void grid_points_kernel(double ox, double oy, double oz, double vs, int dy, int dz, int64_t n,
+                                   float* __restrict__ pts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int64_t iz = i % dz, iy = (i / dz) % dy, ix = i / (static_cast<int64_t>(dz) * dy);
+    pts[3 * i + 0] = static_cast<float>(fma(vs, static_cast<double>(ix), ox));
+    pts[3 * i + 1] = static_cast<float>(fma(vs, static_cast<double>(iy), oy));
+    pts[3 * i + 2] = static_cast<float>(fma(vs, static_cast<double>(iz), oz));
+}
+
+cudaError_t launch_grid_points(const double* origin, double voxel, const int32_t* dims, float* pts, cudaStream_t st) {
+    const int64_t n = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+    if (n <= 0) return cudaSuccess;
+    grid_points_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(origin[0], origin[1], origin[2], voxel,
+                                                                               dims[1], dims[2], n, pts);
+    return cudaGetLastError();
+}
+
+}  // namespace svn

@@ -808,6 +808,43 @@ SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision pr
     return SVN_OK;
 }
 
+SVN_API svn_status svn_eval_grid(const svn_model* m, svn_precision prec, const double* origin, double voxel_size,
+                                 const int32_t* dims, const double* q0, const double* q1, int32_t dof, float* values) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null model");
+    if (!origin || !dims || !q0 || !q1 || !values) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null buffer");
+    if (3 + 2 * dof != m->in)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: q0/q1 must have one angle per joint");
+    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || !(voxel_size > 0))
+        return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: empty grid");
+    const int64_t P = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    std::vector<float> q(static_cast<size_t>(2 * dof));
+    for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
+    for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+    {
+        Scratch sc(st);
+        float *dp = nullptr, *dq = nullptr, *dmin = nullptr, *dvals = nullptr;
+        int32_t* darg = nullptr;
+        uint8_t* dfree = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * P), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * q.size()), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dmin), sizeof(float)), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&darg), sizeof(int32_t)), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dfree), 1), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dvals), sizeof(float) * P), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(dq, q.data(), sizeof(float) * q.size(), cudaMemcpyHostToDevice, st), "H2D q");
+        SVN_CUDA(launch_grid_points(origin, voxel_size, dims, dp, st), "grid_points kernel");
+        ++g_launches;
+        svn_status s = query_dense(m, prec, dp, P, 0, dq, 1, 0.0, dmin, darg, dfree, dvals, nullptr, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(values, dvals, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "D2H values");
+        SVN_CUDA(cudaStreamSynchronize(st), "eval_grid");
+    }
+    return SVN_OK;
+}
+
 // SVCKPT01 (nn.cpp:482-576): magic, u32 {version, n_blocks, block_dim, input_dim},
 // then the Fig. 2 parameter body; strict trailing-byte check.
 SVN_API svn_status svn_model_load_checkpoint(const char* path, int32_t device, svn_model** out) {

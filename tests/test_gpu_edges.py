@@ -136,3 +136,29 @@ def test_batched_proxy_matches_per_motion_calls():
     for m in range(6):
         mn, _ = model.predict_min_distance(pts.astype(np.float64), q[m, :6], q[m, 6:], precision="fp32_exact")
         assert proxy(m) == mn
+
+
+def _fma(a, b, c):
+    from fractions import Fraction
+    return float(Fraction(a) * Fraction(b) + Fraction(c))
+
+
+@pytest.mark.parametrize("prec", ["fp32_exact", "bf16"])
+def test_eval_grid_matches_reference_reconstruction(prec):
+    """cmd_reconstruct NN branch (cli.cpp:240-261): voxel centres in (ix, iy, iz) order."""
+    w = WORKLOADS["c3"] if prec == "bf16" else WORKLOADS["c2"]
+    params = S.init_params(w.program, 13, w.bound)
+    model = S.Model(w.program, params)
+    origin, vs, dims = np.array([-0.31, -0.47, 0.05]), 0.0371, (9, 11, 13)
+    q0 = np.linspace(-1.0, 1.0, 6)
+    q1 = np.linspace(0.5, -0.7, 6)
+    grid = model.eval_grid(origin, vs, dims, q0, q1, precision=prec)
+    cen = np.array([[_fma(vs, float(i), origin[0]), _fma(vs, float(j), origin[1]), _fma(vs, float(k), origin[2])]
+                    for i in range(dims[0]) for j in range(dims[1]) for k in range(dims[2])], np.float64)
+    raw = np.concatenate([cen.astype(np.float32), np.repeat(np.concatenate([q0, q1])[None], len(cen), 0)],
+                         axis=1).astype(np.float32)
+    ref = O.forward_eval(w.program, params, raw).reshape(dims)
+    if prec == "fp32_exact":
+        assert np.array_equal(grid, ref)
+    else:
+        assert np.abs(grid.astype(np.float64) - ref).max() <= BF16_BOUND[w.program.name]
