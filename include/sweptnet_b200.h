@@ -16,6 +16,7 @@
  *                             predict_min_distance over M motions + `proxy > margin` in one call
  *   svn_query_min_keys_device point-sharded partial of the above (new)
  *   svn_eval_grid             NN branch of cmd_reconstruct  src/cli.cpp:240-261
+ *   svn_gcc_min_distance      gcc_min_distance / gcc_clearance  src/collision.cpp:18-34
  *   svn_keys_finalize_device  decode + margin classification of reduced keys (new)
  *   svn_last_error            std::invalid_argument / IoError what() strings (nn.cpp:98-99,462,465;
  *                             errors.hpp:8-27)
@@ -163,6 +164,43 @@ SVN_API svn_status svn_predict_min_distance(const svn_model* model, svn_precisio
 SVN_API svn_status svn_eval_grid(const svn_model* model, svn_precision prec, const double* origin, double voxel_size,
                                  const int32_t* dims, const double* q0, const double* q1, int32_t dof,
                                  float* values);
+
+/* ------------------------------------------------ geometric checker (GCC) --
+ * The exact swept-volume clearance the proxy is checked against:
+ * for each motion, min over points and over the `steps` configurations of
+ * discretize(m, steps) (sweptvol.cpp:22-46) of the signed distance to the posed link
+ * capsules (forward_kinematics robot.cpp:48-67, sdf_capsule geometry.cpp:29-36), with
+ * the bounding-sphere skip of SweptCapsules::sdf (sweptvol.cpp:73-84); double precision.
+ *   dist_out[m] = gcc_min_distance (collision.cpp:18-24)
+ *   free_out[m] = dist_out[m] > margin = gcc_clearance(...).free (collision.cpp:26-34) */
+typedef struct {
+    double axis[3];   /* unit rotation axis in the parent frame (Joint::axis, robot.hpp:15) */
+    double offset[3]; /* translation after the rotation (Joint::offset, robot.hpp:16) */
+} svn_joint;
+
+typedef struct {
+    int32_t link; /* link index; capsules sorted by link (link-major, robot.cpp:62-67) */
+    int32_t pad;
+    double a[3], b[3]; /* segment end points in the link frame */
+    double radius;
+} svn_capsule;
+
+typedef struct {
+    int32_t dof;              /* 1..16 */
+    const svn_joint* joints;  /* [dof] */
+    int32_t n_capsules;       /* 1..64 */
+    const svn_capsule* capsules;
+    const double* base_pose;  /* 3x4 row-major isometry, NULL = identity (robot.hpp:26) */
+} svn_robot_desc;
+
+/* HOST buffers: points double [P x 3], q01 double [M x 2 dof]; outputs [M]. */
+SVN_API svn_status svn_gcc_min_distance(const svn_robot_desc* robot, const double* points, int64_t P,
+                                        const double* q01, int64_t M, int32_t steps, double margin, int32_t device,
+                                        double* dist_out, uint8_t* free_out);
+/* DEVICE buffers on `stream`. */
+SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, const double* points, int64_t P,
+                                               const double* q01, int64_t M, int32_t steps, double margin,
+                                               double* dist_out, uint8_t* free_out, void* stream);
 
 /* Kernel launches issued by this thread since the last reset (evidence for bench.py). */
 SVN_API int64_t svn_launch_count(void);

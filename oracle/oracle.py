@@ -58,6 +58,7 @@ def lib(path: Path | None = None) -> C.CDLL:
     L.oracle_forward_eval_f32.argtypes = [VP, I32, I32, I32, VP, VP, I64, I64, VP]
     L.oracle_forward_eval_f64.argtypes = [VP, I32, I32, I32, VP, VP, I64, I64, VP]
     L.oracle_predict_min_distance.argtypes = [VP, I32, I32, I32, VP, VP, I64, VP, VP, I32, VP, VP]
+    L.oracle_gcc.argtypes = [VP, I32, VP, I32, VP, VP, I64, VP, I64, I32, C.c_double, I32, I32, VP, VP]
     L.oracle_query_min.argtypes = [VP, I32, I32, I32, VP, VP, I64, VP, I64, C.c_double, VP, VP, VP, VP, I32]
     if path is None:
         _lib = L
@@ -135,3 +136,20 @@ def query_min(program, params, points, q01, margin, per_point=False, threads=1, 
     if rc:
         raise ValueError("query_min: empty input")
     return mn, am, fr.astype(bool), pp
+
+
+def gcc(robot, points, q01, steps=200, margin=0.005, early_exit=False, prune=True, library=None):
+    """gcc_min_distance (early_exit False) / gcc_clearance (True) per motion -> (dist, free)."""
+    pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(q01, np.float64).reshape(-1, 2 * robot.dof)
+    j = robot.joints_flat()
+    c = robot.capsules_flat()
+    base = np.ascontiguousarray(robot.base_pose, np.float64).reshape(-1)
+    M = q.shape[0]
+    dist = np.empty(M, np.float64)
+    free = np.empty(M, np.uint8)
+    rc = (library or lib()).oracle_gcc(_p(j), robot.dof, _p(c), c.shape[0], _p(base), _p(pts), pts.shape[0], _p(q),
+                                       M, int(steps), float(margin), int(early_exit), int(prune), _p(dist), _p(free))
+    if rc:
+        raise ValueError("gcc: invalid arguments")
+    return dist, free.astype(bool)

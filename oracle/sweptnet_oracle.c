@@ -493,3 +493,190 @@ OR_API int oracle_query_min(const int* flags, int L, int N, int dof, const float
     free(m.fold);
     return 0;
 }
+
+/* ================================================================ GCC -- */
+/* Geometric collision checker restated (the ground truth the proxy is checked
+ * against):
+ *   discretize                  src/sweptvol.cpp:22-46
+ *   forward_kinematics          src/robot.cpp:48-60 (Eigen AngleAxis / Isometry3d)
+ *   pose_link_capsules          src/robot.cpp:62-67
+ *   pose_swept_capsules bounds  src/sweptvol.cpp:48-71
+ *   SweptCapsules::sdf          src/sweptvol.cpp:73-84 (bounding-sphere pruning)
+ *   sdf_capsule                 src/geometry.cpp:29-36
+ *   gcc_min_distance            src/collision.cpp:18-24
+ *   gcc_clearance               src/collision.cpp:26-34
+ * Double precision throughout, as the reference.  Multiply-adds inside one
+ * expression are written as fma() (the reference's GCC -ffp-contract=fast build);
+ * the CUDA checker uses the same formulas. */
+typedef struct {
+    double axis[3], offset[3];
+} or_joint;
+typedef struct {
+    int32_t link;
+    double a[3], b[3], r;
+} or_capsule;
+
+/* Eigen AngleAxis<double>::toRotationMatrix (Rodrigues), row-major R[9]. */
+static void or_angle_axis(double ang, const double* ax, double* R) {
+    const double s = sin(ang), c = cos(ang), c1 = 1.0 - c;
+    const double sa0 = s * ax[0], sa1 = s * ax[1], sa2 = s * ax[2];
+    const double ca0 = c1 * ax[0], ca1 = c1 * ax[1], ca2 = c1 * ax[2];
+    double tmp;
+    tmp = ca0 * ax[1];
+    R[1] = tmp - sa2;
+    R[3] = tmp + sa2;
+    tmp = ca0 * ax[2];
+    R[2] = tmp + sa1;
+    R[6] = tmp - sa1;
+    tmp = ca1 * ax[2];
+    R[5] = tmp - sa0;
+    R[7] = tmp + sa0;
+    R[0] = fma(ca0, ax[0], c);
+    R[4] = fma(ca1, ax[1], c);
+    R[8] = fma(ca2, ax[2], c);
+}
+
+static double or_dot3(const double* u, const double* v) { return fma(u[2], v[2], fma(u[1], v[1], u[0] * v[0])); }
+
+/* y = R x + p */
+static void or_apply(const double* R, const double* p, const double* x, double* y) {
+    for (int i = 0; i < 3; ++i) y[i] = fma(R[3 * i + 2], x[2], fma(R[3 * i + 1], x[1], fma(R[3 * i], x[0], p[i])));
+}
+
+/* sdf_capsule (geometry.cpp:29-36) */
+static double or_sdf_capsule(const double* x, const double* a, const double* b, double r) {
+    double pa[3], ba[3];
+    for (int k = 0; k < 3; ++k) {
+        pa[k] = x[k] - a[k];
+        ba[k] = b[k] - a[k];
+    }
+    const double bb = or_dot3(ba, ba);
+    if (bb == 0.0) return sqrt(or_dot3(pa, pa)) - r;
+    double t = or_dot3(pa, ba) / bb;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    double d[3];
+    for (int k = 0; k < 3; ++k) d[k] = fma(-t, ba[k], pa[k]);
+    return sqrt(or_dot3(d, d)) - r;
+}
+
+/* Posed sweep of one motion: caps [steps][ncap] (a, b, r) and bounds [steps] (c, R). */
+static void or_pose_sweep(const or_joint* J, int dof, const or_capsule* caps, int ncap, const double* base,
+                          const double* q0, const double* q1, int steps, double* pc, double* bounds) {
+    double q[64];
+    const double denom = steps - 1;
+    for (int i = 0; i < steps; ++i) {
+        for (int c = 0; c < dof; ++c) {
+            if (q0[c] == q1[c] || i == 0)
+                q[c] = q0[c];
+            else if (i == steps - 1)
+                q[c] = q1[c];
+            else
+                q[c] = fma((double)i, q1[c], (double)(steps - 1 - i) * q0[c]) / denom; /* sweptvol.cpp:40 */
+        }
+        /* forward kinematics: T = base; T = T * rot(axis_j, q_j) * trans(offset_j) */
+        double Rt[9], pt[3];
+        for (int k = 0; k < 9; ++k) Rt[k] = base[(k / 3) * 4 + (k % 3)];
+        for (int k = 0; k < 3; ++k) pt[k] = base[k * 4 + 3];
+        int ci = 0;
+        double* out = pc + (size_t)i * ncap * 7;
+        for (int j = 0; j < dof; ++j) {
+            double R[9], M[9];
+            or_angle_axis(q[j], J[j].axis, R);
+            for (int r = 0; r < 3; ++r)
+                for (int cc = 0; cc < 3; ++cc)
+                    M[3 * r + cc] = fma(Rt[3 * r + 2], R[6 + cc], fma(Rt[3 * r + 1], R[3 + cc], Rt[3 * r] * R[cc]));
+            memcpy(Rt, M, sizeof(M));
+            double np[3];
+            or_apply(Rt, pt, J[j].offset, np);
+            memcpy(pt, np, sizeof(np));
+            for (; ci < ncap && caps[ci].link == j; ++ci) {
+                or_apply(Rt, pt, caps[ci].a, out + 7 * ci);
+                or_apply(Rt, pt, caps[ci].b, out + 7 * ci + 3);
+                out[7 * ci + 6] = caps[ci].r;
+            }
+        }
+        /* bounding sphere (sweptvol.cpp:57-67) */
+        double cen[3] = {0, 0, 0};
+        for (int k = 0; k < ncap; ++k)
+            for (int d = 0; d < 3; ++d) cen[d] += out[7 * k + d] + out[7 * k + 3 + d];
+        for (int d = 0; d < 3; ++d) cen[d] /= 2.0 * ncap;
+        double rad = 0;
+        for (int k = 0; k < ncap; ++k) {
+            double da[3], db[3];
+            for (int d = 0; d < 3; ++d) {
+                da[d] = out[7 * k + d] - cen[d];
+                db[d] = out[7 * k + 3 + d] - cen[d];
+            }
+            const double na = sqrt(or_dot3(da, da)), nb = sqrt(or_dot3(db, db));
+            const double e = (na > nb ? na : nb) + out[7 * k + 6];
+            rad = rad > e ? rad : e;
+        }
+        bounds[4 * i + 0] = cen[0];
+        bounds[4 * i + 1] = cen[1];
+        bounds[4 * i + 2] = cen[2];
+        bounds[4 * i + 3] = rad;
+    }
+}
+
+/* SweptCapsules::sdf with the 1e-9-slack bounding-sphere skip (sweptvol.cpp:73-84). */
+static double or_sweep_sdf(const double* pc, const double* bounds, int steps, int ncap, const double* x, int prune) {
+    double best = INFINITY;
+    for (int i = 0; i < steps; ++i) {
+        double d[3] = {x[0] - bounds[4 * i], x[1] - bounds[4 * i + 1], x[2] - bounds[4 * i + 2]};
+        const double lb = sqrt(or_dot3(d, d)) - bounds[4 * i + 3];
+        if (prune && lb - 1e-9 > best) continue;
+        const double* c = pc + (size_t)i * ncap * 7;
+        for (int k = 0; k < ncap; ++k) {
+            const double v = or_sdf_capsule(x, c + 7 * k, c + 7 * k + 3, c[7 * k + 6]);
+            best = v < best ? v : best;
+        }
+    }
+    return best;
+}
+
+/* gcc_min_distance (early_exit = 0) or gcc_clearance (early_exit = 1) for M motions.
+ * joints: [dof] {axis, offset}; caps: [ncap] {link, a, b, r}, link-major; base: 3x4
+ * row-major isometry; points double [P x 3]; q01 double [M x 2 dof].  Outputs per motion
+ * the distance (exact min, or the clearance scan's value) and free = value > margin. */
+OR_API int oracle_gcc(const double* joints, int dof, const double* caps_flat, int ncap, const double* base,
+                      const double* points, int64_t P, const double* q01, int64_t M, int steps, double margin,
+                      int early_exit, int prune, double* dist_out, uint8_t* free_out) {
+    if (P < 1 || steps < 2 || dof < 1 || dof > 64 || ncap < 1) return 1;
+    or_joint* J = (or_joint*)malloc(sizeof(or_joint) * (size_t)dof);
+    or_capsule* C = (or_capsule*)malloc(sizeof(or_capsule) * (size_t)ncap);
+    for (int j = 0; j < dof; ++j)
+        for (int k = 0; k < 3; ++k) {
+            J[j].axis[k] = joints[6 * j + k];
+            J[j].offset[k] = joints[6 * j + 3 + k];
+        }
+    for (int c = 0; c < ncap; ++c) {
+        C[c].link = (int32_t)caps_flat[8 * c];
+        for (int k = 0; k < 3; ++k) {
+            C[c].a[k] = caps_flat[8 * c + 1 + k];
+            C[c].b[k] = caps_flat[8 * c + 4 + k];
+        }
+        C[c].r = caps_flat[8 * c + 7];
+    }
+    double* pc = (double*)malloc(sizeof(double) * (size_t)steps * ncap * 7);
+    double* bounds = (double*)malloc(sizeof(double) * (size_t)steps * 4);
+    for (int64_t m = 0; m < M; ++m) {
+        or_pose_sweep(J, dof, C, ncap, base, q01 + m * 2 * dof, q01 + m * 2 * dof + dof, steps, pc, bounds);
+        double best = INFINITY;
+        int free = 1;
+        for (int64_t p = 0; p < P; ++p) {
+            const double v = or_sweep_sdf(pc, bounds, steps, ncap, points + 3 * p, prune);
+            best = v < best ? v : best;
+            if (early_exit && best <= margin) {
+                free = 0;
+                break;
+            }
+        }
+        dist_out[m] = best;
+        free_out[m] = early_exit ? (uint8_t)free : (uint8_t)(best > margin);
+    }
+    free(J);
+    free(C);
+    free(pc);
+    free(bounds);
+    return 0;
+}

@@ -100,6 +100,8 @@ def _finish(L):
         "svn_forward_eval_device": (C.c_int, [VP, C.c_int, P, I64, I64, P, VP]),
         "svn_predict_min_distance": (C.c_int, [VP, C.c_int, P, I64, P, P, I32, P, P]),
         "svn_eval_grid": (C.c_int, [VP, C.c_int, P, D, P, P, P, I32, P]),
+        "svn_gcc_min_distance": (C.c_int, [P, P, I64, P, I64, I32, D, I32, P, P]),
+        "svn_gcc_min_distance_device": (C.c_int, [P, P, I64, P, I64, I32, D, P, P, VP]),
         "svn_launch_count": (I64, []),
         "svn_launch_count_reset": (None, []),
         "svn_kernel_timing_begin": (None, []),
@@ -118,7 +120,8 @@ def _finish(L):
 EXPORTED = ("svn_param_count", "svn_trainable_param_count", "svn_init_params", "svn_model_create",
             "svn_model_load_checkpoint", "svn_model_destroy", "svn_query_min_device", "svn_query_min",
             "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
-            "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_launch_count",
+            "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_gcc_min_distance",
+            "svn_gcc_min_distance_device", "svn_launch_count",
             "svn_launch_count_reset",
             "svn_kernel_timing_begin", "svn_kernel_timing_end", "svn_last_error", "svn_version")
 

@@ -22,6 +22,7 @@
 
 #include "../../include/sweptnet_b200.h"
 #include "fused.cuh"
+#include "gcc.cuh"
 #include "ptx.cuh"
 
 using namespace svn;
@@ -842,6 +843,92 @@ SVN_API svn_status svn_eval_grid(const svn_model* m, svn_precision prec, const d
         SVN_CUDA(cudaMemcpyAsync(values, dvals, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "D2H values");
         SVN_CUDA(cudaStreamSynchronize(st), "eval_grid");
     }
+    return SVN_OK;
+}
+
+static svn_status gcc_args(const svn_robot_desc* r, int32_t steps, GccArgs& a) {
+    if (!r || !r->joints || !r->capsules) return fail(SVN_ERR_INVALID_ARGUMENT, "robot: null descriptor");
+    if (r->dof < 1 || r->dof > kGccMaxDof) return fail(SVN_ERR_INVALID_ARGUMENT, "robot: dof must be >= 1");
+    if (r->n_capsules < 1 || r->n_capsules > kGccMaxCaps)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "robot: every link needs at least one capsule");
+    if (steps < 2) return fail(SVN_ERR_INVALID_ARGUMENT, "discretize: steps must be >= 2");
+    a = GccArgs{};
+    a.dof = r->dof;
+    a.ncap = r->n_capsules;
+    a.steps = steps;
+    for (int k = 0; k < 12; ++k) a.base[k] = r->base_pose ? r->base_pose[k] : ((k % 4) == (k / 4) ? 1.0 : 0.0);
+    for (int j = 0; j < r->dof; ++j)
+        for (int k = 0; k < 3; ++k) {
+            a.joints[j].axis[k] = r->joints[j].axis[k];
+            a.joints[j].offset[k] = r->joints[j].offset[k];
+        }
+    int prev = -1;
+    for (int c = 0; c < r->n_capsules; ++c) {
+        const svn_capsule& cap = r->capsules[c];
+        if (cap.link < prev || cap.link >= r->dof || !(cap.radius > 0))
+            return fail(SVN_ERR_INVALID_ARGUMENT, "robot: link capsule invalid");
+        prev = cap.link;
+        a.caps[c].link = cap.link;
+        for (int k = 0; k < 3; ++k) {
+            a.caps[c].a[k] = cap.a[k];
+            a.caps[c].b[k] = cap.b[k];
+        }
+        a.caps[c].radius = cap.radius;
+    }
+    if (gcc_smem_bytes(steps, r->n_capsules) > 220 * 1024)
+        return fail(SVN_ERR_UNSUPPORTED, "gcc: steps x capsules exceeds shared memory");
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, const double* points, int64_t P,
+                                               const double* q01, int64_t M, int32_t steps, double margin,
+                                               double* dist_out, uint8_t* free_out, void* stream) {
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_min_distance: empty point cloud");
+    if (M < 1) return SVN_OK;
+    GccArgs a;
+    svn_status s = gcc_args(robot, steps, a);
+    if (s != SVN_OK) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&a.keys), sizeof(unsigned long long) * M), "cudaMallocAsync");
+    a.points = points;
+    a.P = P;
+    a.q01 = q01;
+    a.M = M;
+    a.points_per_chunk = 2048;
+    a.chunks = (P + a.points_per_chunk - 1) / a.points_per_chunk;
+    SVN_CUDA(launch_gcc(a, margin, dist_out, free_out, st), "gcc kernel");
+    g_launches += 3;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_gcc_min_distance(const svn_robot_desc* robot, const double* points, int64_t P,
+                                        const double* q01, int64_t M, int32_t steps, double margin, int32_t device,
+                                        double* dist_out, uint8_t* free_out) {
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_min_distance: empty point cloud");
+    if (M < 1) return SVN_OK;
+    if (!robot || !points || !q01 || !dist_out || !free_out)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_min_distance: null buffer");
+    DeviceGuard guard(device);
+    ensure_pool(device);
+    cudaStream_t st = thread_stream(device);
+    const int64_t nq = 2 * static_cast<int64_t>(robot->dof);
+    {
+        Scratch sc(st);
+        double *dp = nullptr, *dq = nullptr, *dd = nullptr;
+        uint8_t* df = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(double) * 3 * P), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(double) * nq * M), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dd), sizeof(double) * M), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&df), M), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(dp, points, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
+        SVN_CUDA(cudaMemcpyAsync(dq, q01, sizeof(double) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions");
+        svn_status s = svn_gcc_min_distance_device(robot, dp, P, dq, M, steps, margin, dd, df, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(dist_out, dd, sizeof(double) * M, cudaMemcpyDeviceToHost, st), "D2H dist");
+        SVN_CUDA(cudaMemcpyAsync(free_out, df, M, cudaMemcpyDeviceToHost, st), "D2H free");
+    }
+    SVN_CUDA(cudaStreamSynchronize(st), "gcc");
     return SVN_OK;
 }
 
