@@ -192,3 +192,24 @@ def test_checkpoint_round_trip(tmp_path):
         a = m1.query_min(pts, q, 0.0, precision=prec, per_point=True)
         b = m2.query_min(pts, q, 0.0, precision=prec, per_point=True)
         assert np.array_equal(a.per_point, b.per_point)
+
+
+@pytest.mark.parametrize("key", ["c3", "c4"])
+def test_classification_with_calibrated_output_bias(key):
+    """with seeded weights almost every c3/c4 motion is in collision, so the
+    margin test is shifted onto the data by setting b_o so the median per-motion oracle min
+    equals the margin; classification must then be exact outside the ambiguous band."""
+    w = WORKLOADS[key]
+    params = S.init_params(w.program, 31, w.bound)
+    pts, q = w.make(seed=31, motions=48, points=600)
+    omin, _, _, _ = _oracle(w.program, params, pts, q, w.margin)
+    params = params.copy()
+    params[-1] += np.float32(w.margin - np.median(omin.astype(np.float64)))
+    omin, oarg, ofree, opp = _oracle(w.program, params, pts, q, w.margin)
+    assert 0.2 < ofree.mean() < 0.8
+    for prec in ("bf16", "fp32"):
+        r = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec)
+        bound = BF16_BOUND[w.program.name] if prec == "bf16" else 1e-5
+        amb = np.abs(omin.astype(np.float64) - w.margin) <= bound
+        assert np.array_equal(r.free[~amb], ofree[~amb]), (prec, int(amb.sum()))
+        print(f"{key} {prec}: free {r.free.mean():.2f}, ambiguous {int(amb.sum())}/48")
