@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--motions", type=int, default=None, help="experiment override (not a BASELINE config)")
+    ap.add_argument("--points", type=int, default=None, help="experiment override (not a BASELINE config)")
     ap.add_argument("--mode", default=None, choices=["motion", "point"],
                     help="multi-GPU sharding: motion (default) or point (single-motion workloads)")
     return ap.parse_args()
@@ -173,6 +175,10 @@ def main():
     world, rank, local = dist_env()
     from paper_2402_15281_b200.workloads import WORKLOADS
     w = WORKLOADS[args.config]
+    if args.motions or args.points:
+        import dataclasses
+        w = dataclasses.replace(w, key=w.key + "-override", motions=args.motions or w.motions,
+                                points=args.points or w.points)
     prec = args.precision or w.precision
     peaks, peak_src = load_peaks()
 
@@ -279,6 +285,14 @@ def main():
                 "frac": achieved_tf / peak, "traffic": None,
                 "peak_source": f"{peak_src} bf16_tflops (burst)",
                 "frac_of_sustained": achieved_tf / float(peaks.get("bf16_tflops_sustained", peak)),
+                "flop_per_query": flop_q, "kernel_ms": kernel_ms}
+    elif prec == "fp32" and w.program.width == 256 and not os.environ.get("SVN_FP32_SIMT"):
+        # fp32-accurate on tcgen05: every product is three f16 MMAs (hi.hi, hi.lo', lo'.hi), so
+        # the algorithmic-FLOP ceiling of the scheme is the measured f16/bf16 peak / 3.
+        peak = float(peaks["bf16_tflops"]) / 3.0
+        roof = {"bound": "tensor", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved_tf / peak, "traffic": None,
+                "peak_source": f"{peak_src} bf16_tflops / 3 (split-fp16: 3 tensor products per fp32 product)",
                 "flop_per_query": flop_q, "kernel_ms": kernel_ms}
     else:
         peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12

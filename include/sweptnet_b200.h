@@ -58,7 +58,9 @@ typedef enum {
 /* Arithmetic of the fused MLP kernel.
  *  BF16        tcgen05 tensor cores, bf16 weights/activations, fp32 accumulate
  *              in TMEM; per-point delta within the bound stated per config.
- *  FP32        SIMT fp32 FMA with the per-motion q-fold (|d delta| <= 1e-5).
+ *  FP32        fp32-accurate, per-motion q-fold (|d delta| <= 1e-5).  Width 256: tcgen05
+ *              with every operand split into fp16 hi + 2^11-scaled lo and three f16 MMAs
+ *              per product (two fp32 TMEM accumulators); other widths: SIMT fp32 FMA.
  *  FP32_EXACT  SIMT fp32 FMA in the reference's exact accumulation order
  *              (bias, h part, x, q0, q1 — nn.cpp:118-124): bit-identical to the
  *              reference float path up to the documented dot-product order. */

@@ -166,6 +166,10 @@ cudaError_t launch_keys_finalize(const unsigned long long* keys, int64_t M, doub
 cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st);
 cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st);
+cudaError_t launch_split_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
+                             uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init, int64_t n_keys,
+                             cudaStream_t st);
 cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
                               uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,
                               int64_t n_keys, cudaStream_t st);

@@ -1,0 +1,499 @@
+// kernels_split.cu — K1 (fp32-accurate) on tcgen05 for width 256: split-fp16 products.
+//
+// The fp32 path's 1e-5 per-point bar (BASELINE.json north_star) without SIMT FFMA: every
+// operand x is split into fp16 hi = fp16(x) and scaled lo' = fp16((x - hi) * 2^11) (22
+// significant bits), and each width x width product runs as three kind::f16 MMAs into two
+// fp32 TMEM accumulators:
+//     main += A_hi . B_hi          corr += A_hi . B_lo' + A_lo' . B_hi
+//     D = main + corr * 2^-11      (the lo' . lo' term, ~2^-22 relative, is dropped)
+// Measured (scripts/microbench_split.cu): 2.7e-6 max error vs fp64 on a 128x256x256 product
+// with |D| ~ 5, against 2.3e-6 for a sequential fp32 FMA chain.  Bias, the per-motion q-fold
+// and the x-part ride in a K=16 extension slab split the same way.
+//
+// Structure = the CTA-pair kernel (kernels_bf16_pair.cu) with the width-256 layer output
+// treated as two output halves of 128 columns, each owning a main and a corr accumulator:
+// 2 x (128 + 128) = all 512 TMEM columns.  A layer runs as quarter steps (n-half, k-half)
+// (0,0) (1,0) (0,1) (1,1); the epilogue of output half 0 overlaps step (1,1).  The
+// activation tile is held as two fp16 planes (hi, lo'), 2 x 64 KiB per CTA.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "fused.cuh"
+#include "ptx.cuh"
+
+namespace svn {
+
+namespace sp {
+
+constexpr int N = 256;                      // layer width
+constexpr int TM = 128;                     // rows per CTA (pair tile = 256 rows)
+constexpr int NHO = 128;                    // output columns per n-half (MMA N)
+constexpr int BRH = NHO / 2;                // B rows per CTA per n-half (cta_group::2 split of N)
+constexpr int KSL = (N / 2) / 64;           // 64-wide K slabs per k-half
+constexpr uint32_t A_SLAB = TM * 128;       // 16 KiB
+constexpr uint32_t A_PLANE = TM * N * 2;    // 64 KiB per fp16 plane
+constexpr uint32_t AX_BYTES = TM * 32;      // 4 KiB
+constexpr uint32_t B_HALF = BRH * 128;      // 8 KiB: one plane of one slab for this CTA
+constexpr uint32_t CHUNK = 2 * B_HALF;      // 16 KiB: [hi][lo'] of one slab
+constexpr uint32_t XHALF = BRH * 32;        // 2 KiB: extension rows (main or corr) for this CTA
+constexpr int STAGES = 5;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int COLS = NHO / 2;               // columns per epilogue thread per half (64)
+constexpr uint32_t OFF_AHI = 0;
+constexpr uint32_t OFF_ALO = A_PLANE;
+constexpr uint32_t OFF_AX = 2 * A_PLANE;
+constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
+constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * CHUNK;
+constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
+constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
+constexpr uint32_t SMEM = OFF_BAR + 256;
+static_assert(SMEM <= 232448, "shared memory budget");
+constexpr float LO_SCALE = 2048.0f;
+constexpr float LO_INV = 1.0f / 2048.0f;
+
+// kind::f16 instruction descriptor with fp16 A/B (format 0) and fp32 D.
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+    return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void split(float x, __half& hi, __half& lo) {
+    hi = __float2half_rn(x);
+    lo = __float2half_rn((x - __half2float(hi)) * LO_SCALE);
+}
+
+__device__ __forceinline__ uint32_t pack_h2(__half lo_elem, __half hi_elem) {
+    return static_cast<uint32_t>(__half_as_ushort(lo_elem)) | (static_cast<uint32_t>(__half_as_ushort(hi_elem)) << 16);
+}
+
+// A extension row: (1, z0h, z1h, z2h, z0l', z1l', z2l', 0...) fp16.
+__device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, float z1, float z2) {
+    __half h0, l0, h1, l1, h2, l2;
+    split(z0, h0, l0);
+    split(z1, h1, l1);
+    split(z2, h2, l2);
+    const __half one = __float2half_rn(1.0f), zero = __float2half_rn(0.0f);
+    __align__(16) __half v[16] = {one, h0, h1, h2, l0, l1, l2, zero, zero, zero, zero, zero, zero, zero, zero, zero};
+    *reinterpret_cast<uint4*>(ax + ext_offset(row, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
+    *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+}
+
+// 32 output columns of one row: v (fp32, already main + corr/2048) -> act / affine /
+// residual -> next layer's (hi, lo') planes, or the output dot on the last layer.
+__device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
+                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float& dot) {
+    const int fl = ld.flags;
+    const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
+    }
+    if (aff) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 s = __ldg(reinterpret_cast<const float4*>(ld.s + c0 + i));
+            const float4 t = __ldg(reinterpret_cast<const float4*>(ld.t + c0 + i));
+            v[i + 0] = fmaf(v[i + 0], s.x, t.x);
+            v[i + 1] = fmaf(v[i + 1], s.y, t.y);
+            v[i + 2] = fmaf(v[i + 2], s.z, t.z);
+            v[i + 3] = fmaf(v[i + 3], s.w, t.w);
+        }
+    }
+    if (res) {  // residual stream = hi + lo'/2048 from the A planes (same addresses we overwrite)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t off = sw128_offset(row, c0 + 8 * u, TM);
+            const uint4 h = *reinterpret_cast<const uint4*>(Ahi + off);
+            const uint4 o = *reinterpret_cast<const uint4*>(Alo + off);
+            const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const __half2 hh = *reinterpret_cast<const __half2*>(&hw[p]);
+                const __half2 oo = *reinterpret_cast<const __half2*>(&ow[p]);
+                v[8 * u + 2 * p] += fmaf(__low2float(oo), LO_INV, __low2float(hh));
+                v[8 * u + 2 * p + 1] += fmaf(__high2float(oo), LO_INV, __high2float(hh));
+            }
+        }
+    }
+    if (last) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+            dot = fmaf(w.x, v[i + 0], dot);
+            dot = fmaf(w.y, v[i + 1], dot);
+            dot = fmaf(w.z, v[i + 2], dot);
+            dot = fmaf(w.w, v[i + 3], dot);
+        }
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+            __half h0, l0, h1, l1;
+            split(v[8 * u + 2 * p], h0, l0);
+            split(v[8 * u + 2 * p + 1], h1, l1);
+            hw[p] = pack_h2(h0, h1);
+            lw[p] = pack_h2(l0, l1);
+        }
+        const uint32_t off = sw128_offset(row, c0 + 8 * u, TM);
+        *reinterpret_cast<uint4*>(Ahi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+        *reinterpret_cast<uint4*>(Alo + off) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+}
+
+}  // namespace sp
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
+    fused_split_kernel(const __grid_constant__ FusedArgs a) {
+    using namespace sp;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* Ahi = smem + OFF_AHI;
+    uint8_t* Alo = smem + OFF_ALO;
+    uint8_t* AX = smem + OFF_AX;  // [2][AX_BYTES]
+    uint8_t* stages = smem + OFF_STAGE;
+    float* wo_s = reinterpret_cast<float*>(smem + OFF_WO);
+    float* dotbuf = reinterpret_cast<float*>(smem + OFF_DOT);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint64_t* full = bars;
+    uint64_t* empty = full + STAGES;
+    uint64_t* d_full = empty + STAGES;
+    uint64_t* a_ready = d_full + 2;
+    uint64_t* ax_full = a_ready + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ax_full + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const int L = a.L;
+    const int64_t pair = blockIdx.x >> 1;
+    const int64_t npairs = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        if (smem_u32(smem) & 1023u) __trap();
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int j = 0; j < 2; ++j) {
+            mbar_init(&d_full[j], 1);
+            mbar_init(&a_ready[j], 2 * EPI_WARPS);
+            mbar_init(&ax_full[j], 2 * EPI_WARPS);
+        }
+        fence_mbar_init();
+    }
+    for (int i = threadIdx.x; i < N; i += blockDim.x) wo_s[i] = a.wo[i];
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&a.tmap_w);
+        prefetch_tmap(&a.tmap_xm);
+        prefetch_tmap(&a.tmap_xq);
+    }
+    if (warp == 1) tmem_alloc_pair(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- producer --
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_last();
+            const uint32_t full0 = mapa_shared(smem_u32(full), 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            auto slot = [&](uint32_t bytes_one_cta) {
+                mbar_wait(&empty[stage], phase ^ 1u);
+                if (rank == 0) mbar_arrive_expect_tx_local(&full[stage], 2 * bytes_one_cta);
+            };
+            auto advance = [&]() {
+                if (++stage == STAGES) stage = 0, phase ^= 1u;
+            };
+            for (int64_t t = pair; t < a.n_tiles; t += npairs) {
+                int32_t motion, nrows;
+                int64_t pbase, obase;
+                tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+                int64_t wrow = 0;  // 128-byte row of the weight stream
+                for (int l = 0; l < L; ++l) {
+                    const LayerDev& ld = a.layer[l];
+                    const int steps = l == 0 ? 2 : 4;
+                    for (int step = 0; step < steps; ++step) {
+                        const int nh = step & 1, kh = step >> 1;
+                        if (kh == 0 && ld.ext) {
+                            slot(2 * XHALF);
+                            const uint32_t fb = full0 + stage * 8u;
+                            uint8_t* dst = stages + stage * CHUNK;
+                            if (ld.ext == 2) {
+                                const int64_t blob = ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
+                                tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * 2 * BRH), fb, pol);
+                            } else {
+                                const int64_t r0 = ld.ext_row + (nh * 2 + rank) * 2 * BRH;
+                                tma_load_2d_pair(dst, &a.tmap_xm, 0, static_cast<int32_t>(r0), fb, pol);
+                            }
+                            advance();
+                        }
+                        if (l > 0) {
+                            for (int ks = 0; ks < KSL; ++ks) {
+                                slot(CHUNK);
+                                tma_load_2d_pair(stages + stage * CHUNK, &a.tmap_w, 0,
+                                                 static_cast<int32_t>(wrow + rank * 2 * BRH), full0 + stage * 8u, pol);
+                                wrow += 4 * BRH;
+                                advance();
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // -------------------------------------------------------------- MMA issuer --
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc = idesc_f16(2 * TM, NHO);
+            const uint32_t ahi = smem_u32(Ahi), alo = smem_u32(Alo), s_base = smem_u32(stages), ax_base = smem_u32(AX);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
+            int64_t k = 0;
+            for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+                const int b = static_cast<int>(k & 1);
+                mbar_wait(&ax_full[b], ax_ph[b]);
+                ax_ph[b] ^= 1u;
+                for (int l = 0; l < L; ++l) {
+                    const LayerDev& ld = a.layer[l];
+                    const int steps = l == 0 ? 2 : 4;
+                    for (int step = 0; step < steps; ++step) {
+                        const int nh = step & 1, kh = step >> 1;
+                        if (kh == 0 && (k > 0 || l > 0)) {
+                            mbar_wait(&a_ready[nh], ar_ph[nh]);
+                            ar_ph[nh] ^= 1u;
+                        }
+                        tc_fence_after();
+                        const uint32_t d_main = tmem + static_cast<uint32_t>(nh * 256);
+                        const uint32_t d_corr = d_main + 128;
+                        bool acc = false;
+                        if (kh == 0 && ld.ext) {
+                            mbar_wait(&full[stage], phase);
+                            tc_fence_after();
+                            const uint32_t xs = s_base + stage * CHUNK;
+                            const uint64_t adesc = noswz_desc(ax_base + b * AX_BYTES, 128, 256);
+                            mma_bf16_pair(d_main, adesc, noswz_desc(xs, 128, 256), idesc, 0u);
+                            mma_bf16_pair(d_corr, adesc, noswz_desc(xs + XHALF, 128, 256), idesc, 0u);
+                            mma_commit_pair(&empty[stage], 3);
+                            if (++stage == STAGES) stage = 0, phase ^= 1u;
+                            acc = true;
+                        }
+                        if (l > 0) {
+                            for (int ks = 0; ks < KSL; ++ks) {
+                                mbar_wait(&full[stage], phase);
+                                tc_fence_after();
+                                const uint32_t aoff = static_cast<uint32_t>(kh * KSL + ks) * A_SLAB;
+                                const uint32_t bhi = s_base + static_cast<uint32_t>(stage) * CHUNK, blo = bhi + B_HALF;
+#pragma unroll
+                                for (int kk = 0; kk < 4; ++kk) {
+                                    const uint32_t first = (acc || kh || ks || kk) ? 1u : 0u;
+                                    const uint64_t a_hi = sw128_desc(ahi + aoff + kk * 32);
+                                    const uint64_t b_hi = sw128_desc(bhi + kk * 32);
+                                    mma_bf16_pair(d_main, a_hi, b_hi, idesc, first);
+                                    mma_bf16_pair(d_corr, a_hi, sw128_desc(blo + kk * 32), idesc, first);
+                                    mma_bf16_pair(d_corr, sw128_desc(alo + aoff + kk * 32), b_hi, idesc, 1u);
+                                }
+                                mma_commit_pair(&empty[stage], 3);
+                                if (++stage == STAGES) stage = 0, phase ^= 1u;
+                            }
+                        }
+                        if (l == 0) mma_commit_pair(&d_full[nh], 3);
+                        else if (step >= 2) mma_commit_pair(&d_full[step - 2], 3);
+                    }
+                }
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- epilogue --
+        const int e = warp - 2;
+        const uint32_t quad = static_cast<uint32_t>(warp & 3);
+        const int ch = e >> 2;
+        const uint32_t row = quad * 32 + lane;
+        const uint32_t t_lane = (quad * 32u) << 16;
+        const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
+        const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
+        uint32_t dp[2] = {0u, 0u};
+        auto write_ax_tile = [&](int64_t t, int b) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+            const int32_t r = static_cast<int32_t>(rank * TM + row);
+            const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
+            if (ch == 0) {
+                const float z0 = (xp[0] - a.shift[0]) * a.scale[0];
+                const float z1 = (xp[1] - a.shift[1]) * a.scale[1];
+                const float z2 = (xp[2] - a.shift[2]) * a.scale[2];
+                write_ax(AX + b * AX_BYTES, row, z0, z1, z2);
+                fence_proxy_async_smem();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
+        };
+        struct Pending {
+            bool live;
+            int par;
+            int32_t motion;
+            int64_t pbase, obase;
+            int32_t rr;
+            bool valid;
+        } pend{false, 0, 0, 0, 0, 0, false};
+        auto flush_output = [&]() {
+            if (!pend.live) return;
+            named_bar_sync(1, EPI_WARPS * 32);
+            if (ch == 0) {
+                const int par = pend.par;
+                const float delta = (dotbuf[(par * 2) * TM + row] + dotbuf[(par * 2 + 1) * TM + row]) + a.bo;
+                if (pend.valid && a.per_point) a.per_point[pend.obase + pend.rr] = delta;
+                if (a.keys) {
+                    unsigned long long key = pend.valid ? row_key(delta, a.index_offset + pend.pbase + pend.rr) : ~0ull;
+                    key = warp_min_u64(key);
+                    if (lane == 0) atomicMin(a.keys + pend.motion, key);
+                    named_bar_sync(2, 4 * 32);
+                    if (e == 0 && lane == 0 && a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + pend.motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                            __threadfence();
+                            const unsigned long long kk = atomicOr(a.keys + pend.motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + pend.motion, a.argmin_out + pend.motion,
+                                       a.free_out + pend.motion);
+                        }
+                    }
+                }
+            }
+            pend.live = false;
+        };
+        int64_t k = 0;
+        if (pair < a.n_tiles) write_ax_tile(pair, 0);
+        for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+            if (t + npairs < a.n_tiles) write_ax_tile(t + npairs, static_cast<int>((k + 1) & 1));
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+            const int32_t rr = static_cast<int32_t>(rank * TM + row);
+            const bool valid = rr < nrows;
+            float dot = 0.f;
+            for (int l = 0; l < L; ++l) {
+                const LayerDev& ld = a.layer[l];
+                const bool last = (l == L - 1);
+                for (int j = 0; j < 2; ++j) {
+                    mbar_wait(&d_full[j], dp[j]);
+                    dp[j] ^= 1u;
+                    tc_fence_after();
+                    const uint32_t tb = tmem + t_lane + static_cast<uint32_t>(j * 256 + ch * COLS);
+#pragma unroll
+                    for (int q = 0; q < COLS / 32; ++q) {
+                        uint32_t rm[32], rc[32];
+                        tmem_ld32_async(tb + 32 * q, rm);
+                        tmem_ld32_async(tb + 128 + 32 * q, rc);
+                        tmem_wait_tied(rm);
+                        tmem_wait_tied(rc);
+                        float v[32];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc[i]), LO_INV, __uint_as_float(rm[i]));
+                        epi32(ld, l, last, v, j * NHO + ch * COLS + 32 * q, row, Ahi, Alo, wo_s, dot);
+                    }
+                    tc_fence_before();
+                    if (!last) fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(a_ready0 + j * 8u);
+                }
+                if (l == 0) flush_output();
+            }
+            dotbuf[((k & 1) * 2 + ch) * TM + row] = dot;
+            pend = Pending{true, static_cast<int>(k & 1), motion, pbase, obase, rr, valid};
+            if (t + npairs >= a.n_tiles) flush_output();
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc_pair(tmem, 512);
+}
+
+cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e =
+            cudaFuncSetAttribute(fused_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    int64_t pairs = num_sms / 2;
+    if (a.n_tiles < pairs) pairs = a.n_tiles;
+    if (pairs < 1) return cudaSuccess;
+    fused_split_kernel<<<static_cast<unsigned>(2 * pairs), sp::THREADS, sp::SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K0 (split) --
+// Per motion m and concat slot s: b_m = b + Wq . zq (fp32), then extension rows per
+// (n-half, CTA half): [main: (b_h, w0h, w1h, w2h, 0..)] [corr: (b_l', w0l', w1l', w2l', w0h, w1h, w2h, 0..)].
+struct QNormS {
+    float shift[kMaxIn], scale[kMaxIn];
+};
+
+__global__ void split_ext_kernel(const float* __restrict__ q01, int dof, int n_mb, const float* __restrict__ wq,
+                                 const float* __restrict__ base_bias, const float* __restrict__ wx_slots,
+                                 uint8_t* __restrict__ ext, const QNormS qn, unsigned long long* keys,
+                                 unsigned int* counters, int64_t n_keys) {
+    using namespace sp;
+    const int64_t m = blockIdx.x;
+    const int slot = blockIdx.y;
+    if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
+        keys[m] = ~0ull;
+        counters[m] = 0u;
+    }
+    if (slot >= n_mb) return;
+    __shared__ float zq[kMaxIn];
+    const int nq = 2 * dof;
+    if (threadIdx.x < nq) {
+        const float q = q01[m * nq + threadIdx.x];
+        zq[threadIdx.x] = __fmul_rn(__fsub_rn(q, qn.shift[threadIdx.x]), qn.scale[threadIdx.x]);
+    }
+    __syncthreads();
+    const float* w = wq + static_cast<int64_t>(slot) * nq * N;
+    const float* wx = wx_slots + static_cast<int64_t>(slot) * 3 * N;
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        float acc = base_bias[slot * N + n];
+        for (int k = 0; k < nq; ++k) acc = __fmaf_rn(zq[k], w[k * N + n], acc);
+        __half bh, bl, h0, l0, h1, l1, h2, l2;
+        split(acc, bh, bl);
+        split(wx[n], h0, l0);
+        split(wx[N + n], h1, l1);
+        split(wx[2 * N + n], h2, l2);
+        const __half z = __float2half_rn(0.0f);
+        __align__(16) __half mv[16] = {bh, h0, h1, h2, z, z, z, z, z, z, z, z, z, z, z, z};
+        __align__(16) __half cv[16] = {bl, l0, l1, l2, h0, h1, h2, z, z, z, z, z, z, z, z, z};
+        const int nh = n / NHO, wi = n % NHO, r = wi / BRH, rr = wi % BRH;
+        uint8_t* blob = ext + (((m * n_mb + slot) * 2 + nh) * 2 + r) * (2 * XHALF);
+        *reinterpret_cast<uint4*>(blob + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&mv[0]);
+        *reinterpret_cast<uint4*>(blob + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&mv[8]);
+        *reinterpret_cast<uint4*>(blob + XHALF + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&cv[0]);
+        *reinterpret_cast<uint4*>(blob + XHALF + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&cv[8]);
+    }
+}
+
+cudaError_t launch_split_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
+                             uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init, int64_t n_keys,
+                             cudaStream_t st) {
+    if (a.M <= 0) return cudaSuccess;
+    QNormS qn;
+    for (int k = 0; k < 2 * a.dof && k < kMaxIn; ++k) {
+        qn.shift[k] = a.shift[3 + k];
+        qn.scale[k] = a.scale[3 + k];
+    }
+    dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
+    split_ext_kernel<<<grid, 256, 0, st>>>(a.q01, a.dof, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn, keys_init,
+                                           counters_init, n_keys);
+    return cudaGetLastError();
+}
+
+}  // namespace svn

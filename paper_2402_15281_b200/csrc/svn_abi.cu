@@ -8,8 +8,10 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -131,6 +133,8 @@ struct svn_model {
     std::vector<svn_layer> layers;
     std::vector<void*> allocs;
     FusedArgs base{};        // model part of the kernel arguments
+    FusedArgs base_split{};  // width 256: fp32-accurate split-fp16 tensor-core kernel (kernels_split.cu)
+    bool has_split = false;
     float* d_wq = nullptr;     // [n_mb][2dof][N]
     float* d_mbbase = nullptr; // [n_mb][N]
     float* d_wxslots = nullptr; // [n_mb][3][N] x-part columns of the concat layers
@@ -432,6 +436,77 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return cleanup_fail(st);
         m->has_bf16 = true;
     }
+
+    // fp32-accurate tensor-core path (width 256): every weight split into fp16 hi and
+    // 2^11-scaled lo' planes, per (layer, quarter step, 64-wide K slab, CTA half r) a
+    // [hi: 64 rows][lo': 64 rows] SW128 image; extension rows [main 64][corr 64] per
+    // (n-half, r).  Needs |W|, |b| well inside the fp16 range.
+    if (N == 256) {
+        float wmax = 0.f;
+        for (int64_t i = 2 * in; i < n_params; ++i) wmax = std::max(wmax, std::fabs(params[i]));
+        if (wmax < 1.0e4f) {
+            FusedArgs sa = a;
+            auto split_h = [](float x, __half& hi, __half& lo) {
+                hi = __float2half_rn(x);
+                lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
+            };
+            std::vector<uint8_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * 4 * 2 * 2 * 2 * 64 * 128);
+            uint8_t* out = ws.data();
+            const float* Wl = params + 2 * in;
+            for (int l = 0; l < L; ++l) {
+                const int K = layer_k(d->layers, l, N, in);
+                if (l > 0) {
+                    for (int step = 0; step < 4; ++step) {
+                        const int nh = step & 1, kh = step >> 1;
+                        for (int ks = 0; ks < 2; ++ks)
+                            for (int r = 0; r < 2; ++r) {
+                                for (int nr = 0; nr < 64; ++nr)
+                                    for (int kc = 0; kc < 64; ++kc) {
+                                        const int n = nh * 128 + r * 64 + nr, k = (kh * 2 + ks) * 64 + kc;
+                                        __half hi, lo;
+                                        split_h(Wl[static_cast<int64_t>(k) * N + n], hi, lo);
+                                        *reinterpret_cast<__half*>(out + sw128_offset(nr, kc, 64)) = hi;
+                                        *reinterpret_cast<__half*>(out + 8192 + sw128_offset(nr, kc, 64)) = lo;
+                                    }
+                                out += 16384;
+                            }
+                    }
+                }
+                Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+            }
+            uint8_t* dws = nullptr;
+            if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return cleanup_fail(st);
+            if ((st = encode_blob_map(&sa.tmap_w, dws, 128, ws.size() / 128, 128)) != SVN_OK) return cleanup_fail(st);
+            std::vector<uint8_t> xm;
+            const float* Wb = params + 2 * in;
+            for (int l = 0; l < L; ++l) {
+                const int K = layer_k(d->layers, l, N, in);
+                const float* b = Wb + static_cast<int64_t>(N) * K;
+                LayerDev& ld = sa.layer[l];
+                ld.ext_row = 0;
+                if (ld.ext == 1) {
+                    ld.ext_row = static_cast<int64_t>(xm.size() / 32);
+                    const size_t base = xm.size();
+                    xm.resize(base + static_cast<size_t>(N) * 2 * 32, 0);
+                    for (int n = 0; n < N; ++n) {
+                        const int nh = n / 128, wi = n % 128, r = wi / 64, rr = wi % 64;
+                        uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * 128) * 32;
+                        __half hi, lo;
+                        split_h(b[n], hi, lo);
+                        *reinterpret_cast<__half*>(blob + ext_offset(rr, 0)) = hi;         // main: b_h
+                        *reinterpret_cast<__half*>(blob + 2048 + ext_offset(rr, 0)) = lo;  // corr: b_l'
+                    }
+                }
+                Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+            }
+            if (xm.empty()) xm.resize(128 * 32, 0);
+            uint8_t* dxm = nullptr;
+            if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
+            if ((st = encode_blob_map(&sa.tmap_xm, dxm, 32, xm.size() / 32, 128)) != SVN_OK) return cleanup_fail(st);
+            m->base_split = sa;
+            m->has_split = true;
+        }
+    }
     *out = m;
     return SVN_OK;
 }
@@ -457,7 +532,16 @@ svn_status check_prec(const svn_model* m, svn_precision prec) {
     return SVN_OK;
 }
 
-int tile_rows(svn_precision prec, int N) { return prec == SVN_PREC_BF16 ? 256 : (N >= 512 ? 64 : 128); }
+// Which fused kernel serves a (model, precision): bf16 tensor cores; fp32-accurate
+// split-fp16 tensor cores (width 256); or SIMT FFMA (fp32_exact, and fp32 otherwise).
+enum class Kind { BF16, SPLIT, SIMT };
+Kind kernel_kind(const svn_model* m, svn_precision prec) {
+    if (prec == SVN_PREC_BF16) return Kind::BF16;
+    if (prec == SVN_PREC_FP32 && m->has_split && !std::getenv("SVN_FP32_SIMT")) return Kind::SPLIT;
+    return Kind::SIMT;
+}
+
+int tile_rows(Kind k, int N) { return k == Kind::SIMT ? (N >= 512 ? 64 : 128) : 256; }
 
 // Scratch buffers freed on the stream when the call's kernels are done.
 struct Scratch {
@@ -486,7 +570,7 @@ void ensure_pool(int device) {
     });
 }
 
-cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaStream_t st) {
+cudaError_t launch_k1(const FusedArgs& a, Kind kind, int num_sms, cudaStream_t st) {
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g_timing) {
         cudaEventCreate(&e0);
@@ -507,7 +591,9 @@ cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaS
         cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * kProfSlots, st);
         ap.prof = dprof;
     }
-    cudaError_t e = prec == SVN_PREC_BF16 ? launch_fused_bf16_pair(ap, num_sms, st) : launch_fused_fp32(ap, num_sms, st);
+    cudaError_t e = kind == Kind::BF16    ? launch_fused_bf16_pair(ap, num_sms, st)
+                    : kind == Kind::SPLIT ? launch_fused_split(ap, num_sms, st)
+                                          : launch_fused_fp32(ap, num_sms, st);
     ++g_launches;
     if (dprof) {
         cudaMemcpyAsync(g_prof, dprof, sizeof(g_prof), cudaMemcpyDeviceToHost, st);
@@ -526,8 +612,18 @@ cudaError_t launch_k1(const FusedArgs& a, svn_precision prec, int num_sms, cudaS
 
 // bf16: per-motion K=16 extension rows (folded bias + x-part splits) and their TMA view.
 svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long long* keys, unsigned int* counters,
-                      int64_t n_keys, Scratch& sc, cudaStream_t st) {
+                      int64_t n_keys, Scratch& sc, cudaStream_t st, bool split = false) {
     uint8_t* ext = nullptr;
+    if (split) {  // [motion][slot][n-half][CTA half][main 64 rows | corr 64 rows] x 32 B
+        const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * 2 * m->N;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(split ext)");
+        svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, 128);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(launch_split_ext(a, m->d_wq, m->d_mbbase, m->d_wxslots, ext, keys, counters, n_keys, st),
+                 "split_ext kernel");
+        ++g_launches;
+        return SVN_OK;
+    }
     const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * m->N;
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
     svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N == 256 ? m->N / 2 : m->N / 4));
@@ -550,7 +646,8 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     if (s != SVN_OK) return s;
     DeviceGuard guard(m->device);
     ensure_pool(m->device);
-    FusedArgs a = m->base;
+    const Kind kind0 = kernel_kind(m, prec);
+    FusedArgs a = kind0 == Kind::SPLIT ? m->base_split : m->base;
     const bool exact = prec == SVN_PREC_FP32_EXACT;
     a.exact = exact ? 1 : 0;
     a.points = points;
@@ -558,7 +655,8 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.P = P;
     a.q01 = q01;
     a.M = M;
-    const int TM = tile_rows(prec, m->N);
+    const Kind kind = kernel_kind(m, prec);
+    const int TM = tile_rows(kind, m->N);
     a.tiles_per_motion = (P + TM - 1) / TM;
     a.n_tiles = a.tiles_per_motion * M;
     a.tiles = nullptr;
@@ -568,7 +666,7 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     Scratch sc(st);
     float* mb = nullptr;
     const int n_mb = exact ? 0 : m->n_mb;
-    if (prec != SVN_PREC_BF16)
+    if (kind == Kind::SIMT)
         SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb),
                           sizeof(float) * static_cast<size_t>(M) * (n_mb ? n_mb : 1) * m->N),
                  "cudaMallocAsync(motion_bias)");
@@ -587,8 +685,9 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.min_out = min_out;
     a.argmin_out = argmin_out;
     a.free_out = free_out;
-    if (prec == SVN_PREC_BF16) {
-        s = motion_ext(m, a, M, keys_partial ? nullptr : keys, counters, keys_partial ? 0 : M, sc, st);
+    if (kind != Kind::SIMT) {
+        s = motion_ext(m, a, M, keys_partial ? nullptr : keys, counters, keys_partial ? 0 : M, sc, st,
+                       kind == Kind::SPLIT);
         if (s != SVN_OK) return s;
     } else {
         FusedArgs k0 = a;
@@ -598,7 +697,7 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
                  "motion_bias kernel");
         ++g_launches;
     }
-    SVN_CUDA(launch_k1(a, prec, m->num_sms, st), "fused MLP kernel");
+    SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
     return SVN_OK;
 }
 
@@ -693,7 +792,8 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
     if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
     svn_status s = check_prec(m, prec);
     if (s != SVN_OK) return s;
-    const int nq = 2 * m->dof, TM = tile_rows(prec, m->N);
+    const Kind kind = kernel_kind(m, prec);
+    const int nq = 2 * m->dof, TM = tile_rows(kind, m->N);
     std::vector<float> qseg;
     std::vector<TileDesc> tiles;
     int64_t seg_start = 0;
@@ -710,7 +810,7 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
         ++nseg;
         seg_start = r;
     }
-    FusedArgs a = m->base;
+    FusedArgs a = kind == Kind::SPLIT ? m->base_split : m->base;
     a.exact = prec == SVN_PREC_FP32_EXACT ? 1 : 0;
     a.points = raw_dev;
     a.point_stride = cols;
@@ -733,8 +833,8 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
     a.q01 = dq;
     a.tiles = dt;
     a.motion_bias = mb;
-    if (prec == SVN_PREC_BF16) {
-        s = motion_ext(m, a, nseg, nullptr, nullptr, 0, sc, st);
+    if (kind != Kind::SIMT) {
+        s = motion_ext(m, a, nseg, nullptr, nullptr, 0, sc, st, kind == Kind::SPLIT);
         if (s != SVN_OK) return s;
     } else {
         FusedArgs k0 = a;
@@ -742,7 +842,7 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
         SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, nullptr, nullptr, 0, st), "motion_bias kernel");
         ++g_launches;
     }
-    SVN_CUDA(launch_k1(a, prec, m->num_sms, st), "fused MLP kernel");
+    SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
     // keep the host tile/q vectors alive until the async copies have consumed them
     SVN_CUDA(cudaStreamSynchronize(st), "forward kernels");
     return SVN_OK;

@@ -1,0 +1,158 @@
+// Precision probe for an fp32-accurate tensor-core path: D = A.B^T (M=128, N=256, K=256)
+// with A, B split into fp16 hi + 2^11-scaled lo, three kind::f16 tcgen05 MMAs into two TMEM
+// accumulators (main: hi.hi; corr: hi.lo' + lo'.hi), combined as main + corr / 2048.
+// Compares against an fp64 reference and against a sequential fp32 FMA chain.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include "../paper_2402_15281_b200/csrc/ptx.cuh"
+
+using namespace svn;
+
+constexpr int M = 128, N = 256, K = 256;
+
+// kind::f16 instruction descriptor with F16 inputs (a/b format 0), F32 accumulate
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+    return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__global__ void probe(const uint8_t* gA_hi, const uint8_t* gA_lo, const uint8_t* gB_hi, const uint8_t* gB_lo,
+                      float* out_main, float* out_corr) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint8_t* A_hi = sm;                  // 128 x 256 fp16 SW128: 4 slabs x 16 KiB
+    uint8_t* A_lo = sm + 65536;
+    uint8_t* B_hi = sm + 131072;         // 256 x 64-slab: we stream B slabs one at a time (32 KiB each)
+    uint8_t* B_lo = sm + 131072 + 32768;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) {
+        reinterpret_cast<uint4*>(A_hi)[i] = reinterpret_cast<const uint4*>(gA_hi)[i];
+        reinterpret_cast<uint4*>(A_lo)[i] = reinterpret_cast<const uint4*>(gA_lo)[i];
+    }
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc(&tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tslot;
+    uint32_t ph = 0;
+    for (int ks = 0; ks < K / 64; ++ks) {
+        for (int i = threadIdx.x; i < 32768 / 16; i += blockDim.x) {
+            reinterpret_cast<uint4*>(B_hi)[i] = reinterpret_cast<const uint4*>(gB_hi + ks * 32768)[i];
+            reinterpret_cast<uint4*>(B_lo)[i] = reinterpret_cast<const uint4*>(gB_lo + ks * 32768)[i];
+        }
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            tc_fence_after();
+            constexpr uint32_t id = idesc_f16(128, 256);
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint32_t a_hi = smem_u32(A_hi) + ks * 16384 + kk * 32, a_lo = smem_u32(A_lo) + ks * 16384 + kk * 32;
+                const uint32_t b_hi = smem_u32(B_hi) + kk * 32, b_lo = smem_u32(B_lo) + kk * 32;
+                const uint32_t acc = (ks | kk) ? 1u : 0u;
+                mma_bf16(tmem, sw128_desc(a_hi), sw128_desc(b_hi), id, acc);          // main = hi.hi
+                mma_bf16(tmem + 256, sw128_desc(a_hi), sw128_desc(b_lo), id, acc);    // corr = hi.lo'
+                mma_bf16(tmem + 256, sw128_desc(a_lo), sw128_desc(b_hi), id, 1u);     // corr += lo'.hi
+            }
+            mma_commit(&bar);
+        }
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+        tc_fence_after();
+        __syncthreads();
+    }
+    // read back: warp w (0..3) reads lanes 32w..32w+31
+    if (warp < 4) {
+        for (int c = 0; c < 256; c += 32) {
+            float v[32];
+            tmem_ld32(tmem + ((warp * 32u) << 16) + c, v);
+            for (int i = 0; i < 32; ++i) out_main[(warp * 32 + (threadIdx.x & 31)) * 256 + c + i] = v[i];
+            tmem_ld32(tmem + ((warp * 32u) << 16) + 256 + c, v);
+            for (int i = 0; i < 32; ++i) out_corr[(warp * 32 + (threadIdx.x & 31)) * 256 + c + i] = v[i];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+static void put(std::vector<uint8_t>& img, int row, int k, int rows, __half v) {
+    *reinterpret_cast<__half*>(img.data() + sw128_offset(row, k, rows)) = v;
+}
+
+int main() {
+    std::mt19937_64 rng(7);
+    std::uniform_real_distribution<double> ua(0.0, 2.0), ub(-0.15, 0.15);
+    std::vector<float> A(M * K), B(N * K);
+    for (auto& x : A) x = static_cast<float>(ua(rng) * (rng() % 3 == 0 ? 0.0 : 1.0));  // relu-like zeros
+    for (auto& x : B) x = static_cast<float>(ub(rng));
+    std::vector<uint8_t> Ahi(M * K * 2), Alo(M * K * 2), Bhi(N * K * 2), Blo(N * K * 2);
+    auto split = [](float x, __half& hi, __half& lo) {
+        hi = __float2half_rn(x);
+        lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
+    };
+    for (int r = 0; r < M; ++r)
+        for (int k = 0; k < K; ++k) {
+            __half h, l;
+            split(A[r * K + k], h, l);
+            put(Ahi, r, k, M, h);
+            put(Alo, r, k, M, l);
+        }
+    // B as K/64 slabs of [256 rows x 64 k]
+    for (int ks = 0; ks < K / 64; ++ks)
+        for (int n = 0; n < N; ++n)
+            for (int kc = 0; kc < 64; ++kc) {
+                __half h, l;
+                split(B[n * K + ks * 64 + kc], h, l);
+                *reinterpret_cast<__half*>(Bhi.data() + ks * 32768 + sw128_offset(n, kc, N)) = h;
+                *reinterpret_cast<__half*>(Blo.data() + ks * 32768 + sw128_offset(n, kc, N)) = l;
+            }
+    uint8_t *dAh, *dAl, *dBh, *dBl;
+    float *dm, *dc;
+    cudaMalloc(&dAh, Ahi.size());
+    cudaMalloc(&dAl, Alo.size());
+    cudaMalloc(&dBh, Bhi.size());
+    cudaMalloc(&dBl, Blo.size());
+    cudaMalloc(&dm, M * N * 4);
+    cudaMalloc(&dc, M * N * 4);
+    cudaMemcpy(dAh, Ahi.data(), Ahi.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dAl, Alo.data(), Alo.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dBh, Bhi.data(), Bhi.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(dBl, Blo.data(), Blo.size(), cudaMemcpyHostToDevice);
+    const int smem = 131072 + 65536;
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    probe<<<1, 128, smem>>>(dAh, dAl, dBh, dBl, dm, dc);
+    cudaError_t e = cudaDeviceSynchronize();
+    std::vector<float> hm(M * N), hc(M * N);
+    cudaMemcpy(hm.data(), dm, M * N * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hc.data(), dc, M * N * 4, cudaMemcpyDeviceToHost);
+    double e_split = 0, e_fp32 = 0, e_hi = 0, maxabs = 0;
+    for (int r = 0; r < M; ++r)
+        for (int n = 0; n < N; ++n) {
+            double ref = 0;
+            float seq = 0.f;
+            for (int k = 0; k < K; ++k) {
+                ref += static_cast<double>(A[r * K + k]) * B[n * K + k];
+                seq = std::fma(A[r * K + k], B[n * K + k], seq);
+            }
+            const double got = static_cast<double>(hm[r * N + n]) + static_cast<double>(hc[r * N + n]) / 2048.0;
+            e_split = std::max(e_split, std::abs(got - ref));
+            e_fp32 = std::max(e_fp32, std::abs(static_cast<double>(seq) - ref));
+            e_hi = std::max(e_hi, std::abs(static_cast<double>(hm[r * N + n]) - ref));
+            maxabs = std::max(maxabs, std::abs(ref));
+        }
+    printf("status %s | max|D| %.3f | split3 err %.3e | fp32 seq-FMA err %.3e | hi-only err %.3e\n",
+           cudaGetErrorString(e), maxabs, e_split, e_fp32, e_hi);
+    return 0;
+}

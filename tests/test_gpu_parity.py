@@ -2,7 +2,8 @@
 
 Tolerances (BASELINE.json north_star):
   fp32_exact  bit-identical per-point delta (same fmaf order as oracle/sweptnet_oracle.c)
-  fp32        |delta_gpu - delta_oracle| <= 1e-5 (q-fold reorders the sums)
+  fp32        |delta_gpu - delta_oracle| <= 1e-5 (q-fold reorders the sums; width 256 runs
+              on tcgen05 with split-fp16 operands, width 512 on SIMT FFMA)
   bf16        |delta_gpu - delta_oracle| <= BF16_BOUND[config] (frozen, DESIGN.md "bf16 bound")
 Classification is bit-exact except for motions whose oracle min is within the
 bound of the margin ("ambiguous"), which are counted.
