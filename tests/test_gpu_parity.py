@@ -47,7 +47,7 @@ def test_fp32_exact_bit_identical(key, M, P):
     assert np.array_equal(r.min, omin) and np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
 
 
-@pytest.mark.parametrize("key,M,P", [("c1", 1, 4096), ("c2", 4, 2000)])
+@pytest.mark.parametrize("key,M,P", [("c1", 1, 4096), ("c2", 4, 2000), ("c3", 2, 700), ("c4", 2, 500)])
 def test_fp32_within_1e5(key, M, P):
     w, pts, q, params = _case(key, M, P)
     model = S.Model(w.program, params)
@@ -214,3 +214,20 @@ def test_classification_with_calibrated_output_bias(key):
         amb = np.abs(omin.astype(np.float64) - w.margin) <= bound
         assert np.array_equal(r.free[~amb], ofree[~amb]), (prec, int(amb.sum()))
         print(f"{key} {prec}: free {r.free.mean():.2f}, ambiguous {int(amb.sum())}/48")
+
+
+def test_fp32_split_and_simt_agree(monkeypatch):
+    """Width 256 'fp32' runs on tcgen05 (split-fp16); SVN_FP32_SIMT forces the SIMT kernel.
+    Both must sit within 1e-5 of the oracle, hence within 2e-5 of each other."""
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 41, w.bound)
+    pts, q = w.make(seed=41, motions=5, points=1500)
+    model = S.Model(w.program, params)
+    split = model.query_min(pts, q, w.margin, precision="fp32", per_point=True)
+    monkeypatch.setenv("SVN_FP32_SIMT", "1")
+    simt = model.query_min(pts, q, w.margin, precision="fp32", per_point=True)
+    monkeypatch.delenv("SVN_FP32_SIMT")
+    _, _, _, opp = _oracle(w.program, params, pts, q, w.margin)
+    for r in (split, simt):
+        assert np.abs(r.per_point.astype(np.float64) - opp).max() <= 1e-5
+    assert np.abs(split.per_point.astype(np.float64) - simt.per_point).max() <= 2e-5
