@@ -131,11 +131,13 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         uint32_t hw[4], lw[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            __half h0, l0, h1, l1;
-            split(v[8 * u + 2 * p], h0, l0);
-            split(v[8 * u + 2 * p + 1], h1, l1);
-            hw[p] = pack_h2(h0, h1);
-            lw[p] = pack_h2(l0, l1);
+            // paired split: hi = f16x2(x0, x1); lo' = f16x2((x - hi) * 2^11)
+            const float x0 = v[8 * u + 2 * p], x1 = v[8 * u + 2 * p + 1];
+            const __half2 h = __floats2half2_rn(x0, x1);
+            const float2 hf = __half22float2(h);
+            const __half2 lo = __floats2half2_rn((x0 - hf.x) * LO_SCALE, (x1 - hf.y) * LO_SCALE);
+            hw[p] = *reinterpret_cast<const uint32_t*>(&h);
+            lw[p] = *reinterpret_cast<const uint32_t*>(&lo);
         }
         const uint32_t off = sw128_offset(row, c0 + 8 * u, TM);
         *reinterpret_cast<uint4*>(Ahi + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
@@ -386,18 +388,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     dp[j] ^= 1u;
                     tc_fence_after();
                     const uint32_t tb = tmem + t_lane + static_cast<uint32_t>(j * 256 + ch * COLS);
-#pragma unroll
-                    for (int q = 0; q < COLS / 32; ++q) {
+                    static_assert(COLS == 64, "two 32-column chunks per thread per half");
+                    float v[32];
+                    {
                         uint32_t rm[32], rc[32];
-                        tmem_ld32_async(tb + 32 * q, rm);
-                        tmem_ld32_async(tb + 128 + 32 * q, rc);
+                        tmem_ld32_async(tb, rm);
+                        tmem_ld32_async(tb + 128, rc);
                         tmem_wait_tied(rm);
                         tmem_wait_tied(rc);
-                        float v[32];
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc[i]), LO_INV, __uint_as_float(rm[i]));
-                        epi32(ld, l, last, v, j * NHO + ch * COLS + 32 * q, row, Ahi, Alo, wo_s, dot);
                     }
+                    // second chunk's loads fly while the first chunk is split and stored
+                    uint32_t rm2[32], rc2[32];
+                    tmem_ld32_async(tb + 32, rm2);
+                    tmem_ld32_async(tb + 128 + 32, rc2);
+                    epi32(ld, l, last, v, j * NHO + ch * COLS, row, Ahi, Alo, wo_s, dot);
+                    tmem_wait_tied(rm2);
+                    tmem_wait_tied(rc2);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc2[i]), LO_INV, __uint_as_float(rm2[i]));
+                    epi32(ld, l, last, v, j * NHO + ch * COLS + 32, row, Ahi, Alo, wo_s, dot);
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
                     __syncwarp();
