@@ -84,7 +84,9 @@ enum : int {
     kProfEpiOut,         // output dot exchange + keys
     kProfEpiAx,          // A extension writes
     kProfProdWaitEmpty,  // producer waiting for free slots
-    kProfSlots = 16
+    kProfTimeline = 16,  // pp kernel: one round of CTA 0, [MMA wait, ready, committed] x (layer, slot), then
+                         // [epilogue woke, worked, arrived] x (layer, slot)
+    kProfSlots = 96
 };
 
 // Orderable-u32 map of a float: unsigned compare == float compare; NaN -> max.

@@ -32,7 +32,8 @@ constexpr uint32_t XCHUNK = BR * 32;       // 4 KiB
 constexpr int WSTAGES = 4;
 constexpr int XSTAGES = 2;
 constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int OUT_WARP = 2 + EPI_WARPS;    // keys / per-point outputs / next tile's A extension
+constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
 constexpr int COLS = N / 2;                // columns per epilogue thread
 constexpr uint32_t OFF_AX = 2 * A_BYTES;
 constexpr uint32_t OFF_W = OFF_AX + 2 * AX_BYTES;
@@ -66,9 +67,10 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
 }
 
-// 32 columns of one row: activation (+ Fig. 2 affine/residual) then bf16 store or output dot.
+// 32 columns of one row: activation (+ Fig. 2 affine/residual) then bf16 store or output dot
+// (accumulated in four partial sums so the 128-column dot is not one dependent FMA chain).
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                      uint8_t* A, const float* wo_s, float& dot) {
+                                      uint8_t* A, const float* wo_s, float4& dot) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (!aff && !res && !last) {
@@ -123,10 +125,10 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
             const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
-            dot = fmaf(w.x, v[i + 0], dot);
-            dot = fmaf(w.y, v[i + 1], dot);
-            dot = fmaf(w.z, v[i + 2], dot);
-            dot = fmaf(w.w, v[i + 3], dot);
+            dot.x = fmaf(w.x, v[i + 0], dot.x);  // four independent chains (column mod 4)
+            dot.y = fmaf(w.y, v[i + 1], dot.y);
+            dot.z = fmaf(w.z, v[i + 2], dot.z);
+            dot.w = fmaf(w.w, v[i + 3], dot.w);
         }
     } else {
 #pragma unroll
@@ -159,8 +161,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     uint64_t* xfull = wempty + WSTAGES;         // [XSTAGES] leader
     uint64_t* xempty = xfull + XSTAGES;         // [XSTAGES] each CTA
     uint64_t* d_full = xempty + XSTAGES;        // [2] each CTA: slot s accumulator ready
-    uint64_t* a_ready = d_full + 2;             // [2] leader: slot s drained + A_s/AX_s written (16 warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_ready + 2);
+    uint64_t* a_ready = d_full + 2;             // [2] leader: slot s drained + A_s written (16 warps)
+    uint64_t* ax_ready = a_ready + 2;           // [2] leader: AX_s holds the slot's next tile (2 output warps)
+    uint64_t* out_full = ax_ready + 2;          // [2] each CTA: dotbuf_s holds a finished tile (8 warps)
+    uint64_t* out_empty = out_full + 2;         // [2] each CTA: output warp has read dotbuf_s
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(out_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -186,6 +191,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
         for (int s = 0; s < 2; ++s) {
             mbar_init(&d_full[s], 1);
             mbar_init(&a_ready[s], 2 * EPI_WARPS);
+            mbar_init(&ax_ready[s], 2);
+            mbar_init(&out_full[s], EPI_WARPS);
+            mbar_init(&out_empty[s], 1);
         }
         fence_mbar_init();
     }
@@ -252,7 +260,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
             const uint32_t x_base = smem_u32(xring);
             int ws = 0, xs = 0;
             uint32_t wph = 0, xph = 0;
-            uint32_t ar_ph[2] = {0u, 0u};
+            uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
+            unsigned long long pw_a = 0, pw_f = 0, pw_x = 0;
+            const unsigned long long p_start = clock64();
             for (int64_t j = 0; j < R; ++j) {
                 for (int l = 0; l < L; ++l) {
                     const LayerDev& ld = a.layer[l];
@@ -260,13 +270,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                     const uint32_t wph_layer = wph;
                     const int nslots = has(j, 1) ? 2 : 1;
                     for (int s = 0; s < nslots; ++s) {
-                        mbar_wait(&a_ready[s], ar_ph[s]);  // D_s drained, A_s / AX_s written
+                        const unsigned long long c0 = clock64();
+                        const bool tl = a.prof && blockIdx.x == 0 && j == R / 2 && l < 4;  // timeline sample
+                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3] = c0;
+                        mbar_wait(&a_ready[s], ar_ph[s]);  // D_s drained, A_s written
+                        if (l == 0) {
+                            mbar_wait(&ax_ready[s], ax_ph[s]);  // AX_s holds this tile's points
+                            ax_ph[s] ^= 1u;
+                        }
+                        pw_a += clock64() - c0;
+                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3 + 1] = clock64();
                         ar_ph[s] ^= 1u;
                         tc_fence_after();
                         const uint32_t d_addr = tmem + static_cast<uint32_t>(s * N);
                         bool acc = false;
                         if (ld.ext) {
+                            const unsigned long long c1 = clock64();
                             mbar_wait(&xfull[xs], xph);
+                            pw_x += clock64() - c1;
                             tc_fence_after();
                             mma_bf16_pair(d_addr, noswz_desc(ax_base + s * AX_BYTES, 128, 256),
                                           noswz_desc(x_base + xs * XCHUNK, 128, 256), idesc, 0u);
@@ -279,7 +300,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             uint32_t ph = wph_layer;
                             for (int ks = 0; ks < KSL; ++ks) {
                                 if (s == 0) {
+                                    const unsigned long long c2 = clock64();
                                     mbar_wait(&wfull[st], ph);
+                                    pw_f += clock64() - c2;
                                     tc_fence_after();
                                 }
                                 const uint32_t a_slab = a_base + s * A_BYTES + ks * A_SLAB;
@@ -293,14 +316,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             }
                         }
                         mma_commit_pair(&d_full[s], 3);
+                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3 + 2] = clock64();
                     }
                     if (l > 0)
                         for (int ks = 0; ks < KSL; ++ks)
                             if (++ws == WSTAGES) ws = 0, wph ^= 1u;
                 }
             }
+            if (a.prof) {
+                atomicAdd(a.prof + kProfMmaWaitA, pw_a);
+                atomicAdd(a.prof + kProfMmaWaitFull, pw_f);
+                atomicAdd(a.prof + kProfMmaWaitAx, pw_x);
+                atomicAdd(a.prof + kProfMmaTotal, clock64() - p_start);
+            }
         }
-    } else {
+    } else if (warp < OUT_WARP) {
         // ------------------------------------------------------------------ epilogue --
         const int e = warp - 2;
         const uint32_t quad = static_cast<uint32_t>(warp & 3);
@@ -308,60 +338,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
         const uint32_t row = quad * 32 + lane;
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
-        uint32_t dp[2] = {0u, 0u};
-        auto write_ax_for = [&](int64_t t, int s) {
-            int32_t motion, nrows;
-            int64_t pbase, obase;
-            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
-            const int32_t r = static_cast<int32_t>(rank * TM + row);
-            const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
-            if (ch == 0) {
-                const float z0 = (xp[0] - a.shift[0]) * a.scale[0];
-                const float z1 = (xp[1] - a.shift[1]) * a.scale[1];
-                const float z2 = (xp[2] - a.shift[2]) * a.scale[2];
-                write_ax(AX + s * AX_BYTES, row, z0, z1, z2);
-            }
-        };
-        struct Pending {
-            bool live;
-            int32_t motion, rr;
-            int64_t pbase, obase;
-            bool valid;
-        } pend[2] = {{false, 0, 0, 0, 0, false}, {false, 0, 0, 0, 0, false}};
-        auto flush = [&](int s) {
-            if (!pend[s].live) return;
-            named_bar_sync(1 + s, EPI_WARPS * 32);
-            if (ch == 0) {
-                const Pending& p = pend[s];
-                const float delta = (dotbuf[(s * 2) * TM + row] + dotbuf[(s * 2 + 1) * TM + row]) + a.bo;
-                if (p.valid && a.per_point) a.per_point[p.obase + p.rr] = delta;
-                if (a.keys) {
-                    unsigned long long key = p.valid ? row_key(delta, a.index_offset + p.pbase + p.rr) : ~0ull;
-                    key = warp_min_u64(key);
-                    if (lane == 0) atomicMin(a.keys + p.motion, key);
-                    named_bar_sync(3 + s, 4 * 32);
-                    if (e == 0 && lane == 0 && a.counters) {
-                        __threadfence();
-                        const unsigned int prev = atomicAdd(a.counters + p.motion, 1u);
-                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
-                            __threadfence();
-                            const unsigned long long kk = atomicOr(a.keys + p.motion, 0ull);
-                            decode_key(kk, a.margin, a.min_out + p.motion, a.argmin_out + p.motion,
-                                       a.free_out + p.motion);
-                        }
-                    }
-                }
-            }
-            pend[s].live = false;
-        };
-        // round 0: A extensions of both slots, then the initial "slot free" arrivals
+        uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
+        // initial "slot free" arrivals (the output warp separately signals AX_s)
         for (int s = 0; s < 2; ++s) {
-            if (has(0, s)) write_ax_for(tile_of(0, s), s);
-            fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
         }
-        float dot[2] = {0.f, 0.f};
+        float4 dot[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+        unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0;
         for (int64_t j = 0; j < R; ++j) {
             const int nslots = has(j, 1) ? 2 : 1;
             for (int l = 0; l < L; ++l) {
@@ -369,44 +353,149 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                 const bool last = (l == L - 1);
                 for (int s = 0; s < nslots; ++s) {
                     uint8_t* A = Abuf + s * A_BYTES;
+                    const unsigned long long c0 = clock64();
                     mbar_wait(&d_full[s], dp[s]);
+                    const unsigned long long c1 = clock64();
+                    pe_d += c1 - c0;
+                    const bool tl = a.prof && blockIdx.x == 0 && e == 0 && lane == 0 && j == R / 2 && l < 4;
+                    if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3] = c1;
                     dp[s] ^= 1u;
                     tc_fence_after();
                     const int c0c = ch * COLS;
                     constexpr int NCH = COLS / 32;
-                    uint32_t ra[32], rb[32];
                     const uint32_t tbase = tmem + t_lane + static_cast<uint32_t>(s * N);
-                    tmem_ld32_async(tbase + static_cast<uint32_t>(c0c), ra);
-                    tmem_wait_tied(ra);
+                    {
+                        uint32_t ra[32], rb[32];
+                        tmem_ld32_async(tbase + static_cast<uint32_t>(c0c), ra);
+                        tmem_wait_tied(ra);
 #pragma unroll
-                    for (int q = 0; q < NCH; ++q) {
-                        uint32_t(&cur)[32] = (q & 1) ? rb : ra;
-                        uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
-                        if (q + 1 < NCH) tmem_ld32_async(tbase + static_cast<uint32_t>(c0c + 32 * (q + 1)), nxt);
-                        epi32(ld, l, last, reinterpret_cast<float*>(cur), c0c + 32 * q, row, A, wo_s, dot[s]);
-                        if (q + 1 < NCH) tmem_wait_tied(nxt);
+                        for (int q = 0; q < NCH; ++q) {
+                            uint32_t(&cur)[32] = (q & 1) ? rb : ra;
+                            uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
+                            if (q + 1 < NCH) tmem_ld32_async(tbase + static_cast<uint32_t>(c0c + 32 * (q + 1)), nxt);
+                            epi32(ld, l, last, reinterpret_cast<float*>(cur), c0c + 32 * q, row, A, wo_s, dot[s]);
+                            if (q + 1 < NCH) tmem_wait_tied(nxt);
+                        }
                     }
-                    if (last) {
-                        // this slot's tile is done: stash the dot, load the next tile's A extension
-                        dotbuf[(s * 2 + ch) * TM + row] = dot[s];
-                        dot[s] = 0.f;
-                        int32_t motion, nrows;
-                        int64_t pbase, obase;
-                        tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
-                        const int32_t rr = static_cast<int32_t>(rank * TM + row);
-                        pend[s] = Pending{true, motion, rr, pbase, obase, rr < nrows};
-                        if (has(j + 1, s)) write_ax_for(tile_of(j + 1, s), s);
-                    }
+                    const unsigned long long c2 = clock64();
+                    pe_w += c2 - c1;
+                    if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3 + 1] = c2;
                     tc_fence_before();
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
-                    if (l == 0 && j > 0) flush(s);  // previous round's outputs, off the critical path
+                    const unsigned long long c3 = clock64();
+                    pe_a += c3 - c2;
+                    if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3 + 2] = c3;
+                    if (last) {
+                        // hand this row's partial dot to the output warp (dotbuf_s is read a round later)
+                        if (j > 0) {
+                            mbar_wait(&out_empty[s], oe_ph[s]);
+                            oe_ph[s] ^= 1u;
+                        }
+                        dotbuf[(s * 2 + ch) * TM + row] = (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
+                        dot[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&out_full[s]);
+                    }
+                    pe_o += clock64() - c3;
                 }
             }
         }
-        flush(0);
-        flush(1);
+        if (a.prof && e == 0 && lane == 0 && rank == 0) {
+            atomicAdd(a.prof + kProfEpiWaitD, pe_d);
+            atomicAdd(a.prof + kProfEpiWork, pe_w);
+            atomicAdd(a.prof + kProfEpiArrive, pe_a);
+            atomicAdd(a.prof + kProfEpiOut, pe_o);
+        }
+    } else {
+        // ---------------------------------------------------------------- output warp --
+        // Per finished tile of slot s: delta = dot + bo for this CTA's 128 rows, per-point
+        // stores, one packed-key atomicMin, the per-motion completion counter; and the A
+        // extension (bias / x columns) of the slot's next tile, whose point loads are issued
+        // before waiting so they land while the tile is still in the tensor core.
+        const uint32_t ax_ready0 = mapa_shared(smem_u32(ax_ready), 0);
+        uint32_t of_ph[2] = {0u, 0u};
+        float px[2][4][3];
+        auto load_points = [&](int64_t t, int s) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t r = static_cast<int32_t>(rank * TM + k * 32 + lane);
+                const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
+                px[s][k][0] = xp[0];
+                px[s][k][1] = xp[1];
+                px[s][k][2] = xp[2];
+            }
+        };
+        auto store_ax = [&](int s) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                write_ax(AX + s * AX_BYTES, static_cast<uint32_t>(k * 32) + lane, (px[s][k][0] - a.shift[0]) * a.scale[0],
+                         (px[s][k][1] - a.shift[1]) * a.scale[1], (px[s][k][2] - a.shift[2]) * a.scale[2]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(ax_ready0 + s * 8u);
+        };
+        unsigned long long pe_x = 0;
+        for (int s = 0; s < 2; ++s)
+            if (has(0, s)) {
+                load_points(tile_of(0, s), s);
+                store_ax(s);
+            }
+        for (int64_t j = 0; j < R; ++j) {
+            const int nslots = has(j, 1) ? 2 : 1;
+            for (int s = 0; s < nslots; ++s) {
+                const bool next = has(j + 1, s);
+                if (next) load_points(tile_of(j + 1, s), s);
+                int32_t motion, nrows;
+                int64_t pbase, obase;
+                tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
+                mbar_wait(&out_full[s], of_ph[s]);
+                of_ph[s] ^= 1u;
+                const unsigned long long c0 = clock64();
+                // every MMA of tile (j, s) has completed, so AX_s is free for the next tile
+                if (next) store_ax(s);
+                float delta[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int r = k * 32 + static_cast<int>(lane);
+                    delta[k] = (dotbuf[(s * 2) * TM + r] + dotbuf[(s * 2 + 1) * TM + r]) + a.bo;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&out_empty[s]);
+                unsigned long long key = ~0ull;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int32_t rr = static_cast<int32_t>(rank * TM + k * 32 + lane);
+                    if (rr < nrows) {
+                        if (a.per_point) a.per_point[obase + rr] = delta[k];
+                        const unsigned long long kk = row_key(delta[k], a.index_offset + pbase + rr);
+                        key = kk < key ? kk : key;
+                    }
+                }
+                if (a.keys) {
+                    key = warp_min_u64(key);
+                    if (lane == 0) {
+                        atomicMin(a.keys + motion, key);
+                        if (a.counters) {
+                            __threadfence();
+                            const unsigned int prev = atomicAdd(a.counters + motion, 1u);
+                            if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                                __threadfence();
+                                const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
+                                decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion,
+                                           a.free_out + motion);
+                            }
+                        }
+                    }
+                }
+                pe_x += clock64() - c0;
+            }
+        }
+        if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
     }
 
     tc_fence_before();
