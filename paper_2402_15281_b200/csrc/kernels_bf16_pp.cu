@@ -30,6 +30,13 @@ constexpr uint32_t AX_BYTES = TM * 32;     // 4 KiB
 constexpr uint32_t SLAB_B = BR * 128;      // 16 KiB
 constexpr uint32_t XCHUNK = BR * 32;       // 4 KiB
 constexpr int WSTAGES = 4;
+// One-round timeline of CTA 0 into FusedArgs::prof (scripts/pp_timeline.py); costs ~2.5%, so
+// compiled in only with -DSVN_PP_TIMELINE.
+#ifdef SVN_PP_TIMELINE
+constexpr bool kTimeline = true;
+#else
+constexpr bool kTimeline = false;
+#endif
 constexpr int XSTAGES = 2;
 constexpr int EPI_WARPS = 8;
 constexpr int OUT_WARP = 2 + EPI_WARPS;    // keys / per-point outputs / next tile's A extension
@@ -73,6 +80,29 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
                                       uint8_t* A, const float* wo_s, float4& dot) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (!aff && !res && last) {
+        // straight-line activation + output dot (no branches between the TMEM loads and the math)
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+                dot.x = fmaf(w.x, v[i + 0] > 0.f ? v[i + 0] : 0.f, dot.x);
+                dot.y = fmaf(w.y, v[i + 1] > 0.f ? v[i + 1] : 0.f, dot.y);
+                dot.z = fmaf(w.z, v[i + 2] > 0.f ? v[i + 2] : 0.f, dot.z);
+                dot.w = fmaf(w.w, v[i + 3] > 0.f ? v[i + 3] : 0.f, dot.w);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+                dot.x = fmaf(w.x, v[i + 0], dot.x);
+                dot.y = fmaf(w.y, v[i + 1], dot.y);
+                dot.z = fmaf(w.z, v[i + 2], dot.z);
+                dot.w = fmaf(w.w, v[i + 3], dot.w);
+            }
+        }
+        return;
+    }
     if (!aff && !res && !last) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -271,7 +301,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                     const int nslots = has(j, 1) ? 2 : 1;
                     for (int s = 0; s < nslots; ++s) {
                         const unsigned long long c0 = clock64();
-                        const bool tl = a.prof && blockIdx.x == 0 && j == R / 2 && l < 4;  // timeline sample
+                        const bool tl = kTimeline && a.prof && blockIdx.x == 0 && j == R / 2 && l < 4;  // timeline sample
                         if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3] = c0;
                         mbar_wait(&a_ready[s], ar_ph[s]);  // D_s drained, A_s written
                         if (l == 0) {
@@ -357,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                     mbar_wait(&d_full[s], dp[s]);
                     const unsigned long long c1 = clock64();
                     pe_d += c1 - c0;
-                    const bool tl = a.prof && blockIdx.x == 0 && e == 0 && lane == 0 && j == R / 2 && l < 4;
+                    const bool tl = kTimeline && a.prof && blockIdx.x == 0 && e == 0 && lane == 0 && j == R / 2 && l < 4;
                     if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3] = c1;
                     dp[s] ^= 1u;
                     tc_fence_after();
