@@ -38,7 +38,8 @@ constexpr uint32_t CHUNK = 2 * B_HALF;      // 16 KiB: [hi][lo'] of one slab
 constexpr uint32_t XHALF = BRH * 32;        // 2 KiB: extension rows (main or corr) for this CTA
 constexpr int STAGES = 5;
 constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int OUT_WARP = 2 + EPI_WARPS;     // keys / per-point outputs / A extensions of later tiles
+constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
 constexpr int COLS = NHO / 2;               // columns per epilogue thread per half (64)
 constexpr uint32_t OFF_AHI = 0;
 constexpr uint32_t OFF_ALO = A_PLANE;
@@ -81,7 +82,7 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 // 32 output columns of one row: v (fp32, already main + corr/2048) -> act / affine /
 // residual -> next layer's (hi, lo') planes, or the output dot on the last layer.
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float& dot) {
+                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (act) {
@@ -119,10 +120,10 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
             const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
-            dot = fmaf(w.x, v[i + 0], dot);
-            dot = fmaf(w.y, v[i + 1], dot);
-            dot = fmaf(w.z, v[i + 2], dot);
-            dot = fmaf(w.w, v[i + 3], dot);
+            dot.x = fmaf(w.x, v[i + 0], dot.x);  // four partial sums (column mod 4)
+            dot.y = fmaf(w.y, v[i + 1], dot.y);
+            dot.z = fmaf(w.z, v[i + 2], dot.z);
+            dot.w = fmaf(w.w, v[i + 3], dot.w);
         }
         return;
     }
@@ -162,8 +163,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* d_full = empty + STAGES;
     uint64_t* a_ready = d_full + 2;
-    uint64_t* ax_full = a_ready + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ax_full + 2);
+    uint64_t* ax_full = a_ready + 2;    // [tile parity] leader: AX holds the tile's points (2 output warps)
+    uint64_t* out_full = ax_full + 2;   // [tile parity] each CTA: dotbuf holds a finished tile (8 warps)
+    uint64_t* out_empty = out_full + 2; // [tile parity] each CTA: output warp has read dotbuf
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(out_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -181,7 +184,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         for (int j = 0; j < 2; ++j) {
             mbar_init(&d_full[j], 1);
             mbar_init(&a_ready[j], 2 * EPI_WARPS);
-            mbar_init(&ax_full[j], 2 * EPI_WARPS);
+            mbar_init(&ax_full[j], 2);
+            mbar_init(&out_full[j], EPI_WARPS);
+            mbar_init(&out_empty[j], 1);
         }
         fence_mbar_init();
     }
@@ -310,7 +315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                 }
             }
         }
-    } else {
+    } else if (warp < OUT_WARP) {
         // ---------------------------------------------------------------- epilogue --
         const int e = warp - 2;
         const uint32_t quad = static_cast<uint32_t>(warp & 3);
@@ -318,68 +323,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         const uint32_t row = quad * 32 + lane;
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
-        const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
-        uint32_t dp[2] = {0u, 0u};
-        auto write_ax_tile = [&](int64_t t, int b) {
-            int32_t motion, nrows;
-            int64_t pbase, obase;
-            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
-            const int32_t r = static_cast<int32_t>(rank * TM + row);
-            const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
-            if (ch == 0) {
-                const float z0 = (xp[0] - a.shift[0]) * a.scale[0];
-                const float z1 = (xp[1] - a.shift[1]) * a.scale[1];
-                const float z2 = (xp[2] - a.shift[2]) * a.scale[2];
-                write_ax(AX + b * AX_BYTES, row, z0, z1, z2);
-                fence_proxy_async_smem();
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
-        };
-        struct Pending {
-            bool live;
-            int par;
-            int32_t motion;
-            int64_t pbase, obase;
-            int32_t rr;
-            bool valid;
-        } pend{false, 0, 0, 0, 0, 0, false};
-        auto flush_output = [&]() {
-            if (!pend.live) return;
-            named_bar_sync(1, EPI_WARPS * 32);
-            if (ch == 0) {
-                const int par = pend.par;
-                const float delta = (dotbuf[(par * 2) * TM + row] + dotbuf[(par * 2 + 1) * TM + row]) + a.bo;
-                if (pend.valid && a.per_point) a.per_point[pend.obase + pend.rr] = delta;
-                if (a.keys) {
-                    unsigned long long key = pend.valid ? row_key(delta, a.index_offset + pend.pbase + pend.rr) : ~0ull;
-                    key = warp_min_u64(key);
-                    if (lane == 0) atomicMin(a.keys + pend.motion, key);
-                    named_bar_sync(2, 4 * 32);
-                    if (e == 0 && lane == 0 && a.counters) {
-                        __threadfence();
-                        const unsigned int prev = atomicAdd(a.counters + pend.motion, 1u);
-                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
-                            __threadfence();
-                            const unsigned long long kk = atomicOr(a.keys + pend.motion, 0ull);
-                            decode_key(kk, a.margin, a.min_out + pend.motion, a.argmin_out + pend.motion,
-                                       a.free_out + pend.motion);
-                        }
-                    }
-                }
-            }
-            pend.live = false;
-        };
+        uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
         int64_t k = 0;
-        if (pair < a.n_tiles) write_ax_tile(pair, 0);
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
-            if (t + npairs < a.n_tiles) write_ax_tile(t + npairs, static_cast<int>((k + 1) & 1));
-            int32_t motion, nrows;
-            int64_t pbase, obase;
-            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
-            const int32_t rr = static_cast<int32_t>(rank * TM + row);
-            const bool valid = rr < nrows;
-            float dot = 0.f;
+            float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
@@ -414,11 +361,99 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(a_ready0 + j * 8u);
                 }
-                if (l == 0) flush_output();
             }
-            dotbuf[((k & 1) * 2 + ch) * TM + row] = dot;
-            pend = Pending{true, static_cast<int>(k & 1), motion, pbase, obase, rr, valid};
-            if (t + npairs >= a.n_tiles) flush_output();
+            // hand the row's partial dot to the output warp (dotbuf[parity] is reused two tiles later)
+            const int b = static_cast<int>(k & 1);
+            if (k >= 2) {
+                mbar_wait(&out_empty[b], oe_ph[b]);
+                oe_ph[b] ^= 1u;
+            }
+            dotbuf[(b * 2 + ch) * TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&out_full[b]);
+        }
+    } else {
+        // ------------------------------------------------------------- output warp --
+        // Per finished tile: delta = dot + bo for this CTA's 128 rows, per-point stores, one
+        // packed-key atomicMin and the per-motion completion counter; then the A extension of
+        // the tile two ahead (same parity), whose point loads are issued before the wait.
+        const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
+        uint32_t of_ph[2] = {0u, 0u};
+        float px[4][3];
+        auto load_points = [&](int64_t t) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int32_t r = static_cast<int32_t>(rank * TM + q * 32 + lane);
+                const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
+                px[q][0] = xp[0];
+                px[q][1] = xp[1];
+                px[q][2] = xp[2];
+            }
+        };
+        auto store_ax = [&](int b) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                write_ax(AX + b * AX_BYTES, static_cast<uint32_t>(q * 32) + lane, (px[q][0] - a.shift[0]) * a.scale[0],
+                         (px[q][1] - a.shift[1]) * a.scale[1], (px[q][2] - a.shift[2]) * a.scale[2]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
+        };
+        for (int b = 0; b < 2; ++b) {
+            const int64_t t = pair + b * npairs;
+            if (t < a.n_tiles) {
+                load_points(t);
+                store_ax(b);
+            }
+        }
+        int64_t k = 0;
+        for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+            const int b = static_cast<int>(k & 1);
+            const bool next = t + 2 * npairs < a.n_tiles;
+            if (next) load_points(t + 2 * npairs);
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
+            mbar_wait(&out_full[b], of_ph[b]);
+            of_ph[b] ^= 1u;
+            // every MMA of tile t has completed, so AX[b] is free for tile t + 2 npairs
+            if (next) store_ax(b);
+            float delta[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = q * 32 + static_cast<int>(lane);
+                delta[q] = (dotbuf[(b * 2) * TM + r] + dotbuf[(b * 2 + 1) * TM + r]) + a.bo;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&out_empty[b]);
+            unsigned long long key = ~0ull;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int32_t rr = static_cast<int32_t>(rank * TM + q * 32 + lane);
+                if (rr < nrows) {
+                    if (a.per_point) a.per_point[obase + rr] = delta[q];
+                    const unsigned long long kk = row_key(delta[q], a.index_offset + pbase + rr);
+                    key = kk < key ? kk : key;
+                }
+            }
+            if (a.keys) {
+                key = warp_min_u64(key);
+                if (lane == 0) {
+                    atomicMin(a.keys + motion, key);
+                    if (a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                            __threadfence();
+                            const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion, a.free_out + motion);
+                        }
+                    }
+                }
+            }
         }
     }
 
