@@ -20,7 +20,8 @@
 //
 // Warps (per CTA): 0 TMA producer, 1 TMEM owner + MMA issuer (leader CTA only),
 // 2..9 epilogue (two warps per TMEM lane quadrant, each owning half of every
-// output half).  A layer runs as quarter steps (n-half, k-half) in the order
+// output half), 10 output warp (keys, per-point stores, the A extension of the tile
+// two ahead — all off the epilogue warps' critical path).  A layer runs as quarter steps (n-half, k-half) in the order
 // (0,0) (1,0) (0,1) (1,1); the epilogue of output half 0 overlaps step (1,1), that
 // of half 1 overlaps step (0,0) of the next layer.
 #include <cuda_bf16.h>
@@ -44,7 +45,8 @@ struct PairCfg {
     static constexpr uint32_t XCHUNK = BR * 32;      // per-CTA extension chunk
     static constexpr int STAGES = N >= 512 ? 5 : 8;
     static constexpr int EPI_WARPS = 8;
-    static constexpr int THREADS = 64 + EPI_WARPS * 32;
+    static constexpr int OUT_WARP = 2 + EPI_WARPS;   // keys / per-point outputs / A extensions
+    static constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
     static constexpr int COLS = NH / 2;              // columns per epilogue thread per half
     static constexpr uint32_t OFF_AX = A_BYTES;
     static constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
@@ -85,9 +87,31 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 // Epilogue of 32 columns of one row (the MMA already added bias and x-part).
 template <int N>
 __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                           uint8_t* A, const float* wo_s, float& dot) {
+                                           uint8_t* A, const float* wo_s, float4& dot) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (!aff && !res && last) {  // plain last layer: straight-line ReLU + output dot (four partial sums)
+        if (act) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+                dot.x = fmaf(w.x, v[i + 0] > 0.f ? v[i + 0] : 0.f, dot.x);
+                dot.y = fmaf(w.y, v[i + 1] > 0.f ? v[i + 1] : 0.f, dot.y);
+                dot.z = fmaf(w.z, v[i + 2] > 0.f ? v[i + 2] : 0.f, dot.z);
+                dot.w = fmaf(w.w, v[i + 3] > 0.f ? v[i + 3] : 0.f, dot.w);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
+                dot.x = fmaf(w.x, v[i + 0], dot.x);
+                dot.y = fmaf(w.y, v[i + 1], dot.y);
+                dot.z = fmaf(w.z, v[i + 2], dot.z);
+                dot.w = fmaf(w.w, v[i + 3], dot.w);
+            }
+        }
+        return;
+    }
     if (!aff && !res && !last) {  // hidden layer: ReLU fused into the bf16 pack
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -140,10 +164,10 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
 #pragma unroll
         for (int i = 0; i < 32; i += 4) {
             const float4 w = *reinterpret_cast<const float4*>(wo_s + c0 + i);
-            dot = fmaf(w.x, v[i + 0], dot);
-            dot = fmaf(w.y, v[i + 1], dot);
-            dot = fmaf(w.z, v[i + 2], dot);
-            dot = fmaf(w.w, v[i + 3], dot);
+            dot.x = fmaf(w.x, v[i + 0], dot.x);
+            dot.y = fmaf(w.y, v[i + 1], dot.y);
+            dot.z = fmaf(w.z, v[i + 2], dot.z);
+            dot.w = fmaf(w.w, v[i + 3], dot.w);
         }
     } else {
 #pragma unroll
@@ -173,8 +197,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     uint64_t* empty = full + C::STAGES;         // [STAGES] each CTA: slot consumed (MMA commit)
     uint64_t* d_full = empty + C::STAGES;       // [2] each CTA: output half j in TMEM
     uint64_t* a_ready = d_full + 2;             // [2] leader: epilogues of half j done (16 warps)
-    uint64_t* ax_full = a_ready + 2;            // [2] leader: A extension buffer b written (16 warps)
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ax_full + 2);
+    uint64_t* ax_full = a_ready + 2;            // [2] leader: A extension buffer b written (2 output warps)
+    uint64_t* out_full = ax_full + 2;           // [tile parity] each CTA: dotbuf holds a finished tile (8 warps)
+    uint64_t* out_empty = out_full + 2;         // [tile parity] each CTA: output warp has read dotbuf
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(out_empty + 2);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -192,7 +218,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
         for (int j = 0; j < 2; ++j) {
             mbar_init(&d_full[j], 1);
             mbar_init(&a_ready[j], 2 * C::EPI_WARPS);
-            mbar_init(&ax_full[j], 2 * C::EPI_WARPS);
+            mbar_init(&ax_full[j], 2);
+            mbar_init(&out_full[j], C::EPI_WARPS);
+            mbar_init(&out_empty[j], 1);
         }
         fence_mbar_init();
     }
@@ -341,7 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 atomicAdd(a.prof + kProfMmaTotal, clock64() - p_start);
             }
         }
-    } else {
+    } else if (warp < C::OUT_WARP) {
         // ---------------------------------------------------------------- epilogue --
         const int e = warp - 2;
         const uint32_t quad = static_cast<uint32_t>(warp & 3);
@@ -349,75 +377,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
         const uint32_t row = quad * 32 + lane;  // row within this CTA's 128
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
-        const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
-        uint32_t dp[2] = {0u, 0u};
-        auto write_ax_tile = [&](int64_t t, int b) {
-            int32_t motion, nrows;
-            int64_t pbase, obase;
-            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
-            const int32_t r = static_cast<int32_t>(rank * C::TM + row);
-            const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
-            if (ch == 0) {
-                const float z0 = (xp[0] - a.shift[0]) * a.scale[0];
-                const float z1 = (xp[1] - a.shift[1]) * a.scale[1];
-                const float z2 = (xp[2] - a.shift[2]) * a.scale[2];
-                write_ax(AX + b * C::AX_BYTES, row, z0, z1, z2);
-                fence_proxy_async_smem();
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
-        };
-        unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0, pe_x = 0;
-        struct Pending {
-            bool live;
-            int par;
-            int32_t motion;
-            int64_t pbase, obase;
-            int32_t rr;
-            bool valid;
-        } pend{false, 0, 0, 0, 0, 0, false};
-        auto flush_output = [&]() {
-            if (!pend.live) return;
-            const unsigned long long c3 = clock64();
-            named_bar_sync(1, C::EPI_WARPS * 32);
-            if (ch == 0) {
-                const int par = pend.par;
-                const float delta = (dotbuf[(par * 2) * C::TM + row] + dotbuf[(par * 2 + 1) * C::TM + row]) + a.bo;
-                if (pend.valid && a.per_point) a.per_point[pend.obase + pend.rr] = delta;
-                if (a.keys) {
-                    unsigned long long key = pend.valid ? row_key(delta, a.index_offset + pend.pbase + pend.rr) : ~0ull;
-                    key = warp_min_u64(key);
-                    if (lane == 0) atomicMin(a.keys + pend.motion, key);
-                    named_bar_sync(2, 4 * 32);
-                    if (e == 0 && lane == 0 && a.counters) {
-                        __threadfence();
-                        const unsigned int prev = atomicAdd(a.counters + pend.motion, 1u);
-                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
-                            __threadfence();
-                            const unsigned long long kk = atomicOr(a.keys + pend.motion, 0ull);
-                            decode_key(kk, a.margin, a.min_out + pend.motion, a.argmin_out + pend.motion,
-                                       a.free_out + pend.motion);
-                        }
-                    }
-                }
-            }
-            pend.live = false;
-            pe_o += clock64() - c3;
-        };
+        uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
+        unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0;
         int64_t k = 0;
-        if (pair < a.n_tiles) write_ax_tile(pair, 0);
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
-            {
-                const unsigned long long c0 = clock64();
-                if (t + npairs < a.n_tiles) write_ax_tile(t + npairs, static_cast<int>((k + 1) & 1));
-                pe_x += clock64() - c0;
-            }
-            int32_t motion, nrows;
-            int64_t pbase, obase;
-            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
-            const int32_t rr = static_cast<int32_t>(rank * C::TM + row);
-            const bool valid = rr < nrows;
-            float dot = 0.f;
+            float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
@@ -454,21 +418,114 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     if (lane == 0) mbar_arrive_remote(a_ready0 + j * 8u);
                     pe_a += clock64() - c2;
                 }
-                if (l == 0) flush_output();  // previous tile's outputs
             }
-            // the output phase of this tile runs after the next tile's layer-0 epilogue
-            // (off the MMA critical path); dotbuf is double-buffered by tile parity
-            dotbuf[((k & 1) * 2 + ch) * C::TM + row] = dot;
-            pend = Pending{true, static_cast<int>(k & 1), motion, pbase, obase, rr, valid};
-            if (t + npairs >= a.n_tiles) flush_output();
+            // hand the row's partial dot to the output warp (dotbuf[parity] is reused two tiles later)
+            const unsigned long long c3 = clock64();
+            const int b = static_cast<int>(k & 1);
+            if (k >= 2) {
+                mbar_wait(&out_empty[b], oe_ph[b]);
+                oe_ph[b] ^= 1u;
+            }
+            dotbuf[(b * 2 + ch) * C::TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&out_full[b]);
+            pe_o += clock64() - c3;
         }
         if (a.prof && e == 0 && lane == 0 && rank == 0) {
             atomicAdd(a.prof + kProfEpiWaitD, pe_d);
             atomicAdd(a.prof + kProfEpiWork, pe_w);
             atomicAdd(a.prof + kProfEpiArrive, pe_a);
             atomicAdd(a.prof + kProfEpiOut, pe_o);
-            atomicAdd(a.prof + kProfEpiAx, pe_x);
         }
+    } else {
+        // ------------------------------------------------------------- output warp --
+        // Per finished tile: delta = dot + bo for this CTA's 128 rows, per-point stores, one
+        // packed-key atomicMin and the per-motion completion counter; then the A extension of
+        // the tile two ahead (same parity), whose point loads are issued before the wait.
+        const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
+        uint32_t of_ph[2] = {0u, 0u};
+        float px[4][3];
+        unsigned long long pe_x = 0;
+        auto load_points = [&](int64_t t) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int32_t r = static_cast<int32_t>(rank * C::TM + q * 32 + lane);
+                const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
+                px[q][0] = xp[0];
+                px[q][1] = xp[1];
+                px[q][2] = xp[2];
+            }
+        };
+        auto store_ax = [&](int b) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                write_ax(AX + b * C::AX_BYTES, static_cast<uint32_t>(q * 32) + lane,
+                         (px[q][0] - a.shift[0]) * a.scale[0], (px[q][1] - a.shift[1]) * a.scale[1],
+                         (px[q][2] - a.shift[2]) * a.scale[2]);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
+        };
+        for (int b = 0; b < 2; ++b) {
+            const int64_t t = pair + b * npairs;
+            if (t < a.n_tiles) {
+                load_points(t);
+                store_ax(b);
+            }
+        }
+        int64_t k = 0;
+        for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+            const int b = static_cast<int>(k & 1);
+            const bool next = t + 2 * npairs < a.n_tiles;
+            if (next) load_points(t + 2 * npairs);
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+            if (a.sleep_hint) mbar_wait_sleep(&out_full[b], of_ph[b], a.sleep_hint);
+            else mbar_wait(&out_full[b], of_ph[b]);
+            of_ph[b] ^= 1u;
+            const unsigned long long c0 = clock64();
+            // every MMA of tile t has completed, so AX[b] is free for tile t + 2 npairs
+            if (next) store_ax(b);
+            float delta[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = q * 32 + static_cast<int>(lane);
+                delta[q] = (dotbuf[(b * 2) * C::TM + r] + dotbuf[(b * 2 + 1) * C::TM + r]) + a.bo;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&out_empty[b]);
+            unsigned long long key = ~0ull;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int32_t rr = static_cast<int32_t>(rank * C::TM + q * 32 + lane);
+                if (rr < nrows) {
+                    if (a.per_point) a.per_point[obase + rr] = delta[q];
+                    const unsigned long long kk = row_key(delta[q], a.index_offset + pbase + rr);
+                    key = kk < key ? kk : key;
+                }
+            }
+            if (a.keys) {
+                key = warp_min_u64(key);
+                if (lane == 0) {
+                    atomicMin(a.keys + motion, key);
+                    if (a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
+                            __threadfence();
+                            const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion, a.free_out + motion);
+                        }
+                    }
+                }
+            }
+            pe_x += clock64() - c0;
+        }
+        if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
     }
 
     tc_fence_before();
