@@ -36,6 +36,23 @@ def test_ragged_point_counts(prec, P):
         assert np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
 
 
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("motions,P", [(3, 1000), (1, 257), (227, 256), (149, 300), (75, 512)])
+def test_tile_counts_around_the_pair_count(prec, motions, P):
+    # width 256: bf16 runs two tiles in flight per CTA pair (odd tile counts leave slot 1 idle
+    # in the last round), fp32 the split kernel; tile counts below, at and above 74 pairs
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 23, w.bound)
+    pts, q = w.make(seed=23, motions=motions, points=P)
+    r = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec, per_point=True)
+    omin, oarg, ofree, opp = O.query_min(w.program, params, pts, q, w.margin, per_point=True, threads=8)
+    assert np.abs(r.per_point.astype(np.float64) - opp).max() <= _tol(prec, w.program)
+    assert np.array_equal(r.min, r.per_point.min(axis=1))
+    assert np.array_equal(r.argmin, r.per_point.argmin(axis=1))
+    r2 = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec)
+    assert np.array_equal(r2.min, r.min) and np.array_equal(r2.argmin, r.argmin)
+
+
 @pytest.mark.parametrize("prec", ["bf16", "fp32_exact"])
 def test_many_motions_few_points(prec):
     w = WORKLOADS["c2"]
