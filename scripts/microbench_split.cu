@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdio>
 #include <random>
 #include <vector>
 
@@ -23,7 +24,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
 }
 
 __global__ void probe(const uint8_t* gA_hi, const uint8_t* gA_lo, const uint8_t* gB_hi, const uint8_t* gB_lo,
-                      float* out_main, float* out_corr) {
+                      float* out_main, float* out_corr, int one_acc) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* A_hi = sm;                  // 128 x 256 fp16 SW128: 4 slabs x 16 KiB
     uint8_t* A_lo = sm + 65536;
@@ -98,9 +99,10 @@ int main() {
     for (auto& x : A) x = static_cast<float>(ua(rng) * (rng() % 3 == 0 ? 0.0 : 1.0));  // relu-like zeros
     for (auto& x : B) x = static_cast<float>(ub(rng));
     std::vector<uint8_t> Ahi(M * K * 2), Alo(M * K * 2), Bhi(N * K * 2), Blo(N * K * 2);
-    auto split = [](float x, __half& hi, __half& lo) {
+    const float LS = getenv("UNSCALED") ? 1.0f : 2048.0f;  // UNSCALED=1: lo stored as plain fp16 (subnormals)
+    auto split = [LS](float x, __half& hi, __half& lo) {
         hi = __float2half_rn(x);
-        lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
+        lo = __float2half_rn((x - __half2float(hi)) * LS);
     };
     for (int r = 0; r < M; ++r)
         for (int k = 0; k < K; ++k) {
@@ -132,12 +134,13 @@ int main() {
     cudaMemcpy(dBl, Blo.data(), Blo.size(), cudaMemcpyHostToDevice);
     const int smem = 131072 + 65536;
     cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    probe<<<1, 128, smem>>>(dAh, dAl, dBh, dBl, dm, dc);
+    const int one_acc = getenv("ONEACC") ? 1 : 0;
+    probe<<<1, 128, smem>>>(dAh, dAl, dBh, dBl, dm, dc, one_acc);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<float> hm(M * N), hc(M * N);
     cudaMemcpy(hm.data(), dm, M * N * 4, cudaMemcpyDeviceToHost);
     cudaMemcpy(hc.data(), dc, M * N * 4, cudaMemcpyDeviceToHost);
-    double e_split = 0, e_fp32 = 0, e_hi = 0, maxabs = 0;
+    double e_split = 0, e_fp32 = 0, e_hi = 0, maxabs = 0, e_one = 0;
     for (int r = 0; r < M; ++r)
         for (int n = 0; n < N; ++n) {
             double ref = 0;
@@ -146,13 +149,16 @@ int main() {
                 ref += static_cast<double>(A[r * K + k]) * B[n * K + k];
                 seq = std::fma(A[r * K + k], B[n * K + k], seq);
             }
-            const double got = static_cast<double>(hm[r * N + n]) + static_cast<double>(hc[r * N + n]) / 2048.0;
+            const double got = static_cast<double>(hm[r * N + n]) + static_cast<double>(hc[r * N + n]) / LS;
+            // single fp32 accumulator variant (UNSCALED): main + corr rounded in fp32
+            const float got1 = one_acc ? hm[r * N + n] : hm[r * N + n] + hc[r * N + n];
+            e_one = std::max(e_one, std::abs(static_cast<double>(got1) - ref));
             e_split = std::max(e_split, std::abs(got - ref));
             e_fp32 = std::max(e_fp32, std::abs(static_cast<double>(seq) - ref));
             e_hi = std::max(e_hi, std::abs(static_cast<double>(hm[r * N + n]) - ref));
             maxabs = std::max(maxabs, std::abs(ref));
         }
-    printf("status %s | max|D| %.3f | split3 err %.3e | fp32 seq-FMA err %.3e | hi-only err %.3e\n",
-           cudaGetErrorString(e), maxabs, e_split, e_fp32, e_hi);
+    printf("status %s | lo scale %.0f | max|D| %.3f | split3 err %.3e | one-acc err %.3e | fp32 seq-FMA err %.3e | hi-only err %.3e\n",
+           cudaGetErrorString(e), LS, maxabs, e_split, e_one, e_fp32, e_hi);
     return 0;
 }
