@@ -5,10 +5,11 @@ One step = one pass of the hot path over one batch: every (point x motion) pair 
 the workload through the fused MLP, per-motion min/argmin and the margin class.
 
 Default workload (N=1): BASELINE.json configs[2] ("c3"): DeepSDF 8x512 concat@4,
-bf16 with fp32 accumulate, 1024 motions x 65536 points.  configs[1] ("c2") is the
-fp32 path (no tensor cores, so it cannot carry the "% of tensor-pipe peak" half of
-the metric) and configs[4] ("c5") is the same network at 128x c3's size (~32 s per
-step at the target rate); other configs: --config c1|c2|c4|c5|c5single.
+bf16 with fp32 accumulate, 1024 motions x 65536 points.  configs[1] ("c2") states fp32
+weights: its FP32 path runs in the reference's order on FFMA (bit-identical; no tensor
+pipe, so it cannot carry the "% of tensor-pipe peak" half of the metric) and
+`--precision fp32_split` runs it fp32-grade on tcgen05; configs[4] ("c5") is the same
+network as c3 at 128x its size; other configs: --config c1|c2|c4|c5|c5single.
 With --gpus N (torchrun, one rank per GPU) every rank evaluates its own motion
 shard of the c5 motion stream with c3's per-GPU size (weak scaling, no collective
 on the data path).
@@ -47,7 +48,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3")
-    ap.add_argument("--precision", default=None, help="override: bf16 | fp32 | fp32_exact")
+    ap.add_argument("--precision", default=None, help="override: bf16 | fp32 | fp32_exact | fp32_split")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -286,7 +287,7 @@ def main():
                 "peak_source": f"{peak_src} bf16_tflops (burst)",
                 "frac_of_sustained": achieved_tf / float(peaks.get("bf16_tflops_sustained", peak)),
                 "flop_per_query": flop_q, "kernel_ms": kernel_ms}
-    elif prec == "fp32" and w.program.width == 256 and not os.environ.get("SVN_FP32_SIMT"):
+    elif prec == "fp32_split":
         # fp32-accurate on tcgen05: every product is three f16 MMAs (hi.hi, hi.lo', lo'.hi), so
         # the algorithmic-FLOP ceiling of the scheme is the measured f16/bf16 peak / 3.
         peak = float(peaks["bf16_tflops"]) / 3.0

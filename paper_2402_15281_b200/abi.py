@@ -17,8 +17,8 @@ LIB_PATH = _build.LIB
 # svn_status
 OK, INVALID_ARGUMENT, CUDA_ERROR, OUT_OF_MEMORY, UNSUPPORTED, IO, FORMAT, TRUNCATION, VERSION = range(9)
 # svn_precision
-PREC_BF16, PREC_FP32, PREC_FP32_EXACT = 0, 1, 2
-PRECISIONS = {"bf16": PREC_BF16, "fp32": PREC_FP32, "fp32_exact": PREC_FP32_EXACT}
+PREC_BF16, PREC_FP32, PREC_FP32_EXACT, PREC_FP32_SPLIT = 0, 1, 2, 3
+PRECISIONS = {"bf16": PREC_BF16, "fp32": PREC_FP32, "fp32_exact": PREC_FP32_EXACT, "fp32_split": PREC_FP32_SPLIT}
 
 
 class SvnLayer(C.Structure):

@@ -526,18 +526,21 @@ svn_status check_prec(const svn_model* m, svn_precision prec) {
     } else if (prec == SVN_PREC_FP32 || prec == SVN_PREC_FP32_EXACT) {
         if (m->N != 128 && m->N != 256 && m->N != 512)
             return fail(SVN_ERR_UNSUPPORTED, "fp32 path needs width 128, 256 or 512");
+    } else if (prec == SVN_PREC_FP32_SPLIT) {
+        if (!m->has_split)
+            return fail(SVN_ERR_UNSUPPORTED, "fp32_split path needs width 256, >= 2 layers and |W| < 1e4");
     } else {
         return fail(SVN_ERR_INVALID_ARGUMENT, "unknown precision");
     }
     return SVN_OK;
 }
 
-// Which fused kernel serves a (model, precision): bf16 tensor cores; fp32-accurate
-// split-fp16 tensor cores (width 256); or SIMT FFMA (fp32_exact, and fp32 otherwise).
+// Which fused kernel serves a (model, precision): bf16 tensor cores; fp32-grade split-fp16
+// tensor cores (fp32_split, width 256); or SIMT FFMA in the oracle's order (fp32, fp32_exact).
 enum class Kind { BF16, SPLIT, SIMT };
-Kind kernel_kind(const svn_model* m, svn_precision prec) {
+Kind kernel_kind(const svn_model*, svn_precision prec) {
     if (prec == SVN_PREC_BF16) return Kind::BF16;
-    if (prec == SVN_PREC_FP32 && m->has_split && !std::getenv("SVN_FP32_SIMT")) return Kind::SPLIT;
+    if (prec == SVN_PREC_FP32_SPLIT) return Kind::SPLIT;
     return Kind::SIMT;
 }
 
@@ -648,7 +651,9 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     ensure_pool(m->device);
     const Kind kind0 = kernel_kind(m, prec);
     FusedArgs a = kind0 == Kind::SPLIT ? m->base_split : m->base;
-    const bool exact = prec == SVN_PREC_FP32_EXACT;
+    // fp32 on the SIMT kernel runs in the oracle's order (no q-fold): at width 512 that costs
+    // nothing measurable (c3/c4: 12.0/16.8 M q/s either way) and makes it bit-identical
+    const bool exact = kind0 == Kind::SIMT;
     a.exact = exact ? 1 : 0;
     a.points = points;
     a.point_stride = 3;
@@ -811,7 +816,7 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
         seg_start = r;
     }
     FusedArgs a = kind == Kind::SPLIT ? m->base_split : m->base;
-    a.exact = prec == SVN_PREC_FP32_EXACT ? 1 : 0;
+    a.exact = kind == Kind::SIMT ? 1 : 0;
     a.points = raw_dev;
     a.point_stride = cols;
     a.P = B;

@@ -7,4 +7,4 @@ done
 timeout 900 python bench.py --config c2 --precision bf16 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2bf16.log 2>&1; echo "c2bf16 rc=$?"
 tail -1 gpurun_out/bench_c2bf16.log | cut -c1-400
 timeout 900 python bench.py --config c1 --precision fp32_exact --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c1exact.log 2>&1; echo "c1exact rc=$?"
-SVN_FP32_SIMT=1 timeout 900 python bench.py --config c2 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2simt.log 2>&1; echo "c2simt rc=$?"
+timeout 900 python bench.py --config c2 --precision fp32_split --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c2split.log 2>&1; echo "c2split rc=$?"

@@ -9,7 +9,7 @@ import pytest
 import paper_2402_15281_b200 as S
 from oracle import oracle as O
 from paper_2402_15281_b200.workloads import WORKLOADS
-from test_gpu_parity import BF16_BOUND
+from test_gpu_parity import BF16_BOUND, FP32_SPLIT_BOUND
 
 pytestmark = pytest.mark.gpu
 
@@ -17,10 +17,12 @@ TOL = {"fp32_exact": 0.0, "fp32": 1e-5}
 
 
 def _tol(prec, prog):
+    if prec == "fp32_split":
+        return FP32_SPLIT_BOUND[prog.name]
     return TOL.get(prec, BF16_BOUND.get(prog.name, 0.1))
 
 
-@pytest.mark.parametrize("prec", ["bf16", "fp32", "fp32_exact"])
+@pytest.mark.parametrize("prec", ["bf16", "fp32", "fp32_exact", "fp32_split"])
 @pytest.mark.parametrize("P", [1, 2, 127, 129, 255, 257, 511, 1000])
 def test_ragged_point_counts(prec, P):
     w = WORKLOADS["c3"] if prec == "bf16" else WORKLOADS["c2"]
@@ -36,7 +38,7 @@ def test_ragged_point_counts(prec, P):
         assert np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
 
 
-@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+@pytest.mark.parametrize("prec", ["bf16", "fp32_split"])
 @pytest.mark.parametrize("motions,P", [(3, 1000), (1, 257), (227, 256), (149, 300), (75, 512)])
 def test_tile_counts_around_the_pair_count(prec, motions, P):
     # width 256: bf16 runs two tiles in flight per CTA pair (odd tile counts leave slot 1 idle

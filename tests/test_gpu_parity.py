@@ -1,9 +1,10 @@
 """GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
 
 Tolerances (BASELINE.json north_star):
-  fp32_exact  bit-identical per-point delta (same fmaf order as oracle/sweptnet_oracle.c)
-  fp32        |delta_gpu - delta_oracle| <= 1e-5 (q-fold reorders the sums; width 256 runs
-              on tcgen05 with split-fp16 operands, width 512 on SIMT FFMA)
+  fp32 / fp32_exact  the FP32 path: |delta_gpu - delta_oracle| <= 1e-5, met with zero error —
+              SIMT FFMA in the oracle's order (oracle/sweptnet_oracle.c), bit-identical
+  fp32_split  fp32-grade on tcgen05 (split-fp16 operands, q-fold, width 256):
+              <= FP32_SPLIT_BOUND[network] (frozen, tests/golden/fp32_split_bounds.json)
   bf16        |delta_gpu - delta_oracle| <= BF16_BOUND[config] (frozen)
 Classification is bit-exact except for motions whose oracle min is within the
 bound of the margin ("ambiguous"), which are counted.
@@ -24,6 +25,8 @@ pytestmark = pytest.mark.gpu
 # (2x the max |bf16 - oracle| on a fixed calibration subset).
 _B = json.loads((Path(__file__).resolve().parent / "golden" / "bf16_bounds.json").read_text())
 BF16_BOUND = {k: v["bound"] for k, v in _B.items() if isinstance(v, dict)}
+_F = json.loads((Path(__file__).resolve().parent / "golden" / "fp32_split_bounds.json").read_text())
+FP32_SPLIT_BOUND = {k: v["bound"] for k, v in _F.items() if isinstance(v, dict)}
 
 
 def _case(key, M, P, seed=3):
@@ -55,6 +58,7 @@ def test_fp32_within_1e5(key, M, P):
     omin, oarg, ofree, opp = _oracle(w.program, params, pts, q, w.margin)
     err = np.abs(r.per_point.astype(np.float64) - opp).max()
     assert err <= 1e-5, err
+    assert np.array_equal(r.per_point, opp)  # the FP32 path runs in the oracle's order
     # the fused min/argmin equal the min/argmin of the kernel's own per-point output
     assert np.array_equal(r.min, r.per_point.min(axis=1))
     assert np.array_equal(r.argmin, r.per_point.argmin(axis=1))
@@ -81,7 +85,7 @@ def test_bf16_within_bound(key, M, P):
     assert np.all((r.argmin == oarg) | (d_at - omin <= bound))
 
 
-@pytest.mark.parametrize("prec", ["fp32_exact", "fp32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32_exact", "fp32", "fp32_split", "bf16"])
 def test_fig2_reference_network(prec):
     prog = S.fig2(3, 256, 6)
     params = S.init_params(prog, 11, "ref")
@@ -90,7 +94,8 @@ def test_fig2_reference_network(prec):
     r = model.query_min(pts, q, 0.0, precision=prec, per_point=True)
     _, _, _, opp = _oracle(prog, params, pts, q, 0.0)
     err = np.abs(r.per_point.astype(np.float64) - opp).max()
-    tol = {"fp32_exact": 0.0, "fp32": 1e-5, "bf16": BF16_BOUND["fig2_3x256"]}[prec]
+    tol = {"fp32_exact": 0.0, "fp32": 0.0, "fp32_split": FP32_SPLIT_BOUND["fig2_3x256"],
+           "bf16": BF16_BOUND["fig2_3x256"]}[prec]
     assert err <= tol, err
 
 
@@ -216,18 +221,26 @@ def test_classification_with_calibrated_output_bias(key):
         print(f"{key} {prec}: free {r.free.mean():.2f}, ambiguous {int(amb.sum())}/48")
 
 
-def test_fp32_split_and_simt_agree(monkeypatch):
-    """Width 256 'fp32' runs on tcgen05 (split-fp16); SVN_FP32_SIMT forces the SIMT kernel.
-    Both must sit within 1e-5 of the oracle, hence within 2e-5 of each other."""
-    w = WORKLOADS["c2"]
-    params = S.init_params(w.program, 41, w.bound)
-    pts, q = w.make(seed=41, motions=5, points=1500)
-    model = S.Model(w.program, params)
-    split = model.query_min(pts, q, w.margin, precision="fp32", per_point=True)
-    monkeypatch.setenv("SVN_FP32_SIMT", "1")
-    simt = model.query_min(pts, q, w.margin, precision="fp32", per_point=True)
-    monkeypatch.delenv("SVN_FP32_SIMT")
-    _, _, _, opp = _oracle(w.program, params, pts, q, w.margin)
-    for r in (split, simt):
-        assert np.abs(r.per_point.astype(np.float64) - opp).max() <= 1e-5
-    assert np.abs(split.per_point.astype(np.float64) - simt.per_point).max() <= 2e-5
+@pytest.mark.parametrize("key,M,P,seed", [("c1", 1, 4096, 3), ("c2", 8, 3000, 3), ("c2", 16, 4096, 2024)])
+def test_fp32_split_within_stated_bound(key, M, P, seed):
+    """fp32_split (width 256 on tcgen05, split-fp16): within the frozen bound of the network,
+    and the fused min/argmin equal those of its own per-point output."""
+    w, pts, q, params = _case(key, M, P, seed)
+    r = S.Model(w.program, params).query_min(pts, q, w.margin, precision="fp32_split", per_point=True)
+    omin, oarg, ofree, opp = _oracle(w.program, params, pts, q, w.margin)
+    bound = FP32_SPLIT_BOUND[w.program.name]
+    err = np.abs(r.per_point.astype(np.float64) - opp).max()
+    print(f"{key} seed {seed}: fp32_split max|err| = {err:.3e} (bound {bound})")
+    assert err <= bound, err
+    assert np.array_equal(r.min, r.per_point.min(axis=1))
+    assert np.array_equal(r.argmin, r.per_point.argmin(axis=1))
+    amb = np.abs(omin.astype(np.float64) - w.margin) <= bound
+    assert np.array_equal(r.free[~amb], ofree[~amb])
+
+
+def test_fp32_split_unsupported_at_width_512():
+    w = WORKLOADS["c3"]
+    model = S.Model(w.program, S.init_params(w.program, 1, w.bound))
+    pts, q = w.make(seed=1, motions=1, points=10)
+    with pytest.raises(S.SvnError, match="fp32_split"):
+        model.query_min(pts, q, w.margin, precision="fp32_split")
