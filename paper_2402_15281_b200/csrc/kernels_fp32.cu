@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG>::THREADS, 1) fused_fp32_kernel(
                 mbar_wait(&full[s], static_cast<uint32_t>((g / C::STAGES) & 1));
                 const float* w = wst + static_cast<size_t>(s) * C::KS * N;
                 const int nk = rows - r0 < C::KS ? rows - r0 : C::KS;
-                for (int kk = 0; kk < nk; ++kk) {
+                auto kstep = [&](int kk) {
                     const float* arow = actT + (a_off + r0 + kk) * C::TM + rg * 8;
                     const float4 a0 = *reinterpret_cast<const float4*>(arow);
                     const float4 a1 = *reinterpret_cast<const float4*>(arow + 4);
@@ -243,6 +243,14 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG>::THREADS, 1) fused_fp32_kernel(
                     for (int i = 0; i < 8; ++i)
 #pragma unroll
                         for (int j = 0; j < C::NC; ++j) acc[i][j] = __fmaf_rn(av[i], wv[j], acc[i][j]);
+                };
+                if (nk == C::KS) {
+                    // full chunk: unrolled so the next k's shared-memory loads are scheduled
+                    // under the current k's FMAs (each output keeps its own k-ordered chain)
+#pragma unroll 4
+                    for (int kk = 0; kk < C::KS; ++kk) kstep(kk);
+                } else {
+                    for (int kk = 0; kk < nk; ++kk) kstep(kk);
                 }
                 __syncthreads();  // every thread is done with stage s
                 if (tid == 0 && g_prod < total_chunks) issue();
