@@ -213,6 +213,30 @@ SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, cons
                                                const double* q01, int64_t M, int32_t steps, double margin,
                                                double* dist_out, uint8_t* free_out, void* stream);
 
+/* ---------------------------------------- Alg. 1: proxy-guided search (§8f) --
+ * gcc_nn_search (collision.cpp:120-130 -> gcc_nn_search_impl, collision.cpp:55-107) with
+ * both callables on the GPU: every proxy in one batched launch (predict_min_distance's
+ * float casts, nn.cpp:466-474), then the geometric checker on the motions in exactly the
+ * order the sequential algorithm visits them — first those with proxy > margin in index
+ * order, then the rest by proxy descending (stable) — in batches of `batch` motions (<= 0:
+ * 64) until the first free one.  found / motion_index / certified_distance are the
+ * sequential algorithm's; nn_checks / exact_checks are the counts IT would report (the GPU
+ * evaluates every proxy and may check up to batch-1 motions past the answer); the seconds
+ * are the wall time of the GPU phases.  HOST buffers: cloud double [P x 3], q01 double
+ * [M x 2 dof]. */
+typedef struct {
+    int32_t found;
+    int32_t motion_index;       /* -1 when no motion is free */
+    double certified_distance;  /* checker distance of the certified motion */
+    int64_t exact_checks;
+    int64_t nn_checks;
+    double proxy_seconds, exact_seconds, total_seconds;
+} svn_search_result;
+
+SVN_API svn_status svn_gcc_nn_search(const svn_model* model, svn_precision prec, const svn_robot_desc* robot,
+                                     const double* cloud, int64_t P, const double* q01, int64_t M, int32_t steps,
+                                     double margin, int32_t batch, svn_search_result* out);
+
 /* Kernel launches issued by this thread since the last reset (evidence for bench.py). */
 SVN_API int64_t svn_launch_count(void);
 SVN_API void svn_launch_count_reset(void);

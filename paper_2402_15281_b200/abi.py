@@ -29,6 +29,13 @@ class SvnModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int32), ("width", C.c_int32), ("dof", C.c_int32), ("layers", C.POINTER(SvnLayer))]
 
 
+class SvnSearchResult(C.Structure):
+    """svn_search_result: sweptnet::SearchResult (collision.hpp:31-40)."""
+    _fields_ = [("found", C.c_int32), ("motion_index", C.c_int32), ("certified_distance", C.c_double),
+                ("exact_checks", C.c_int64), ("nn_checks", C.c_int64), ("proxy_seconds", C.c_double),
+                ("exact_seconds", C.c_double), ("total_seconds", C.c_double)]
+
+
 class SvnError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(msg)
@@ -102,6 +109,7 @@ def _finish(L):
         "svn_eval_grid": (C.c_int, [VP, C.c_int, P, D, P, P, P, I32, P]),
         "svn_gcc_min_distance": (C.c_int, [P, P, I64, P, I64, I32, D, I32, P, P]),
         "svn_gcc_min_distance_device": (C.c_int, [P, P, I64, P, I64, I32, D, P, P, VP]),
+        "svn_gcc_nn_search": (C.c_int, [P, C.c_int, P, P, I64, P, I64, I32, D, I32, C.POINTER(SvnSearchResult)]),
         "svn_launch_count": (I64, []),
         "svn_launch_count_reset": (None, []),
         "svn_kernel_timing_begin": (None, []),
@@ -121,7 +129,7 @@ EXPORTED = ("svn_param_count", "svn_trainable_param_count", "svn_init_params", "
             "svn_model_load_checkpoint", "svn_model_destroy", "svn_query_min_device", "svn_query_min",
             "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
             "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_gcc_min_distance",
-            "svn_gcc_min_distance_device", "svn_launch_count",
+            "svn_gcc_min_distance_device", "svn_gcc_nn_search", "svn_launch_count",
             "svn_launch_count_reset",
             "svn_kernel_timing_begin", "svn_kernel_timing_end", "svn_last_error", "svn_version")
 

@@ -96,3 +96,21 @@ def gcc_min_distance(robot: Robot, points: np.ndarray, q01: np.ndarray, steps: i
     abi.check(abi.lib().svn_gcc_min_distance(C.byref(desc), abi.ptr(pts), pts.shape[0], abi.ptr(q), M, int(steps),
                                              float(margin), int(device), abi.ptr(dist), abi.ptr(free)))
     return dist, free.astype(bool)
+
+
+def gcc_nn_search(model, robot: Robot, cloud: np.ndarray, q01: np.ndarray, steps: int = 200, margin: float = 0.005,
+                  precision: str = "fp32", batch: int = 64) -> dict:
+    """Alg. 1 on the GPU: gcc_nn_search (collision.cpp:120-130, impl 55-107) with the proxy
+    (`model`, one batched launch) and the geometric checker (batches in the sequential
+    algorithm's visiting order).  Returns the fields of sweptnet::SearchResult."""
+    pts = np.ascontiguousarray(cloud, np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(q01, np.float64).reshape(-1, 2 * robot.dof)
+    res = abi.SvnSearchResult()
+    desc, keep = robot.desc()
+    abi.check(abi.lib().svn_gcc_nn_search(model._h, abi.PRECISIONS[precision], C.byref(desc), abi.ptr(pts),
+                                          pts.shape[0], abi.ptr(q), q.shape[0], int(steps), float(margin), int(batch),
+                                          C.byref(res)))
+    return {"found": bool(res.found), "motion_index": int(res.motion_index),
+            "certified_distance": float(res.certified_distance), "exact_checks": int(res.exact_checks),
+            "nn_checks": int(res.nn_checks), "proxy_seconds": float(res.proxy_seconds),
+            "exact_seconds": float(res.exact_seconds), "total_seconds": float(res.total_seconds)}

@@ -88,3 +88,55 @@ def test_gpu_gcc_matches_oracle(dof, wkey):
     assert np.abs(d_gpu - d_ref).max() <= 1e-12
     amb = np.abs(d_ref - 0.02) <= 1e-12
     assert np.array_equal(f_gpu[~amb], f_ref[~amb])
+
+
+def _sequential_search(proxies, dist, margin):
+    """gcc_nn_search_impl (collision.cpp:55-107) over precomputed proxy and checker values."""
+    M = len(proxies)
+    nn = ex = 0
+    done = [False] * M
+    for j in range(M):
+        nn += 1
+        if proxies[j] > margin:
+            ex += 1
+            done[j] = True
+            if dist[j] > margin:
+                return True, j, dist[j], ex, nn
+    for j in sorted((j for j in range(M) if not done[j]), key=lambda j: -proxies[j]):  # stable, descending
+        ex += 1
+        if dist[j] > margin:
+            return True, j, dist[j], ex, nn
+    return False, -1, 0.0, ex, nn
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["loop1", "loop2", "none"])
+def test_gcc_nn_search_matches_sequential_algorithm(case):
+    import paper_2402_15281_b200 as S
+    from paper_2402_15281_b200.robot import gcc_nn_search
+    r = default_robot(6)
+    rng = np.random.default_rng(12)
+    lo, hi = ([0.2, -0.5, 0.1], [0.6, 0.5, 0.8]) if case != "none" else ([-0.2, -0.2, 0.0], [0.2, 0.2, 0.3])
+    cloud = rng.uniform(lo, hi, size=(1200, 3))
+    M, margin, steps = 40, 0.02, 24
+    q01 = rng.uniform(-1, 1, size=(M, 12)) * np.concatenate([r.upper, r.upper])
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 12, w.bound)
+    prox = np.array([O.predict_min_distance(w.program, params, cloud, q[:6], q[6:])[0] for q in q01])
+    params = params.copy()  # move the proxy's decision onto the data: median (loop1) or below (loop2)
+    params[-1] += np.float32(margin - np.median(prox) + (0.0 if case == "loop1" else -10.0))
+    prox = np.array([O.predict_min_distance(w.program, params, cloud, q[:6], q[6:])[0] for q in q01])
+    dist, _ = O.gcc(r, cloud, q01, steps=steps, margin=margin)
+    want = _sequential_search(prox, dist, margin)
+    got = gcc_nn_search(S.Model(w.program, params), r, cloud, q01, steps=steps, margin=margin, precision="fp32",
+                        batch=7)
+    print(case, want, {k: got[k] for k in ("found", "motion_index", "exact_checks", "nn_checks")})
+    assert got["found"] == want[0] and got["motion_index"] == want[1]
+    assert abs(got["certified_distance"] - want[2]) <= 1e-12
+    assert got["exact_checks"] == want[3] and got["nn_checks"] == want[4]
+    if case == "loop1":
+        assert want[0] and want[4] < M  # certified inside the first loop
+    if case == "loop2":
+        assert want[0] and want[4] == M and (prox <= margin).all()
+    if case == "none":
+        assert not want[0]
