@@ -17,6 +17,7 @@
  *   svn_query_min_keys_device point-sharded partial of the above (new)
  *   svn_eval_grid             NN branch of cmd_reconstruct  src/cli.cpp:240-261
  *   svn_gcc_min_distance      gcc_min_distance / gcc_clearance  src/collision.cpp:18-34
+ *   svn_gcc_nn_search         gcc_nn_search / gcc_nn_search_impl  src/collision.cpp:55-107,120-130 (Alg. 1)
  *   svn_keys_finalize_device  decode + margin classification of reduced keys (new)
  *   svn_last_error            std::invalid_argument / IoError what() strings (nn.cpp:98-99,462,465;
  *                             errors.hpp:8-27)
