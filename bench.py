@@ -296,11 +296,16 @@ def main():
                 "peak_source": f"{peak_src} bf16_tflops / 3 (split-fp16: 3 tensor products per fp32 product)",
                 "flop_per_query": flop_q, "kernel_ms": kernel_ms}
     else:
-        peak = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        formula = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+        fp = ROOT / "profiles" / "fp32_peak.json"
+        if fp.exists():  # our FFMA-chain microbenchmark (MEASURED_PEAKS.json has no FP32 figure)
+            peak = float(json.loads(fp.read_text())["ffma_tflops"])
+            src = "measured FFMA peak, scripts/microbench_ffma.cu (profiles/fp32_peak.json)"
+        else:
+            peak, src = formula, "formula 148 SM x 128 FFMA lanes x 2 x sm_max_mhz"
         roof = {"bound": "fp32-simt", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
-                "frac": achieved_tf / peak, "traffic": None,
-                "peak_source": "formula 148 SM x 128 FFMA lanes x 2 x sm_max_mhz (no measured FP32 peak)",
-                "flop_per_query": flop_q, "kernel_ms": kernel_ms}
+                "frac": achieved_tf / peak, "traffic": None, "peak_source": src,
+                "frac_of_formula": achieved_tf / formula, "flop_per_query": flop_q, "kernel_ms": kernel_ms}
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
