@@ -1,5 +1,6 @@
 // fused.cuh — launch parameters shared by the host ABI and the device kernels.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -155,6 +156,22 @@ __device__ __forceinline__ void tile_decode(const FusedArgs& a, int64_t t, int64
         nrows = static_cast<int32_t>(rem < TM ? rem : TM);
     }
 }
+
+// Opt a kernel into > 48 KiB of dynamic shared memory once per device; safe under concurrent
+// host callers (a repeated set is idempotent, the per-device bit only skips the call).
+struct SmemOptIn {
+    std::atomic<unsigned long long> done{0ull};
+    cudaError_t ensure(const void* kernel, int bytes) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        const unsigned long long bit = dev < 64 ? (1ull << dev) : 0ull;
+        if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+        return e;
+    }
+};
 
 // Launchers (kernels_*.cu).
 cudaError_t launch_motion_bias(const FusedArgs& a, const float* wq /*[n_mb][2dof][N]*/,

@@ -538,13 +538,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
 template <int N>
 static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
     using C = PairCfg<N>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(fused_bf16_pair_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static SmemOptIn opt;
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pair_kernel<N>), (int)C::SMEM);
+    if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;

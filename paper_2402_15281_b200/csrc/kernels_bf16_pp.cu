@@ -536,13 +536,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
 }
 
 cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e =
-            cudaFuncSetAttribute(fused_bf16_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pp::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static SmemOptIn opt;
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pp_kernel), (int)pp::SMEM);
+    if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     const int64_t need = (a.n_tiles + 1) / 2;  // two tiles in flight per pair
     if (need < pairs) pairs = need;

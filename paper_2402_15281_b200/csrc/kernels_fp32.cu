@@ -308,13 +308,9 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG>::THREADS, 1) fused_fp32_kernel(
 template <int N, int CG>
 static cudaError_t launch_fp32_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
     using C = Fp32Cfg<N, CG>;
-    static bool attr_set = false;  // benign race: idempotent attribute set
-    if (!attr_set) {
-        cudaError_t e =
-            cudaFuncSetAttribute(fused_fp32_kernel<N, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static SmemOptIn opt;
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_fp32_kernel<N, CG>), (int)C::SMEM);
+    if (e != cudaSuccess) return e;
     int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
     if (grid < 1) return cudaSuccess;
     fused_fp32_kernel<N, CG><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, st>>>(a);

@@ -19,6 +19,8 @@
 
 #include <cstdint>
 
+#include <mutex>
+
 #include "gcc.cuh"
 
 namespace svn {
@@ -213,9 +215,15 @@ cudaError_t launch_gcc(const GccArgs& a, double margin, double* dist, uint8_t* f
     const unsigned g = static_cast<unsigned>((a.M + 255) / 256);
     gcc_init_kernel<<<g, 256, 0, st>>>(a.keys, a.M);
     const size_t smem = gcc_smem_bytes(a.steps, a.ncap);
-    cudaError_t e = cudaFuncSetAttribute(gcc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    gcc_kernel<<<static_cast<unsigned>(a.M * a.chunks), 256, smem, st>>>(a);
+    {
+        // the opt-in size depends on (steps, capsules): set and launch under one lock so
+        // concurrent host callers with different sizes cannot interleave
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lock(mu);
+        cudaError_t e = cudaFuncSetAttribute(gcc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        gcc_kernel<<<static_cast<unsigned>(a.M * a.chunks), 256, smem, st>>>(a);
+    }
     gcc_finalize_kernel<<<g, 256, 0, st>>>(a.keys, a.M, margin, dist, free_out);
     return cudaGetLastError();
 }

@@ -465,13 +465,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
 }
 
 cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e =
-            cudaFuncSetAttribute(fused_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp::SMEM);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    static SmemOptIn opt;
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_split_kernel), (int)sp::SMEM);
+    if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;
