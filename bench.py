@@ -206,8 +206,15 @@ def main():
     import torch.distributed as dist
     import paper_2402_15281_b200 as S
 
+    # SVN_BENCH_BACKEND / SVN_BENCH_DEVICE exist only to exercise the multi-rank code path
+    # on a one-GPU box (gloo, every rank on device 0); production runs use NCCL, rank = GPU.
+    backend = os.environ.get("SVN_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("SVN_BENCH_DEVICE", local))
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
