@@ -21,7 +21,7 @@ from typing import Callable
 
 import numpy as np
 
-from .program import LayerProgram, deepsdf, plain
+from .program import LayerProgram, deepsdf, fig2, plain
 
 BIN_LO = np.array([0.0, -0.4, 0.0])
 BIN_HI = np.array([1.2, 0.4, 0.5])
@@ -163,4 +163,9 @@ WORKLOADS: dict[str, Workload] = {
     "c5single": Workload("c5single", "DeepSDF 8x512 concat@4 bf16, 1 motion x 16777216 points (point-sharded)",
                          deepsdf(8, 512, 6, 4), 1, 1 << 24, 0.02, "bf16", "he", bin_cloud,
                          lambda: limits_default(6)),
+    # context only (not a BASELINE config): the network the paper timed on an RTX 3090
+    # (Fig. 2 wiring, 5 blocks x 512), one motion x 20000 points as there,
+    # reference init (nn.cpp:57-93); --motions widens it to a batch of motions
+    "paper": Workload("paper", "paper's Fig. 2 5x512 network (PAPER.md:556), 1 motion x 20000 points",
+                      fig2(5, 512, 6), 1, 20000, 0.005, "bf16", "ref", bin_cloud, lambda: limits_default(6)),
 }
