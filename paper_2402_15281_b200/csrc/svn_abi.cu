@@ -79,6 +79,60 @@ int layer_k(const svn_layer* layers, int l, int N, int in) {
     return N + (layers[l].concat ? in : 0);
 }
 
+// bf16 kernels only: fold every Fig. 2 block's BN affine out of the epilogue (nn.cpp:125:
+// h += max(a,0)*s + t).  With s >= 0 (or no activation), max(a,0)*s = max(s*a,0), so s scales
+// the layer's weight rows and bias; the shifts t are carried as a running offset c (the
+// kernel keeps h~ = h - c) and re-enter as W_h.c in the next layer's bias and wo.c in b_o.
+// The epilogue of a folded layer is then ReLU + residual only.  Returns the folded
+// parameter buffer (same layout) and which layers were folded; layers with a negative s
+// under ReLU keep their affine (their offset still folds).  Arithmetic in double.
+std::vector<float> fold_affine_bf16(const svn_model_desc* d, const float* params, int64_t n_params,
+                                    std::vector<char>& folded) {
+    const int N = d->width, in = 3 + 2 * d->dof, L = d->n_layers;
+    std::vector<float> P(params, params + n_params);
+    folded.assign(static_cast<size_t>(L), 0);
+    std::vector<double> c(static_cast<size_t>(N), 0.0), cn(static_cast<size_t>(N), 0.0);
+    int64_t off = 2 * in;
+    for (int l = 0; l < L; ++l) {
+        const svn_layer& ly = d->layers[l];
+        const int K = layer_k(d->layers, l, N, in);
+        float* W = P.data() + off;
+        float* b = W + static_cast<int64_t>(N) * K;
+        const bool res = ly.residual && l > 0;
+        if (l > 0)
+            for (int n = 0; n < N; ++n) {  // the incoming offset, through the h-part weights
+                double acc = b[n];
+                for (int k = 0; k < N; ++k) acc += static_cast<double>(W[static_cast<int64_t>(k) * N + n]) * c[k];
+                b[n] = static_cast<float>(acc);
+            }
+        for (int n = 0; n < N; ++n) cn[n] = res ? c[n] : 0.0;
+        if (ly.affine) {
+            const float *gamma = b + N, *beta = b + 2 * N, *mean = b + 3 * N, *var = b + 4 * N;
+            std::vector<float> sv(N), tv(N);
+            bool ok = true;
+            for (int n = 0; n < N; ++n) {
+                sv[n] = gamma[n] / std::sqrt(var[n] + 1e-5f);  // as the model build (nn.cpp:108-110)
+                tv[n] = std::fma(-mean[n], sv[n], beta[n]);
+                if (ly.act && !(sv[n] >= 0.0f)) ok = false;
+            }
+            if (ok) {
+                for (int n = 0; n < N; ++n) {
+                    for (int k = 0; k < K; ++k) W[static_cast<int64_t>(k) * N + n] *= sv[n];
+                    b[n] *= sv[n];
+                    cn[n] += tv[n];
+                }
+                folded[static_cast<size_t>(l)] = 1;
+            }
+        }
+        c.swap(cn);
+        off += static_cast<int64_t>(N) * K + N + (ly.affine ? 4 * N : 0);
+    }
+    double bo = P[static_cast<size_t>(off + N)];
+    for (int n = 0; n < N; ++n) bo += static_cast<double>(P[static_cast<size_t>(off + n)]) * c[n];
+    P[static_cast<size_t>(off + N)] = static_cast<float>(bo);
+    return P;
+}
+
 svn_status validate_desc(const svn_model_desc* d) {
     if (!d || !d->layers) return fail(SVN_ERR_INVALID_ARGUMENT, "model: null descriptor");
     if (d->n_layers < 1 || d->n_layers > kMaxLayers)
@@ -140,6 +194,10 @@ struct svn_model {
     float* d_mbbase = nullptr; // [n_mb][N]
     float* d_wxslots = nullptr; // [n_mb][3][N] x-part columns of the concat layers
     bool has_bf16 = false;
+    FusedArgs base_bf16{};       // bf16 kernels: base with the BN affine folded (see fold_affine_bf16)
+    float* d_wq_bf = nullptr;     // K0 inputs of the bf16 kernels, from the folded parameters
+    float* d_mbbase_bf = nullptr;
+    float* d_wxslots_bf = nullptr;
 
     template <class T>
     svn_status upload(const T* host, size_t count, T** out) {
@@ -354,8 +412,10 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
     if (N == 256 || N == 512) {
         const int NH = N / 2, KSL = NH / 64;
         const size_t chunk_elems = static_cast<size_t>(NH) * 64;
+        std::vector<char> folded;
+        const std::vector<float> pbf = fold_affine_bf16(d, params, n_params, folded);
         std::vector<__nv_bfloat16> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * N * N);
-        const float* Wl = params + 2 * in;
+        const float* Wl = pbf.data() + 2 * in;
         size_t pos = 0;
         for (int l = 0; l < L; ++l) {
             const int K = layer_k(d->layers, l, N, in);
@@ -398,16 +458,26 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         const int BR = N == 256 ? N / 2 : N / 4;  // B rows per CTA per TMA box (128 for both kernels)
         if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return cleanup_fail(st);
         std::vector<uint8_t> xm;
-        const float* Wb = params + 2 * in;
+        const float* Wb = pbf.data() + 2 * in;
+        std::vector<float> wq_bf, mbbase_bf, wx_bf;  // K0 inputs from the folded parameters
         for (int l = 0; l < L; ++l) {
             const int K = layer_k(d->layers, l, N, in);
+            const float* Wfull = Wb;
             const float* b = Wb + static_cast<int64_t>(N) * K;
             LayerDev& ld = a.layer[l];
             ld.ext = 0;
             ld.ext_row = 0;
+            bool bias_zero = true;
+            for (int n = 0; n < N; ++n)
+                if (b[n] != 0.0f) bias_zero = false;
             if (ld.mb_slot >= 0) {
                 ld.ext = 2;
-            } else if (!ld.bias_zero) {
+                const int xoff = (l == 0) ? 0 : N;
+                wq_bf.insert(wq_bf.end(), Wfull + static_cast<int64_t>(xoff + 3) * N,
+                             Wfull + static_cast<int64_t>(xoff + 3 + nq) * N);
+                wx_bf.insert(wx_bf.end(), Wfull + static_cast<int64_t>(xoff) * N, Wfull + static_cast<int64_t>(xoff + 3) * N);
+                mbbase_bf.insert(mbbase_bf.end(), b, b + N);
+            } else if (!bias_zero) {
                 ld.ext = 1;
                 ld.ext_row = static_cast<int64_t>(xm.size() / 32);
                 const size_t base = xm.size();
@@ -435,6 +505,13 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         uint8_t* dxm = nullptr;
         if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
         if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return cleanup_fail(st);
+        if ((st = m->upload(wq_bf.data(), wq_bf.size(), &m->d_wq_bf)) != SVN_OK) return cleanup_fail(st);
+        if ((st = m->upload(mbbase_bf.data(), mbbase_bf.size(), &m->d_mbbase_bf)) != SVN_OK) return cleanup_fail(st);
+        if ((st = m->upload(wx_bf.data(), wx_bf.size(), &m->d_wxslots_bf)) != SVN_OK) return cleanup_fail(st);
+        m->base_bf16 = a;
+        for (int l = 0; l < L; ++l)
+            if (folded[static_cast<size_t>(l)]) m->base_bf16.layer[l].flags &= ~kAffine;
+        m->base_bf16.bo = pbf[static_cast<size_t>(n_params - 1)];
         m->has_bf16 = true;
     }
 
@@ -632,7 +709,7 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
     svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N == 256 ? m->N / 2 : m->N / 4));
     if (s != SVN_OK) return s;
-    SVN_CUDA(launch_motion_ext(a, m->d_wq, m->d_mbbase, m->d_wxslots, ext, keys, counters, n_keys, st),
+    SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, ext, keys, counters, n_keys, st),
              "motion_ext kernel");
     ++g_launches;
     return SVN_OK;
@@ -651,7 +728,7 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     DeviceGuard guard(m->device);
     ensure_pool(m->device);
     const Kind kind0 = kernel_kind(m, prec);
-    FusedArgs a = kind0 == Kind::SPLIT ? m->base_split : m->base;
+    FusedArgs a = kind0 == Kind::SPLIT ? m->base_split : kind0 == Kind::BF16 ? m->base_bf16 : m->base;
     // fp32 on the SIMT kernel runs in the oracle's order (no q-fold): at width 512 that costs
     // nothing measurable (c3/c4: 12.0/16.8 M q/s either way) and makes it bit-identical
     const bool exact = kind0 == Kind::SIMT;
@@ -816,7 +893,7 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
         ++nseg;
         seg_start = r;
     }
-    FusedArgs a = kind == Kind::SPLIT ? m->base_split : m->base;
+    FusedArgs a = kind == Kind::SPLIT ? m->base_split : kind == Kind::BF16 ? m->base_bf16 : m->base;
     a.exact = kind == Kind::SIMT ? 1 : 0;
     a.points = raw_dev;
     a.point_stride = cols;

@@ -244,3 +244,21 @@ def test_fp32_split_unsupported_at_width_512():
     pts, q = w.make(seed=1, motions=1, points=10)
     with pytest.raises(S.SvnError, match="fp32_split"):
         model.query_min(pts, q, w.margin, precision="fp32_split")
+
+
+@pytest.mark.parametrize("width,blocks", [(256, 3), (512, 5)])
+@pytest.mark.parametrize("neg", [None, 2])
+def test_fig2_bf16_affine_fold_with_trained_like_bn(width, blocks, neg):
+    """The bf16 kernels fold each block's BN affine into its weights and carry the shifts as an
+    offset (svn_abi.cu fold_affine_bf16).  With non-trivial BN statistics — and a layer with
+    negative gamma columns, which is kept unfolded — the result stays within the network's
+    frozen bf16 bound of the oracle."""
+    from fig2_bn import randomize_bn
+    prog = S.fig2(blocks, width, 6)
+    params = randomize_bn(prog, S.init_params(prog, 7, "ref"), 7, negative_gamma_layer=neg)
+    pts, q = WORKLOADS["c2"].make(seed=7, motions=4, points=1500)
+    r = S.Model(prog, params).query_min(pts, q, 0.0, precision="bf16", per_point=True)
+    _, _, _, opp = _oracle(prog, params, pts, q, 0.0)
+    err = np.abs(r.per_point.astype(np.float64) - opp).max()
+    assert err <= BF16_BOUND[prog.name], err
+    assert np.array_equal(r.min, r.per_point.min(axis=1))
