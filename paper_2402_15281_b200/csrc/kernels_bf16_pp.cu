@@ -103,20 +103,6 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         }
         return;
     }
-    if (act && res && !aff && !last) {  // folded Fig. 2 block: h~ += ReLU(a), as bf16x2
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            uint4* slot = reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
-            const uint4 o = *slot;
-            uint4 p;
-            p.x = add_bf16x2(pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
-            p.y = add_bf16x2(pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]), o.y);
-            p.z = add_bf16x2(pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]), o.z);
-            p.w = add_bf16x2(pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]), o.w);
-            *slot = p;
-        }
-        return;
-    }
     if (!aff && !res && !last) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
@@ -133,6 +119,20 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
                 p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
             }
             *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
+        }
+        return;
+    }
+    if (act && res && !aff && !last) {  // folded Fig. 2 block: h~ += ReLU(a), as bf16x2
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint4* slot = reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
+            const uint4 o = *slot;
+            uint4 p;
+            p.x = add_bf16x2(pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
+            p.y = add_bf16x2(pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]), o.y);
+            p.z = add_bf16x2(pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]), o.z);
+            p.w = add_bf16x2(pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]), o.w);
+            *slot = p;
         }
         return;
     }
