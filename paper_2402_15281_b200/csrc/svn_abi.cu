@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -722,6 +723,31 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
     if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
     if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    {
+        // TMA row coordinates of the per-motion extension stream are int32: beyond ~1e9 rows
+        // (about a million motions at width 512) the query runs as consecutive motion chunks
+        static const int64_t override_max = [] {
+            const char* e = std::getenv("SVN_MAX_MOTIONS_PER_LAUNCH");  // test hook
+            return e ? std::atoll(e) : 0ll;
+        }();
+        const int64_t rows_per_motion = static_cast<int64_t>(m->n_mb ? m->n_mb : 1) * m->N * 2;
+        int64_t max_m = (static_cast<int64_t>(INT32_MAX) / 2) / rows_per_motion;
+        if (override_max > 0) max_m = override_max;
+        if (max_m < 1) max_m = 1;
+        if (M > max_m) {
+            const int64_t nq = 2 * static_cast<int64_t>(m->dof);
+            for (int64_t b0 = 0; b0 < M; b0 += max_m) {
+                const int64_t n = std::min(max_m, M - b0);
+                const svn_status s = query_dense(m, prec, points, P, index_offset, q01 + b0 * nq, n, margin,
+                                                 min_out ? min_out + b0 : nullptr, argmin_out ? argmin_out + b0 : nullptr,
+                                                 free_out ? free_out + b0 : nullptr,
+                                                 per_point ? per_point + b0 * P : nullptr,
+                                                 keys_partial ? keys_partial + b0 : nullptr, st);
+                if (s != SVN_OK) return s;
+            }
+            return SVN_OK;
+        }
+    }
     if (P + index_offset > 0xFFFFFFFFll) return fail(SVN_ERR_UNSUPPORTED, "query: more than 2^32 points");
     svn_status s = check_prec(m, prec);
     if (s != SVN_OK) return s;

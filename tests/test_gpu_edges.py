@@ -181,3 +181,38 @@ def test_eval_grid_matches_reference_reconstruction(prec):
         assert np.array_equal(grid, ref)
     else:
         assert np.abs(grid.astype(np.float64) - ref).max() <= BF16_BOUND[w.program.name]
+
+
+def test_motion_chunking_matches_single_launch():
+    """Queries beyond the per-launch motion limit (int32 TMA rows) run as motion chunks; the
+    limit is lowered through the test hook in a subprocess so the chunked path is exercised."""
+    import subprocess
+    import sys
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, "{root}")
+import paper_2402_15281_b200 as S
+from paper_2402_15281_b200.workloads import WORKLOADS
+out = []
+for key, prec in (("c3", "bf16"), ("c2", "bf16"), ("c2", "fp32_split"), ("c2", "fp32")):
+    w = WORKLOADS[key]
+    p = S.init_params(w.program, 5, w.bound)
+    pts, q = w.make(seed=5, motions=23, points=700)
+    r = S.Model(w.program, p).query_min(pts, q, w.margin, precision=prec, per_point=True)
+    out.append(np.concatenate([r.min, r.argmin.astype(np.float32), r.free.astype(np.float32), r.per_point.ravel()]))
+np.save(sys.argv[1], np.concatenate(out))
+'''
+    from pathlib import Path
+    import tempfile
+    import os
+    root = str(Path(__file__).resolve().parents[1])
+    d = tempfile.mkdtemp()
+    res = []
+    for i, env_max in enumerate(("", "5")):
+        env = dict(os.environ)
+        if env_max:
+            env["SVN_MAX_MOTIONS_PER_LAUNCH"] = env_max
+        f = os.path.join(d, f"r{i}.npy")
+        subprocess.run([sys.executable, "-c", code.replace("{root}", root), f], check=True, env=env)
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1])
