@@ -901,6 +901,26 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
     if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
     svn_status s = check_prec(m, prec);
     if (s != SVN_OK) return s;
+    {
+        // every row can be its own motion: keep the per-motion extension stream inside the
+        // int32 TMA row range by running large batches as row chunks (rows are independent)
+        static const int64_t override_max = [] {
+            const char* e = std::getenv("SVN_MAX_MOTIONS_PER_LAUNCH");  // test hook
+            return e ? std::atoll(e) : 0ll;
+        }();
+        const int64_t rows_per_motion = static_cast<int64_t>(m->n_mb ? m->n_mb : 1) * m->N * 2;
+        int64_t max_b = (static_cast<int64_t>(INT32_MAX) / 2) / rows_per_motion;
+        if (override_max > 0) max_b = override_max;
+        if (max_b < 1) max_b = 1;
+        if (B > max_b) {
+            for (int64_t b0 = 0; b0 < B; b0 += max_b) {
+                const int64_t n = std::min(max_b, B - b0);
+                s = forward_rows(m, prec, raw_host + b0 * cols, raw_dev + b0 * cols, n, cols, out_dev + b0, st);
+                if (s != SVN_OK) return s;
+            }
+            return SVN_OK;
+        }
+    }
     const Kind kind = kernel_kind(m, prec);
     const int nq = 2 * m->dof, TM = tile_rows(kind, m->N);
     std::vector<float> qseg;

@@ -216,3 +216,35 @@ np.save(sys.argv[1], np.concatenate(out))
         subprocess.run([sys.executable, "-c", code.replace("{root}", root), f], check=True, env=env)
         res.append(np.load(f))
     assert np.array_equal(res[0], res[1])
+
+
+def test_forward_eval_row_chunking_matches_single_launch():
+    """forward_eval with every row its own motion, run as row chunks through the test hook."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    from pathlib import Path
+    code = r'''
+import numpy as np, sys
+sys.path.insert(0, "{root}")
+import paper_2402_15281_b200 as S
+from paper_2402_15281_b200.workloads import WORKLOADS
+w = WORKLOADS["c2"]
+p = S.init_params(w.program, 9, w.bound)
+pts, q = w.make(seed=9, motions=300, points=1)
+raw = np.concatenate([np.repeat(pts, 300, 0), q], 1).astype(np.float32)
+m = S.Model(w.program, p)
+np.save(sys.argv[1], np.concatenate([m.forward_eval(raw, precision=pr) for pr in ("bf16", "fp32", "fp32_split")]))
+'''
+    root = str(Path(__file__).resolve().parents[1])
+    d = tempfile.mkdtemp()
+    res = []
+    for i, env_max in enumerate(("", "37")):
+        env = dict(os.environ)
+        if env_max:
+            env["SVN_MAX_MOTIONS_PER_LAUNCH"] = env_max
+        f = os.path.join(d, f"r{i}.npy")
+        subprocess.run([sys.executable, "-c", code.replace("{root}", root), f], check=True, env=env)
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1])
