@@ -9,6 +9,7 @@ namespace svn {
 
 constexpr int kMaxLayers = 32;
 constexpr int kMaxIn = 32;  // input_dim = 3 + 2*dof <= 32
+constexpr int kFp32SmallTile = 32;  // SIMT tile rows when a query has fewer big tiles than SMs
 
 enum : int { kConcat = 1, kAct = 2, kAffine = 4, kResidual = 8 };
 
@@ -60,6 +61,7 @@ struct FusedArgs {
     int64_t n_tiles;
     const TileDesc* tiles;     // non-null: explicit tile table (forward_eval segments)
     int exact;                 // fp32 exact order (no q fold)
+    int tile_rows;             // rows per work item the host cut the tiles with (SIMT: 128/64, or 32)
     unsigned sleep_hint;       // bf16 kernel: try_wait suspend hint (ns) for idle-warp waits, 0 = poll
     // outputs
     unsigned long long* keys;  // [M] packed (orderable(delta) << 32 | index), or null

@@ -106,9 +106,11 @@ __device__ __forceinline__ void tile_done(const FusedArgs& a, int32_t motion) {
 }
 
 // ------------------------------------------------------------------ K1f -----
-template <int N, int CG = 32>
+template <int N, int CG = 32, int TMO = 0>
 struct Fp32Cfg {
-    static constexpr int TM = N >= 512 ? 64 : 128;  // rows per tile (activations must fit in smem)
+    // rows per tile (activations must fit in smem); TMO = 32 for workloads with fewer tiles
+    // than SMs, where per-warp issue, not the SM's FMA rate, bounds a tile
+    static constexpr int TM = TMO ? TMO : (N >= 512 ? 64 : 128);
     static constexpr int THREADS = TM / 8 * CG;     // TM/8 row groups x CG column groups
     static constexpr int NC = N / CG;               // columns per thread (8 x NC register tile)
     static constexpr int KS = 4096 / N;           // weight rows per 16 KiB chunk
@@ -130,9 +132,9 @@ __device__ __forceinline__ int layer_rows(const FusedArgs& a, int l) {
     return (a.exact || !concat) ? a.wt_rows[l] : a.wt_rows[l] - 2 * a.dof;
 }
 
-template <int N, int CG>
-__global__ void __launch_bounds__(Fp32Cfg<N, CG>::THREADS, 1) fused_fp32_kernel(const __grid_constant__ FusedArgs a) {
-    using C = Fp32Cfg<N, CG>;
+template <int N, int CG, int TMO>
+__global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_kernel(const __grid_constant__ FusedArgs a) {
+    using C = Fp32Cfg<N, CG, TMO>;
     extern __shared__ __align__(128) uint8_t smem[];
     float* actT = reinterpret_cast<float*>(smem);
     float* wst = reinterpret_cast<float*>(smem + C::ACT_BYTES);
@@ -305,15 +307,15 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG>::THREADS, 1) fused_fp32_kernel(
     }
 }
 
-template <int N, int CG>
+template <int N, int CG, int TMO = 0>
 static cudaError_t launch_fp32_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
-    using C = Fp32Cfg<N, CG>;
+    using C = Fp32Cfg<N, CG, TMO>;
     static SmemOptIn opt;
-    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_fp32_kernel<N, CG>), (int)C::SMEM);
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_fp32_kernel<N, CG, TMO>), (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
     if (grid < 1) return cudaSuccess;
-    fused_fp32_kernel<N, CG><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, st>>>(a);
+    fused_fp32_kernel<N, CG, TMO><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -326,6 +328,14 @@ static int fp32_cg() {
 }
 
 cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    if (a.tile_rows == kFp32SmallTile) {  // few tiles: 32-row tiles, 4 warps each (64 columns gave 8 warps
+        switch (a.N) {                     // but measured 8 % slower on c1)
+            case 128: return launch_fp32_n<128, 32, kFp32SmallTile>(a, num_sms, st);
+            case 256: return launch_fp32_n<256, 32, kFp32SmallTile>(a, num_sms, st);
+            case 512: return launch_fp32_n<512, 32, kFp32SmallTile>(a, num_sms, st);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (a.N) {
         case 128: return launch_fp32_n<128, 32>(a, num_sms, st);
         case 256: return fp32_cg() == 16 ? launch_fp32_n<256, 16>(a, num_sms, st) : launch_fp32_n<256, 32>(a, num_sms, st);

@@ -624,6 +624,12 @@ Kind kernel_kind(const svn_model*, svn_precision prec) {
 }
 
 int tile_rows(Kind k, int N) { return k == Kind::SIMT ? (N >= 512 ? 64 : 128) : 256; }
+// SIMT: a query with fewer big tiles than SMs is cut into 32-row tiles (4 warps per CTA,
+// more SMs busy; each output's k-ordered FMA chain is unchanged)
+int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
+    const int t = tile_rows(k, N);
+    return (k == Kind::SIMT && big_tiles < num_sms) ? kFp32SmallTile : t;
+}
 
 // Scratch buffers freed on the stream when the call's kernels are done.
 struct Scratch {
@@ -765,7 +771,9 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.q01 = q01;
     a.M = M;
     const Kind kind = kernel_kind(m, prec);
-    const int TM = tile_rows(kind, m->N);
+    const int TM0 = tile_rows(kind, m->N);
+    const int TM = tile_rows_for(kind, m->N, M * ((P + TM0 - 1) / TM0), m->num_sms);
+    a.tile_rows = TM;
     a.tiles_per_motion = (P + TM - 1) / TM;
     a.n_tiles = a.tiles_per_motion * M;
     a.tiles = nullptr;
@@ -922,7 +930,8 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
         }
     }
     const Kind kind = kernel_kind(m, prec);
-    const int nq = 2 * m->dof, TM = tile_rows(kind, m->N);
+    const int TM0 = tile_rows(kind, m->N);
+    const int nq = 2 * m->dof, TM = tile_rows_for(kind, m->N, (B + TM0 - 1) / TM0, m->num_sms);
     std::vector<float> qseg;
     std::vector<TileDesc> tiles;
     int64_t seg_start = 0;
@@ -946,6 +955,7 @@ static svn_status forward_rows(const svn_model* m, svn_precision prec, const flo
     a.P = B;
     a.M = nseg;
     a.n_tiles = static_cast<int64_t>(tiles.size());
+    a.tile_rows = TM;
     a.tiles_per_motion = 1;
     a.per_point = out_dev;
     a.keys = nullptr;
