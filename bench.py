@@ -146,19 +146,19 @@ def build_native_oracle():
         return O.lib(), "x86-64-v3"
 
 
-def cpu_sample(w, threads):
-    """Bounded sample of the workload for the CPU path: `threads` motions x a point
-    count sized for ~10-20 s of CPU work at ~2 ns/FLOP-per-core."""
+def cpu_sample(w, threads, seconds=10.0):
+    """Bounded sample of the workload for the CPU path: `threads` motions x a point count
+    sized for ~`seconds` of CPU work (the oracle runs ~1.4e10 FLOP/s per core here)."""
     fq = w.program.flops_per_query()
-    budget = 4e10 * max(1, threads)  # FLOPs for the whole sample
+    budget = 1.4e10 * seconds * max(1, threads)  # FLOPs for the whole sample
     M = max(1, min(w.motions, threads))
     per_motion = int(max(256, min(w.points, budget / M / fq)))
     return M, per_motion
 
 
-def run_cpu(w, params, seed, threads, lib, steps, warmup):
+def run_cpu(w, params, seed, threads, lib, steps, warmup, seconds=10.0):
     from oracle import oracle as O
-    M, P = cpu_sample(w, threads)
+    M, P = cpu_sample(w, threads, seconds)
     pts, q = w.make(seed=seed, motions=M, points=P)
     times = []
     for i in range(warmup + steps):
@@ -190,7 +190,9 @@ def main():
         params = S.init_params(w.program, args.seed, w.bound)
         threads = os.cpu_count() or 1
         lib, march = build_native_oracle()
-        val, sample = run_cpu(w, params, args.seed, threads, lib, max(1, args.steps), max(0, min(args.warmup, 1)))
+        steps, warm = max(1, args.steps), max(0, min(args.warmup, 1))
+        per_step = max(2.0, min(10.0, 120.0 / (steps + warm)))  # whole arm within ~2 minutes
+        val, sample = run_cpu(w, params, args.seed, threads, lib, steps, warm, per_step)
         line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
