@@ -554,7 +554,9 @@ cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t s
     cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pp_kernel), (int)pp::SMEM);
     if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
-    const int64_t need = (a.n_tiles + 1) / 2;  // two tiles in flight per pair
+    // two tiles in flight per pair, unless there are too few tiles to fill the SMs that way:
+    // then one tile per pair (latency-bound queries finish ~2x sooner)
+    const int64_t need = a.n_tiles <= pairs ? a.n_tiles : (a.n_tiles + 1) / 2;
     if (need < pairs) pairs = need;
     if (pairs < 1) return cudaSuccess;
     fused_bf16_pp_kernel<<<static_cast<unsigned>(2 * pairs), pp::THREADS, pp::SMEM, st>>>(a);
