@@ -646,6 +646,47 @@ struct Scratch {
     }
 };
 
+// Per-thread, per-device staging of the host-buffer entry points: one pinned host block and
+// one device block, grown on demand and reused, so a call costs one H2D, one D2H and no
+// allocation (calls are synchronous, so reuse after the stream sync is safe).
+struct Staging {
+    int device = -1;
+    uint8_t* host = nullptr;
+    uint8_t* dev = nullptr;
+    size_t bytes = 0;
+    cudaError_t reserve(int dev_id, size_t need) {
+        if (need <= bytes && device == dev_id) return cudaSuccess;
+        release();
+        size_t n = 1 << 16;
+        while (n < need) n <<= 1;
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&host), n);
+        if (e != cudaSuccess) return e;
+        e = cudaMalloc(reinterpret_cast<void**>(&dev), n);
+        if (e != cudaSuccess) {
+            cudaFreeHost(host);
+            host = nullptr;
+            return e;
+        }
+        bytes = n;
+        device = dev_id;
+        return cudaSuccess;
+    }
+    void release() {
+        if (host) cudaFreeHost(host);
+        if (dev) cudaFree(dev);
+        host = dev = nullptr;
+        bytes = 0;
+    }
+};
+
+Staging& thread_staging(int device) {
+    thread_local Staging st[8];
+    thread_local Staging other;
+    return (device >= 0 && device < 8) ? st[device] : other;
+}
+
+inline size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
+
 void ensure_pool(int device) {
     static std::once_flag flags[64];
     if (device < 0 || device >= 64) return;
@@ -873,30 +914,35 @@ SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const f
     ensure_pool(m->device);
     cudaStream_t st = thread_stream(m->device);
     const int nq = 2 * m->dof;
+    // staged layout: [points | q01] in, [min | argmin | free] out
+    const size_t o_q = align256(sizeof(float) * 3 * P), o_min = align256(o_q + sizeof(float) * nq * M);
+    const size_t o_arg = align256(o_min + sizeof(float) * M), o_free = align256(o_arg + sizeof(int32_t) * M);
+    const size_t total = align256(o_free + M);
+    Staging& sg = thread_staging(m->device);
+    SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
+    std::memcpy(sg.host, points, sizeof(float) * 3 * P);
+    std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
     svn_status s;
     {
         Scratch sc(st);
-        float *dp = nullptr, *dq = nullptr, *dmin = nullptr, *dpp = nullptr;
-        int32_t* darg = nullptr;
-        uint8_t* dfree = nullptr;
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * P), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * nq * M), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dmin), sizeof(float) * M), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&darg), sizeof(int32_t) * M), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dfree), M), "cudaMallocAsync");
+        float* dpp = nullptr;
         if (per_point)
             SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
-        SVN_CUDA(cudaMemcpyAsync(dp, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
-        SVN_CUDA(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions");
-        s = query_dense(m, prec, dp, P, 0, dq, M, margin, dmin, darg, dfree, dpp, nullptr, st);
+        SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
+        s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
+                        reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
+                        reinterpret_cast<float*>(sg.dev + o_min), reinterpret_cast<int32_t*>(sg.dev + o_arg),
+                        sg.dev + o_free, dpp, nullptr, st);
         if (s != SVN_OK) return s;
-        SVN_CUDA(cudaMemcpyAsync(min_out, dmin, sizeof(float) * M, cudaMemcpyDeviceToHost, st), "D2H min");
-        SVN_CUDA(cudaMemcpyAsync(argmin_out, darg, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st), "D2H argmin");
-        SVN_CUDA(cudaMemcpyAsync(free_out, dfree, M, cudaMemcpyDeviceToHost, st), "D2H free");
+        SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
+                 "D2H min/argmin/free");
         if (per_point)
             SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
     }
     SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+    std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
+    std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
+    std::memcpy(free_out, sg.host + o_free, M);
     return SVN_OK;
 }
 
