@@ -46,6 +46,11 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.is_file())
 
 
+def _defines() -> list[str]:
+    # e.g. SVN_NVCC_DEFINES="SVN_KERNEL_PROF SVN_PP_TIMELINE" for the instrumented kernels
+    return [f"-D{d}" for d in os.environ.get("SVN_NVCC_DEFINES", "").split() if d]
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
@@ -53,7 +58,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in sources():
         obj = LIBDIR / (src.stem + ".o")
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc(), *NVCC_FLAGS, *_defines(), "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)

@@ -75,6 +75,17 @@ struct FusedArgs {
     unsigned long long* prof;  // optional wait-time counters (clock64 cycles), see kProf*
 };
 
+// Wait/work accounting of the tensor-core kernels (scripts/profsum.py) costs ~1.3 % on c3, so
+// its clock reads are compiled in only with -DSVN_KERNEL_PROF (SVN_NVCC_DEFINES=SVN_KERNEL_PROF
+// python paper_2402_15281_b200/build.py); otherwise the counters stay zero.
+__device__ __forceinline__ unsigned long long prof_clock() {
+#ifdef SVN_KERNEL_PROF
+    return clock64();
+#else
+    return 0ull;
+#endif
+}
+
 // Instrumentation slots (summed over CTAs) when FusedArgs::prof is set.
 enum : int {
     kProfMmaWaitA = 0,   // MMA issuer waiting for epilogue (a_ready)

@@ -260,10 +260,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             uint32_t phase = 0;
             unsigned long long pw_e = 0;
             auto slot = [&](uint32_t bytes_one_cta) {
-                const unsigned long long c0 = clock64();
+                const unsigned long long c0 = prof_clock();
                 if (a.sleep_hint) mbar_wait_sleep(&empty[stage], phase ^ 1u, a.sleep_hint);
                 else mbar_wait(&empty[stage], phase ^ 1u);
-                pw_e += clock64() - c0;
+                pw_e += prof_clock() - c0;
                 if (rank == 0) mbar_arrive_expect_tx_local(&full[stage], 2 * bytes_one_cta);
             };
             auto advance = [&]() {
@@ -315,14 +315,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             uint32_t phase = 0;
             uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
             unsigned long long pw_a = 0, pw_f = 0, pw_x = 0;
-            const unsigned long long p_start = clock64();
+            const unsigned long long p_start = prof_clock();
             int64_t k = 0;  // local tile counter
             for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
                 const int b = static_cast<int>(k & 1);
                 {
-                    const unsigned long long c0 = clock64();
+                    const unsigned long long c0 = prof_clock();
                     mbar_wait(&ax_full[b], ax_ph[b]);
-                    pw_x += clock64() - c0;
+                    pw_x += prof_clock() - c0;
                 }
                 ax_ph[b] ^= 1u;
                 for (int l = 0; l < L; ++l) {
@@ -331,9 +331,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     for (int step = 0; step < steps; ++step) {
                         const int nh = step & 1, kh = step >> 1;
                         if (kh == 0 && (k > 0 || l > 0)) {  // D[nh] drained / A[k-half nh] written
-                            const unsigned long long c0 = clock64();
+                            const unsigned long long c0 = prof_clock();
                             mbar_wait(&a_ready[nh], ar_ph[nh]);
-                            pw_a += clock64() - c0;
+                            pw_a += prof_clock() - c0;
                             ar_ph[nh] ^= 1u;
                         }
                         tc_fence_after();
@@ -341,9 +341,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                         bool acc = false;
                         if (kh == 0 && ld.ext) {
                             {
-                                const unsigned long long c0 = clock64();
+                                const unsigned long long c0 = prof_clock();
                                 mbar_wait(&full[stage], phase);
-                                pw_f += clock64() - c0;
+                                pw_f += prof_clock() - c0;
                             }
                             tc_fence_after();
                             mma_bf16_pair(d_addr, noswz_desc(ax_base + b * C::AX_BYTES, 128, 256),
@@ -355,9 +355,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                         if (l > 0) {
                             for (int ks = 0; ks < C::KSL; ++ks) {
                                 {
-                                    const unsigned long long c0 = clock64();
+                                    const unsigned long long c0 = prof_clock();
                                     mbar_wait(&full[stage], phase);
-                                    pw_f += clock64() - c0;
+                                    pw_f += prof_clock() - c0;
                                 }
                                 tc_fence_after();
                                 const uint32_t a_slab = a_base + static_cast<uint32_t>(kh * C::KSL + ks) * C::A_SLAB;
@@ -380,7 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 atomicAdd(a.prof + kProfMmaWaitA, pw_a);
                 atomicAdd(a.prof + kProfMmaWaitFull, pw_f);
                 atomicAdd(a.prof + kProfMmaWaitAx, pw_x);
-                atomicAdd(a.prof + kProfMmaTotal, clock64() - p_start);
+                atomicAdd(a.prof + kProfMmaTotal, prof_clock() - p_start);
             }
         }
     } else if (warp < C::OUT_WARP) {
@@ -400,10 +400,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
                 for (int j = 0; j < 2; ++j) {
-                    const unsigned long long c0 = clock64();
+                    const unsigned long long c0 = prof_clock();
                     if (a.sleep_hint) mbar_wait_sleep(&d_full[j], dp[j], a.sleep_hint);
                     else mbar_wait(&d_full[j], dp[j]);
-                    const unsigned long long c1 = clock64();
+                    const unsigned long long c1 = prof_clock();
                     pe_d += c1 - c0;
                     dp[j] ^= 1u;
                     tc_fence_after();
@@ -424,17 +424,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                             if (q + 1 < NCH) tmem_wait_tied(nxt);
                         }
                     }
-                    const unsigned long long c2 = clock64();
+                    const unsigned long long c2 = prof_clock();
                     pe_w += c2 - c1;
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(a_ready0 + j * 8u);
-                    pe_a += clock64() - c2;
+                    pe_a += prof_clock() - c2;
                 }
             }
             // hand the row's partial dot to the output warp (dotbuf[parity] is reused two tiles later)
-            const unsigned long long c3 = clock64();
+            const unsigned long long c3 = prof_clock();
             const int b = static_cast<int>(k & 1);
             if (k >= 2) {
                 mbar_wait(&out_empty[b], oe_ph[b]);
@@ -443,7 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             dotbuf[(b * 2 + ch) * C::TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
-            pe_o += clock64() - c3;
+            pe_o += prof_clock() - c3;
         }
         if (a.prof && e == 0 && lane == 0 && rank == 0) {
             atomicAdd(a.prof + kProfEpiWaitD, pe_d);
@@ -501,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             if (a.sleep_hint) mbar_wait_sleep(&out_full[b], of_ph[b], a.sleep_hint);
             else mbar_wait(&out_full[b], of_ph[b]);
             of_ph[b] ^= 1u;
-            const unsigned long long c0 = clock64();
+            const unsigned long long c0 = prof_clock();
             // every MMA of tile t has completed, so AX[b] is free for tile t + 2 npairs
             if (next) store_ax(b);
             float delta[4];
@@ -537,7 +537,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     }
                 }
             }
-            pe_x += clock64() - c0;
+            pe_x += prof_clock() - c0;
         }
         if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
     }

@@ -306,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
             uint32_t wph = 0, xph = 0;
             uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
             unsigned long long pw_a = 0, pw_f = 0, pw_x = 0;
-            const unsigned long long p_start = clock64();
+            const unsigned long long p_start = prof_clock();
             for (int64_t j = 0; j < R; ++j) {
                 for (int l = 0; l < L; ++l) {
                     const LayerDev& ld = a.layer[l];
@@ -314,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                     const uint32_t wph_layer = wph;
                     const int nslots = has(j, 1) ? 2 : 1;
                     for (int s = 0; s < nslots; ++s) {
-                        const unsigned long long c0 = clock64();
+                        const unsigned long long c0 = prof_clock();
                         const bool tl = kTimeline && a.prof && blockIdx.x == 0 && j == R / 2 && l < 4;  // timeline sample
                         if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3] = c0;
                         mbar_wait(&a_ready[s], ar_ph[s]);  // D_s drained, A_s written
@@ -322,16 +322,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             mbar_wait(&ax_ready[s], ax_ph[s]);  // AX_s holds this tile's points
                             ax_ph[s] ^= 1u;
                         }
-                        pw_a += clock64() - c0;
-                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3 + 1] = clock64();
+                        pw_a += prof_clock() - c0;
+                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3 + 1] = prof_clock();
                         ar_ph[s] ^= 1u;
                         tc_fence_after();
                         const uint32_t d_addr = tmem + static_cast<uint32_t>(s * N);
                         bool acc = false;
                         if (ld.ext) {
-                            const unsigned long long c1 = clock64();
+                            const unsigned long long c1 = prof_clock();
                             mbar_wait(&xfull[xs], xph);
-                            pw_x += clock64() - c1;
+                            pw_x += prof_clock() - c1;
                             tc_fence_after();
                             mma_bf16_pair(d_addr, noswz_desc(ax_base + s * AX_BYTES, 128, 256),
                                           noswz_desc(x_base + xs * XCHUNK, 128, 256), idesc, 0u);
@@ -344,9 +344,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             uint32_t ph = wph_layer;
                             for (int ks = 0; ks < KSL; ++ks) {
                                 if (s == 0) {
-                                    const unsigned long long c2 = clock64();
+                                    const unsigned long long c2 = prof_clock();
                                     mbar_wait(&wfull[st], ph);
-                                    pw_f += clock64() - c2;
+                                    pw_f += prof_clock() - c2;
                                     tc_fence_after();
                                 }
                                 const uint32_t a_slab = a_base + s * A_BYTES + ks * A_SLAB;
@@ -360,7 +360,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             }
                         }
                         mma_commit_pair(&d_full[s], 3);
-                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3 + 2] = clock64();
+                        if (tl) a.prof[kProfTimeline + (l * 2 + s) * 3 + 2] = prof_clock();
                     }
                     if (l > 0)
                         for (int ks = 0; ks < KSL; ++ks)
@@ -371,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                 atomicAdd(a.prof + kProfMmaWaitA, pw_a);
                 atomicAdd(a.prof + kProfMmaWaitFull, pw_f);
                 atomicAdd(a.prof + kProfMmaWaitAx, pw_x);
-                atomicAdd(a.prof + kProfMmaTotal, clock64() - p_start);
+                atomicAdd(a.prof + kProfMmaTotal, prof_clock() - p_start);
             }
         }
     } else if (warp < OUT_WARP) {
@@ -397,9 +397,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                 const bool last = (l == L - 1);
                 for (int s = 0; s < nslots; ++s) {
                     uint8_t* A = Abuf + s * A_BYTES;
-                    const unsigned long long c0 = clock64();
+                    const unsigned long long c0 = prof_clock();
                     mbar_wait(&d_full[s], dp[s]);
-                    const unsigned long long c1 = clock64();
+                    const unsigned long long c1 = prof_clock();
                     pe_d += c1 - c0;
                     const bool tl = kTimeline && a.prof && blockIdx.x == 0 && e == 0 && lane == 0 && j == R / 2 && l < 4;
                     if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3] = c1;
@@ -421,14 +421,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             if (q + 1 < NCH) tmem_wait_tied(nxt);
                         }
                     }
-                    const unsigned long long c2 = clock64();
+                    const unsigned long long c2 = prof_clock();
                     pe_w += c2 - c1;
                     if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3 + 1] = c2;
                     tc_fence_before();
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
-                    const unsigned long long c3 = clock64();
+                    const unsigned long long c3 = prof_clock();
                     pe_a += c3 - c2;
                     if (tl) a.prof[kProfTimeline + 24 + (l * 2 + s) * 3 + 2] = c3;
                     if (last) {
@@ -442,7 +442,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&out_full[s]);
                     }
-                    pe_o += clock64() - c3;
+                    pe_o += prof_clock() - c3;
                 }
             }
         }
@@ -499,7 +499,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                 tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
                 mbar_wait(&out_full[s], of_ph[s]);
                 of_ph[s] ^= 1u;
-                const unsigned long long c0 = clock64();
+                const unsigned long long c0 = prof_clock();
                 // every MMA of tile (j, s) has completed, so AX_s is free for the next tile
                 if (next) store_ax(s);
                 float delta[4];
@@ -536,7 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                         }
                     }
                 }
-                pe_x += clock64() - c0;
+                pe_x += prof_clock() - c0;
             }
         }
         if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
