@@ -62,7 +62,6 @@ struct FusedArgs {
     const TileDesc* tiles;     // non-null: explicit tile table (forward_eval segments)
     int exact;                 // fp32 exact order (no q fold)
     int tile_rows;             // rows per work item the host cut the tiles with (SIMT: 128/64, or 32)
-    unsigned sleep_hint;       // bf16 kernel: try_wait suspend hint (ns) for idle-warp waits, 0 = poll
     // outputs
     unsigned long long* keys;  // [M] packed (orderable(delta) << 32 | index), or null
     unsigned int* counters;    // [M] tiles done, for the fused finaliser, or null

@@ -261,8 +261,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             unsigned long long pw_e = 0;
             auto slot = [&](uint32_t bytes_one_cta) {
                 const unsigned long long c0 = prof_clock();
-                if (a.sleep_hint) mbar_wait_sleep(&empty[stage], phase ^ 1u, a.sleep_hint);
-                else mbar_wait(&empty[stage], phase ^ 1u);
+                mbar_wait(&empty[stage], phase ^ 1u);
                 pw_e += prof_clock() - c0;
                 if (rank == 0) mbar_arrive_expect_tx_local(&full[stage], 2 * bytes_one_cta);
             };
@@ -401,8 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 const bool last = (l == L - 1);
                 for (int j = 0; j < 2; ++j) {
                     const unsigned long long c0 = prof_clock();
-                    if (a.sleep_hint) mbar_wait_sleep(&d_full[j], dp[j], a.sleep_hint);
-                    else mbar_wait(&d_full[j], dp[j]);
+                    mbar_wait(&d_full[j], dp[j]);
                     const unsigned long long c1 = prof_clock();
                     pe_d += c1 - c0;
                     dp[j] ^= 1u;
@@ -498,8 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
-            if (a.sleep_hint) mbar_wait_sleep(&out_full[b], of_ph[b], a.sleep_hint);
-            else mbar_wait(&out_full[b], of_ph[b]);
+            mbar_wait(&out_full[b], of_ph[b]);
             of_ph[b] ^= 1u;
             const unsigned long long c0 = prof_clock();
             // every MMA of tile t has completed, so AX[b] is free for tile t + 2 npairs

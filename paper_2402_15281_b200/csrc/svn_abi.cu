@@ -708,13 +708,6 @@ cudaError_t launch_k1(const FusedArgs& a, Kind kind, int num_sms, cudaStream_t s
     }
     unsigned long long* dprof = nullptr;
     FusedArgs ap = a;
-    {
-        static const unsigned hint = [] {
-            const char* e = std::getenv("SVN_SLEEP_NS");
-            return e ? static_cast<unsigned>(std::atoi(e)) : 0u;
-        }();
-        ap.sleep_hint = hint;
-    }
     if (prof_enabled()) {
         cudaMalloc(&dprof, sizeof(unsigned long long) * kProfSlots);
         cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * kProfSlots, st);
