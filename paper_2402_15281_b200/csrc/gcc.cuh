@@ -32,6 +32,11 @@ struct GccArgs {
     int64_t chunks;            // point chunks per motion
     int64_t points_per_chunk;
     unsigned long long* keys;  // [M] orderable-u64 minima
+    // gcc_clearance mode (collision.cpp:26-34): stop a motion as soon as some point is within
+    // the margin (its distance is then a partial minimum <= margin; free motions scan fully)
+    int early_exit;
+    double margin;
+    unsigned int* hit;  // [M] set once a point within the margin is found
 };
 
 size_t gcc_smem_bytes(int steps, int ncap);

@@ -88,8 +88,16 @@ __global__ void __launch_bounds__(256) gcc_kernel(const __grid_constant__ GccArg
     const int ncap = a.ncap, steps = a.steps;
     double* pc = sm;                                          // [steps][ncap][8]: a, b, r | later a, ba, r, 1/|ba|^2
     double* bounds = sm + static_cast<size_t>(steps) * ncap * 8;  // [steps][4]
-    const int64_t m = blockIdx.x / a.chunks;
-    const int64_t chunk = blockIdx.x % a.chunks;
+    // chunk-major order: the first waves cover the first chunk of every motion, so in
+    // early-exit mode a colliding motion is usually flagged before its later chunks start
+    const int64_t m = blockIdx.x % a.M;
+    const int64_t chunk = blockIdx.x / a.M;
+    if (a.early_exit) {
+        __shared__ unsigned int skip;
+        if (threadIdx.x == 0) skip = *reinterpret_cast<volatile unsigned int*>(a.hit + m);
+        __syncthreads();
+        if (skip) return;
+    }
     const double* q0 = a.q01 + m * 2 * a.dof;
     const double* q1 = q0 + a.dof;
 
@@ -184,6 +192,10 @@ __global__ void __launch_bounds__(256) gcc_kernel(const __grid_constant__ GccArg
             }
         }
         best = bp < best ? bp : best;
+        if (a.early_exit && bp <= a.margin) {  // not free: stop this motion everywhere
+            *reinterpret_cast<volatile unsigned int*>(a.hit + m) = 1u;
+            break;
+        }
     }
     // block min -> one atomic per CTA
     unsigned long long key = orderable64(best);

@@ -1158,15 +1158,16 @@ static svn_status gcc_args(const svn_robot_desc* r, int32_t steps, GccArgs& a) {
     return SVN_OK;
 }
 
-SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, const double* points, int64_t P,
-                                               const double* q01, int64_t M, int32_t steps, double margin,
-                                               double* dist_out, uint8_t* free_out, void* stream) {
+// The checker on device buffers; early_exit = gcc_clearance semantics (a motion stops as soon
+// as one point is within the margin; its distance is then a partial minimum <= margin).
+static svn_status gcc_run(const svn_robot_desc* robot, const double* points, int64_t P, const double* q01, int64_t M,
+                          int32_t steps, double margin, bool early_exit, double* dist_out, uint8_t* free_out,
+                          cudaStream_t st) {
     if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_min_distance: empty point cloud");
     if (M < 1) return SVN_OK;
     GccArgs a;
     svn_status s = gcc_args(robot, steps, a);
     if (s != SVN_OK) return s;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
     Scratch sc(st);
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&a.keys), sizeof(unsigned long long) * M), "cudaMallocAsync");
     a.points = points;
@@ -1175,14 +1176,21 @@ SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, cons
     a.M = M;
     a.points_per_chunk = 2048;  // 512..32768 measured within 4 % at c3 size: the scan dominates
     a.chunks = (P + a.points_per_chunk - 1) / a.points_per_chunk;
+    a.early_exit = early_exit ? 1 : 0;
+    a.margin = margin;
+    if (early_exit) {
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&a.hit), sizeof(unsigned int) * M), "cudaMallocAsync");
+        SVN_CUDA(cudaMemsetAsync(a.hit, 0, sizeof(unsigned int) * M, st), "memset hit");
+    }
     SVN_CUDA(launch_gcc(a, margin, dist_out, free_out, st), "gcc kernel");
     g_launches += 3;
     return SVN_OK;
 }
 
-SVN_API svn_status svn_gcc_min_distance(const svn_robot_desc* robot, const double* points, int64_t P,
-                                        const double* q01, int64_t M, int32_t steps, double margin, int32_t device,
-                                        double* dist_out, uint8_t* free_out) {
+// Host buffers in and out, on the calling thread's stream.
+static svn_status gcc_host(const svn_robot_desc* robot, const double* points, int64_t P, const double* q01, int64_t M,
+                           int32_t steps, double margin, bool early_exit, int32_t device, double* dist_out,
+                           uint8_t* free_out) {
     if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_min_distance: empty point cloud");
     if (M < 1) return SVN_OK;
     if (!robot || !points || !q01 || !dist_out || !free_out)
@@ -1201,13 +1209,26 @@ SVN_API svn_status svn_gcc_min_distance(const svn_robot_desc* robot, const doubl
         SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&df), M), "cudaMallocAsync");
         SVN_CUDA(cudaMemcpyAsync(dp, points, sizeof(double) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
         SVN_CUDA(cudaMemcpyAsync(dq, q01, sizeof(double) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions");
-        svn_status s = svn_gcc_min_distance_device(robot, dp, P, dq, M, steps, margin, dd, df, st);
+        svn_status s = gcc_run(robot, dp, P, dq, M, steps, margin, early_exit, dd, df, st);
         if (s != SVN_OK) return s;
         SVN_CUDA(cudaMemcpyAsync(dist_out, dd, sizeof(double) * M, cudaMemcpyDeviceToHost, st), "D2H dist");
         SVN_CUDA(cudaMemcpyAsync(free_out, df, M, cudaMemcpyDeviceToHost, st), "D2H free");
     }
     SVN_CUDA(cudaStreamSynchronize(st), "gcc");
     return SVN_OK;
+}
+
+SVN_API svn_status svn_gcc_min_distance_device(const svn_robot_desc* robot, const double* points, int64_t P,
+                                               const double* q01, int64_t M, int32_t steps, double margin,
+                                               double* dist_out, uint8_t* free_out, void* stream) {
+    return gcc_run(robot, points, P, q01, M, steps, margin, false, dist_out, free_out,
+                   static_cast<cudaStream_t>(stream));
+}
+
+SVN_API svn_status svn_gcc_min_distance(const svn_robot_desc* robot, const double* points, int64_t P,
+                                        const double* q01, int64_t M, int32_t steps, double margin, int32_t device,
+                                        double* dist_out, uint8_t* free_out) {
+    return gcc_host(robot, points, P, q01, M, steps, margin, false, device, dist_out, free_out);
 }
 
 // Alg. 1 (collision.cpp:55-107) with both callables on the GPU; see the header.
@@ -1262,7 +1283,8 @@ SVN_API svn_status svn_gcc_nn_search(const svn_model* m, svn_precision prec, con
         const int64_t nb = std::min<int64_t>(B, M - pos);
         for (int64_t i = 0; i < nb; ++i)
             std::memcpy(qb.data() + i * nq, q01 + order[static_cast<size_t>(pos + i)] * nq, sizeof(double) * nq);
-        s = svn_gcc_min_distance(robot, cloud, P, qb.data(), nb, steps, margin, m->device, db.data(), fb.data());
+        // gcc_clearance semantics: a colliding motion stops at its first point within the margin
+        s = gcc_host(robot, cloud, P, qb.data(), nb, steps, margin, true, m->device, db.data(), fb.data());
         if (s != SVN_OK) return s;
         for (int64_t i = 0; i < nb; ++i) {
             if (!fb[static_cast<size_t>(i)]) continue;
