@@ -673,10 +673,17 @@ struct Staging {
     }
     void release() {
         if (host) cudaFreeHost(host);
-        if (dev) cudaFree(dev);
+        if (dev) {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(device);
+            cudaFree(dev);
+            cudaSetDevice(prev);
+        }
         host = dev = nullptr;
         bytes = 0;
     }
+    ~Staging() { release(); }  // thread exit (worker threads come and go)
 };
 
 Staging& thread_staging(int device) {
@@ -852,11 +859,27 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     return SVN_OK;
 }
 
+// One non-blocking stream per (thread, device), destroyed when the thread exits (callers such
+// as the reference's parallel_for workers come and go).
+struct ThreadStreams {
+    cudaStream_t s[64] = {};
+    ~ThreadStreams() {
+        for (int d = 0; d < 64; ++d)
+            if (s[d]) {
+                int prev = 0;
+                cudaGetDevice(&prev);
+                cudaSetDevice(d);
+                cudaStreamDestroy(s[d]);
+                cudaSetDevice(prev);
+            }
+    }
+};
+
 cudaStream_t thread_stream(int device) {
-    thread_local cudaStream_t streams[64] = {};
+    thread_local ThreadStreams ts;
     if (device < 0 || device >= 64) return nullptr;
-    if (!streams[device]) cudaStreamCreateWithFlags(&streams[device], cudaStreamNonBlocking);
-    return streams[device];
+    if (!ts.s[device]) cudaStreamCreateWithFlags(&ts.s[device], cudaStreamNonBlocking);
+    return ts.s[device];
 }
 
 }  // namespace

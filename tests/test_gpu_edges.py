@@ -248,3 +248,23 @@ np.save(sys.argv[1], np.concatenate([m.forward_eval(raw, precision=pr) for pr in
         subprocess.run([sys.executable, "-c", code.replace("{root}", root), f], check=True, env=env)
         res.append(np.load(f))
     assert np.array_equal(res[0], res[1])
+
+
+def test_many_short_lived_host_threads():
+    """Each host thread gets its own stream and staging buffers; they are released when the
+    thread exits, so threads that come and go (a parallel_for pool) do not accumulate them."""
+    import torch
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 4, w.bound)
+    model = S.Model(w.program, params)
+    pts, q = w.make(seed=4, motions=1, points=3000)
+    ref = model.query_min(pts, q, w.margin, precision="bf16")
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(40):
+        out = []
+        t = threading.Thread(target=lambda: out.append(model.query_min(pts, q, w.margin, precision="bf16")))
+        t.start()
+        t.join()
+        assert np.array_equal(out[0].min, ref.min)
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20  # no per-thread growth
