@@ -168,6 +168,7 @@ def run_cpu(w, params, seed, threads, lib, steps, warmup, seconds=10.0):
         if i >= warmup:
             times.append(dt)
     sec = statistics.median(times)
+    run_cpu.last_ms = sec * 1e3
     return M * P / sec, f"{M} motions x {P} points of {w.key} ({M * P} queries), {len(times)} runs, median"
 
 
@@ -194,7 +195,8 @@ def main():
         per_step = max(2.0, min(10.0, 120.0 / (steps + warm)))  # whole arm within ~2 minutes
         val, sample = run_cpu(w, params, args.seed, threads, lib, steps, warm, per_step)
         line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": getattr(run_cpu, "last_ms", None),
+                "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
                 "config": {"workload": w.key, "description": w.description, "network": w.program.name},
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
