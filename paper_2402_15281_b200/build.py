@@ -55,16 +55,27 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     LIBDIR.mkdir(parents=True, exist_ok=True)
+    # several processes may import the package at once (torchrun ranks): one builds under an
+    # exclusive lock, the others wait and then find the library fresh
+    import fcntl
+    with open(LIBDIR / ".build.lock", "w") as lock:
+        fcntl.flock(lock, fcntl.LOCK_EX)
+        if not force and not _stale():
+            return LIB
+        return _build_locked(verbose)
+
+
+def _build_locked(verbose: bool) -> Path:
     objs = []
     for src in sources():
-        obj = LIBDIR / (src.stem + ".o")
+        obj = LIBDIR / f"{src.stem}.{os.getpid()}.o"
         cmd = [nvcc(), *NVCC_FLAGS, *_defines(), "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = LIB.with_suffix(f".so.{os.getpid()}.tmp")
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
            "-o", str(tmp), *objs, "-lpthread", "-ldl", "-lrt"]
     if verbose:
