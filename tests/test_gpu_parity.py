@@ -262,3 +262,26 @@ def test_fig2_bf16_affine_fold_with_trained_like_bn(width, blocks, neg):
     err = np.abs(r.per_point.astype(np.float64) - opp).max()
     assert err <= BF16_BOUND[prog.name], err
     assert np.array_equal(r.min, r.per_point.min(axis=1))
+
+
+def test_trained_like_checkpoint_through_the_loader(tmp_path):
+    """A Fig. 2 checkpoint with non-trivial BN statistics (as training leaves them) through
+    svn_model_load_checkpoint: FP32 path bit-identical to the oracle, bf16 (affine folded) within
+    the frozen bound, and both identical to the model built from the same parameters in memory."""
+    import struct
+    from fig2_bn import randomize_bn
+    prog = S.fig2(5, 512, 6)
+    params = randomize_bn(prog, S.init_params(prog, 33, "ref"), 33, negative_gamma_layer=3)
+    path = tmp_path / "trained.ckpt"
+    with open(path, "wb") as f:
+        f.write(b"SVCKPT01")
+        f.write(struct.pack("<4I", 1, 5, 512, 15))
+        f.write(params.astype("<f4").tobytes())
+    loaded, direct = S.Model.from_checkpoint(str(path)), S.Model(prog, params)
+    pts, q = WORKLOADS["c2"].make(seed=33, motions=3, points=900)
+    _, _, _, opp = _oracle(prog, params, pts, q, 0.0)
+    for prec, tol in (("fp32", 0.0), ("bf16", BF16_BOUND["fig2_5x512"])):
+        a = loaded.query_min(pts, q, 0.0, precision=prec, per_point=True)
+        b = direct.query_min(pts, q, 0.0, precision=prec, per_point=True)
+        assert np.array_equal(a.per_point, b.per_point)
+        assert np.abs(a.per_point.astype(np.float64) - opp).max() <= tol
