@@ -24,6 +24,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges for Nsight tools, no-ops otherwise
+
 #include "../../include/sweptnet_b200.h"
 #include "fused.cuh"
 #include "gcc.cuh"
@@ -631,6 +633,12 @@ int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
     return (k == Kind::SIMT && big_tiles < num_sms) ? kFp32SmallTile : t;
 }
 
+// NVTX range for the duration of a scope (names the entry points and kernels in Nsight).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 // Scratch buffers freed on the stream when the call's kernels are done.
 struct Scratch {
     cudaStream_t st;
@@ -767,6 +775,7 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
 svn_status query_dense(const svn_model* m, svn_precision prec, const float* points, int64_t P, int64_t index_offset,
                        const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
                        uint8_t* free_out, float* per_point, uint64_t* keys_partial, cudaStream_t st) {
+    NvtxRange nvtx("svn query (K0 + fused K1)");
     if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
     if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
     if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
@@ -966,6 +975,7 @@ SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const f
 // motion segment; each segment is cut into tiles of one motion.
 static svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw_host, const float* raw_dev,
                                int64_t B, int64_t cols, float* out_dev, cudaStream_t st) {
+    NvtxRange nvtx("svn forward_eval rows");
     if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
     if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
     if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
@@ -1186,6 +1196,7 @@ static svn_status gcc_args(const svn_robot_desc* r, int32_t steps, GccArgs& a) {
 static svn_status gcc_run(const svn_robot_desc* robot, const double* points, int64_t P, const double* q01, int64_t M,
                           int32_t steps, double margin, bool early_exit, double* dist_out, uint8_t* free_out,
                           cudaStream_t st) {
+    NvtxRange nvtx(early_exit ? "svn gcc (clearance)" : "svn gcc (min distance)");
     if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_min_distance: empty point cloud");
     if (M < 1) return SVN_OK;
     GccArgs a;
@@ -1258,6 +1269,7 @@ SVN_API svn_status svn_gcc_min_distance(const svn_robot_desc* robot, const doubl
 SVN_API svn_status svn_gcc_nn_search(const svn_model* m, svn_precision prec, const svn_robot_desc* robot,
                                      const double* cloud, int64_t P, const double* q01, int64_t M, int32_t steps,
                                      double margin, int32_t batch, svn_search_result* out) {
+    NvtxRange nvtx("svn gcc_nn_search (Alg. 1)");
     using clk = std::chrono::steady_clock;
     auto secs = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double>(b - a).count(); };
     if (!m || !robot || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "gcc_nn_search: null argument");
