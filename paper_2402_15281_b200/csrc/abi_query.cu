@@ -1,0 +1,516 @@
+// abi_query.cu — C-ABI: kernel selection and sequencing (K0 -> fused K1), dense queries
+// (device and host buffers), forward_eval rows of mixed motions, predict_min_distance,
+// dense-grid evaluation; scratch, staging and per-thread streams.
+#include "abi_internal.cuh"
+
+using namespace svn;
+using namespace svn::abi;
+
+namespace svn {
+namespace abi {
+
+svn_status check_prec(const svn_model* m, svn_precision prec) {
+    if (prec == SVN_PREC_BF16) {
+        if (!m->has_bf16) return fail(SVN_ERR_UNSUPPORTED, "bf16 path needs width 256 or 512");
+    } else if (prec == SVN_PREC_FP32 || prec == SVN_PREC_FP32_EXACT) {
+        if (m->N != 128 && m->N != 256 && m->N != 512)
+            return fail(SVN_ERR_UNSUPPORTED, "fp32 path needs width 128, 256 or 512");
+    } else if (prec == SVN_PREC_FP32_SPLIT) {
+        if (!m->has_split)
+            return fail(SVN_ERR_UNSUPPORTED, "fp32_split path needs width 256, >= 2 layers and |W| < 1e4");
+    } else {
+        return fail(SVN_ERR_INVALID_ARGUMENT, "unknown precision");
+    }
+    return SVN_OK;
+}
+
+// Which fused kernel serves a (model, precision): bf16 tensor cores; fp32-grade split-fp16
+// tensor cores (fp32_split, width 256); or SIMT FFMA in the oracle's order (fp32, fp32_exact).
+Kind kernel_kind(const svn_model*, svn_precision prec) {
+    if (prec == SVN_PREC_BF16) return Kind::BF16;
+    if (prec == SVN_PREC_FP32_SPLIT) return Kind::SPLIT;
+    return Kind::SIMT;
+}
+
+int tile_rows(Kind k, int N) { return k == Kind::SIMT ? (N >= 512 ? 64 : 128) : 256; }
+// SIMT: a query with fewer big tiles than SMs is cut into 32-row tiles (4 warps per CTA,
+// more SMs busy; each output's k-ordered FMA chain is unchanged)
+int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
+    const int t = tile_rows(k, N);
+    return (k == Kind::SIMT && big_tiles < num_sms) ? kFp32SmallTile : t;
+}
+
+
+
+
+Staging& thread_staging(int device) {
+    thread_local Staging st[8];
+    thread_local Staging other;
+    return (device >= 0 && device < 8) ? st[device] : other;
+}
+
+
+void ensure_pool(int device) {
+    static std::once_flag flags[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(flags[device], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t threshold = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+        }
+    });
+}
+
+cudaError_t launch_k1(const FusedArgs& a, Kind kind, int num_sms, cudaStream_t st) {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g_timing) {
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+    }
+    unsigned long long* dprof = nullptr;
+    FusedArgs ap = a;
+    if (prof_enabled()) {
+        cudaMalloc(&dprof, sizeof(unsigned long long) * kProfSlots);
+        cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * kProfSlots, st);
+        ap.prof = dprof;
+    }
+    cudaError_t e = kind == Kind::BF16    ? launch_fused_bf16_pair(ap, num_sms, st)
+                    : kind == Kind::SPLIT ? launch_fused_split(ap, num_sms, st)
+                                          : launch_fused_fp32(ap, num_sms, st);
+    ++g_launches;
+    if (dprof) {
+        cudaMemcpyAsync(g_prof, dprof, sizeof(g_prof), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        cudaFree(dprof);
+        std::fprintf(stderr, "[svn prof]");
+        for (int i = 0; i < kProfSlots; ++i) std::fprintf(stderr, " %llu", g_prof[i]);
+        std::fprintf(stderr, "\n");
+    }
+    if (g_timing) {
+        cudaEventRecord(e1, st);
+        g_events.emplace_back(e0, e1);
+    }
+    return e;
+}
+
+// bf16: per-motion K=16 extension rows (folded bias + x-part splits) and their TMA view.
+svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long long* keys, unsigned int* counters,
+                      int64_t n_keys, Scratch& sc, cudaStream_t st, bool split) {
+    uint8_t* ext = nullptr;
+    if (split) {  // [motion][slot][n-half][CTA half][main 64 rows | corr 64 rows] x 32 B
+        const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * 2 * m->N;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(split ext)");
+        svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, 128);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(launch_split_ext(a, m->d_wq, m->d_mbbase, m->d_wxslots, ext, keys, counters, n_keys, st),
+                 "split_ext kernel");
+        ++g_launches;
+        return SVN_OK;
+    }
+    const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * m->N;
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
+    svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N == 256 ? m->N / 2 : m->N / 4));
+    if (s != SVN_OK) return s;
+    SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, ext, keys, counters, n_keys, st),
+             "motion_ext kernel");
+    ++g_launches;
+    return SVN_OK;
+}
+
+// Shared body of the dense query (full result or keys-only partial).
+svn_status query_dense(const svn_model* m, svn_precision prec, const float* points, int64_t P, int64_t index_offset,
+                       const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
+                       uint8_t* free_out, float* per_point, uint64_t* keys_partial, cudaStream_t st) {
+    NvtxRange nvtx("svn query (K0 + fused K1)");
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    {
+        // TMA row coordinates of the per-motion extension stream are int32: beyond ~1e9 rows
+        // (about a million motions at width 512) the query runs as consecutive motion chunks
+        static const int64_t override_max = [] {
+            const char* e = std::getenv("SVN_MAX_MOTIONS_PER_LAUNCH");  // test hook
+            return e ? std::atoll(e) : 0ll;
+        }();
+        const int64_t rows_per_motion = static_cast<int64_t>(m->n_mb ? m->n_mb : 1) * m->N * 2;
+        int64_t max_m = (static_cast<int64_t>(INT32_MAX) / 2) / rows_per_motion;
+        if (override_max > 0) max_m = override_max;
+        if (max_m < 1) max_m = 1;
+        if (M > max_m) {
+            const int64_t nq = 2 * static_cast<int64_t>(m->dof);
+            for (int64_t b0 = 0; b0 < M; b0 += max_m) {
+                const int64_t n = std::min(max_m, M - b0);
+                const svn_status s = query_dense(m, prec, points, P, index_offset, q01 + b0 * nq, n, margin,
+                                                 min_out ? min_out + b0 : nullptr, argmin_out ? argmin_out + b0 : nullptr,
+                                                 free_out ? free_out + b0 : nullptr,
+                                                 per_point ? per_point + b0 * P : nullptr,
+                                                 keys_partial ? keys_partial + b0 : nullptr, st);
+                if (s != SVN_OK) return s;
+            }
+            return SVN_OK;
+        }
+    }
+    if (P + index_offset > 0xFFFFFFFFll) return fail(SVN_ERR_UNSUPPORTED, "query: more than 2^32 points");
+    svn_status s = check_prec(m, prec);
+    if (s != SVN_OK) return s;
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    const Kind kind0 = kernel_kind(m, prec);
+    FusedArgs a = kind0 == Kind::SPLIT ? m->base_split : kind0 == Kind::BF16 ? m->base_bf16 : m->base;
+    // fp32 on the SIMT kernel runs in the oracle's order (no q-fold): at width 512 that costs
+    // nothing measurable (c3/c4: 12.0/16.8 M q/s either way) and makes it bit-identical
+    const bool exact = kind0 == Kind::SIMT;
+    a.exact = exact ? 1 : 0;
+    a.points = points;
+    a.point_stride = 3;
+    a.P = P;
+    a.q01 = q01;
+    a.M = M;
+    const Kind kind = kernel_kind(m, prec);
+    const int TM0 = tile_rows(kind, m->N);
+    const int TM = tile_rows_for(kind, m->N, M * ((P + TM0 - 1) / TM0), m->num_sms);
+    a.tile_rows = TM;
+    a.tiles_per_motion = (P + TM - 1) / TM;
+    a.n_tiles = a.tiles_per_motion * M;
+    a.tiles = nullptr;
+    a.margin = margin;
+    a.per_point = per_point;
+    a.index_offset = index_offset;
+    Scratch sc(st);
+    float* mb = nullptr;
+    const int n_mb = exact ? 0 : m->n_mb;
+    if (kind == Kind::SIMT)
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb),
+                          sizeof(float) * static_cast<size_t>(M) * (n_mb ? n_mb : 1) * m->N),
+                 "cudaMallocAsync(motion_bias)");
+    a.motion_bias = mb;
+    a.n_mb = m->n_mb;  // slot stride stays the model's (exact mode never reads it)
+    unsigned long long* keys = nullptr;
+    unsigned int* counters = nullptr;
+    if (keys_partial) {
+        keys = reinterpret_cast<unsigned long long*>(keys_partial);
+    } else {
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&keys), sizeof(unsigned long long) * M), "cudaMallocAsync(keys)");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&counters), sizeof(unsigned int) * M), "cudaMallocAsync(counters)");
+    }
+    a.keys = keys;
+    a.counters = counters;
+    a.min_out = min_out;
+    a.argmin_out = argmin_out;
+    a.free_out = free_out;
+    if (kind != Kind::SIMT) {
+        s = motion_ext(m, a, M, keys_partial ? nullptr : keys, counters, keys_partial ? 0 : M, sc, st,
+                       kind == Kind::SPLIT);
+        if (s != SVN_OK) return s;
+    } else {
+        FusedArgs k0 = a;
+        k0.n_mb = n_mb;
+        SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, keys_partial ? nullptr : keys, counters,
+                                    keys_partial ? 0 : M, st),
+                 "motion_bias kernel");
+        ++g_launches;
+    }
+    SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
+    return SVN_OK;
+}
+
+// One non-blocking stream per (thread, device), destroyed when the thread exits (callers such
+// as the reference's parallel_for workers come and go).
+struct ThreadStreams {
+    cudaStream_t s[64] = {};
+    ~ThreadStreams() {
+        for (int d = 0; d < 64; ++d)
+            if (s[d]) {
+                int prev = 0;
+                cudaGetDevice(&prev);
+                cudaSetDevice(d);
+                cudaStreamDestroy(s[d]);
+                cudaSetDevice(prev);
+            }
+    }
+};
+
+cudaStream_t thread_stream(int device) {
+    thread_local ThreadStreams ts;
+    if (device < 0 || device >= 64) return nullptr;
+    if (!ts.s[device]) cudaStreamCreateWithFlags(&ts.s[device], cudaStreamNonBlocking);
+    return ts.s[device];
+}
+
+}  // namespace abi
+}  // namespace svn
+
+namespace svn {
+namespace abi {
+
+// forward_eval (nn.cpp:95-130).  Consecutive rows with identical (q0, q1) form one
+// motion segment; each segment is cut into tiles of one motion.
+svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw_host, const float* raw_dev,
+                               int64_t B, int64_t cols, float* out_dev, cudaStream_t st) {
+    NvtxRange nvtx("svn forward_eval rows");
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+    svn_status s = check_prec(m, prec);
+    if (s != SVN_OK) return s;
+    {
+        // every row can be its own motion: keep the per-motion extension stream inside the
+        // int32 TMA row range by running large batches as row chunks (rows are independent)
+        static const int64_t override_max = [] {
+            const char* e = std::getenv("SVN_MAX_MOTIONS_PER_LAUNCH");  // test hook
+            return e ? std::atoll(e) : 0ll;
+        }();
+        const int64_t rows_per_motion = static_cast<int64_t>(m->n_mb ? m->n_mb : 1) * m->N * 2;
+        int64_t max_b = (static_cast<int64_t>(INT32_MAX) / 2) / rows_per_motion;
+        if (override_max > 0) max_b = override_max;
+        if (max_b < 1) max_b = 1;
+        if (B > max_b) {
+            for (int64_t b0 = 0; b0 < B; b0 += max_b) {
+                const int64_t n = std::min(max_b, B - b0);
+                s = forward_rows(m, prec, raw_host + b0 * cols, raw_dev + b0 * cols, n, cols, out_dev + b0, st);
+                if (s != SVN_OK) return s;
+            }
+            return SVN_OK;
+        }
+    }
+    const Kind kind = kernel_kind(m, prec);
+    const int TM0 = tile_rows(kind, m->N);
+    const int nq = 2 * m->dof, TM = tile_rows_for(kind, m->N, (B + TM0 - 1) / TM0, m->num_sms);
+    std::vector<float> qseg;
+    std::vector<TileDesc> tiles;
+    int64_t seg_start = 0;
+    int32_t nseg = 0;
+    for (int64_t r = 1; r <= B; ++r) {
+        const bool cut = (r == B) || std::memcmp(raw_host + r * cols + 3, raw_host + (r - 1) * cols + 3,
+                                                 sizeof(float) * nq) != 0;
+        if (!cut) continue;
+        qseg.insert(qseg.end(), raw_host + seg_start * cols + 3, raw_host + seg_start * cols + 3 + nq);
+        for (int64_t t0 = seg_start; t0 < r; t0 += TM) {
+            const int64_t n = (r - t0) < TM ? (r - t0) : TM;
+            tiles.push_back(TileDesc{t0, t0, nseg, static_cast<int32_t>(n)});
+        }
+        ++nseg;
+        seg_start = r;
+    }
+    FusedArgs a = kind == Kind::SPLIT ? m->base_split : kind == Kind::BF16 ? m->base_bf16 : m->base;
+    a.exact = kind == Kind::SIMT ? 1 : 0;
+    a.points = raw_dev;
+    a.point_stride = cols;
+    a.P = B;
+    a.M = nseg;
+    a.n_tiles = static_cast<int64_t>(tiles.size());
+    a.tile_rows = TM;
+    a.tiles_per_motion = 1;
+    a.per_point = out_dev;
+    a.keys = nullptr;
+    a.counters = nullptr;
+    Scratch sc(st);
+    float *dq = nullptr, *mb = nullptr;
+    TileDesc* dt = nullptr;
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * qseg.size()), "cudaMallocAsync");
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dt), sizeof(TileDesc) * tiles.size()), "cudaMallocAsync");
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&mb), sizeof(float) * static_cast<size_t>(nseg) * (m->n_mb ? m->n_mb : 1) * m->N),
+             "cudaMallocAsync");
+    SVN_CUDA(cudaMemcpyAsync(dq, qseg.data(), sizeof(float) * qseg.size(), cudaMemcpyHostToDevice, st), "H2D q");
+    SVN_CUDA(cudaMemcpyAsync(dt, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice, st), "H2D tiles");
+    a.q01 = dq;
+    a.tiles = dt;
+    a.motion_bias = mb;
+    if (kind != Kind::SIMT) {
+        s = motion_ext(m, a, nseg, nullptr, nullptr, 0, sc, st, kind == Kind::SPLIT);
+        if (s != SVN_OK) return s;
+    } else {
+        FusedArgs k0 = a;
+        k0.n_mb = a.exact ? 0 : m->n_mb;
+        SVN_CUDA(launch_motion_bias(k0, m->d_wq, m->d_mbbase, mb, nullptr, nullptr, 0, st), "motion_bias kernel");
+        ++g_launches;
+    }
+    SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
+    // keep the host tile/q vectors alive until the async copies have consumed them
+    SVN_CUDA(cudaStreamSynchronize(st), "forward kernels");
+    return SVN_OK;
+}
+
+}  // namespace abi
+}  // namespace svn
+
+extern "C" {
+
+SVN_API svn_status svn_query_min_device(const svn_model* m, svn_precision prec, const float* points, int64_t P,
+                                        const float* q01, int64_t M, double margin, float* min_out,
+                                        int32_t* argmin_out, uint8_t* free_out, float* per_point, void* stream) {
+    if (!min_out || !argmin_out || !free_out) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null output");
+    return query_dense(m, prec, points, P, 0, q01, M, margin, min_out, argmin_out, free_out, per_point, nullptr,
+                       static_cast<cudaStream_t>(stream));
+}
+
+SVN_API svn_status svn_keys_init_device(uint64_t* keys, int64_t M, void* stream) {
+    SVN_CUDA(launch_keys_init(reinterpret_cast<unsigned long long*>(keys), M, static_cast<cudaStream_t>(stream)),
+             "keys_init kernel");
+    ++g_launches;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_query_min_keys_device(const svn_model* m, svn_precision prec, const float* points, int64_t P,
+                                             int64_t index_offset, const float* q01, int64_t M, uint64_t* keys,
+                                             void* stream) {
+    if (!keys) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null keys");
+    return query_dense(m, prec, points, P, index_offset, q01, M, 0.0, nullptr, nullptr, nullptr, nullptr, keys,
+                       static_cast<cudaStream_t>(stream));
+}
+
+SVN_API svn_status svn_keys_finalize_device(const uint64_t* keys, int64_t M, double margin, float* min_out,
+                                            int32_t* argmin_out, uint8_t* free_out, void* stream) {
+    SVN_CUDA(launch_keys_finalize(reinterpret_cast<const unsigned long long*>(keys), M, margin, min_out, argmin_out,
+                                  free_out, static_cast<cudaStream_t>(stream)),
+             "keys_finalize kernel");
+    ++g_launches;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const float* points, int64_t P,
+                                 const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
+                                 uint8_t* free_out, float* per_point) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    if (!points || !q01 || !min_out || !argmin_out || !free_out)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    const int nq = 2 * m->dof;
+    // staged layout: [points | q01] in, [min | argmin | free] out
+    const size_t o_q = align256(sizeof(float) * 3 * P), o_min = align256(o_q + sizeof(float) * nq * M);
+    const size_t o_arg = align256(o_min + sizeof(float) * M), o_free = align256(o_arg + sizeof(int32_t) * M);
+    const size_t total = align256(o_free + M);
+    Staging& sg = thread_staging(m->device);
+    SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
+    std::memcpy(sg.host, points, sizeof(float) * 3 * P);
+    std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
+    svn_status s;
+    {
+        Scratch sc(st);
+        float* dpp = nullptr;
+        if (per_point)
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
+        s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
+                        reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
+                        reinterpret_cast<float*>(sg.dev + o_min), reinterpret_cast<int32_t*>(sg.dev + o_arg),
+                        sg.dev + o_free, dpp, nullptr, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
+                 "D2H min/argmin/free");
+        if (per_point)
+            SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
+    }
+    SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+    std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
+    std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
+    std::memcpy(free_out, sg.host + o_free, M);
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_forward_eval(const svn_model* m, svn_precision prec, const float* raw, int64_t B, int64_t cols,
+                                    float* out) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+    if (!raw || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null buffer");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    float *draw = nullptr, *dout = nullptr;
+    {
+        Scratch sc(st);
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&draw), sizeof(float) * B * cols), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dout), sizeof(float) * B), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(draw, raw, sizeof(float) * B * cols, cudaMemcpyHostToDevice, st), "H2D raw");
+        svn_status s = forward_rows(m, prec, raw, draw, B, cols, dout, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * B, cudaMemcpyDeviceToHost, st), "D2H out");
+    }
+    SVN_CUDA(cudaStreamSynchronize(st), "forward");
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_forward_eval_device(const svn_model* m, svn_precision prec, const float* raw, int64_t B,
+                                           int64_t cols, float* out, void* stream) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // segmenting needs the q columns on the host
+    std::vector<float> host(static_cast<size_t>(B * cols));
+    SVN_CUDA(cudaMemcpyAsync(host.data(), raw, sizeof(float) * B * cols, cudaMemcpyDeviceToHost, st), "D2H raw");
+    SVN_CUDA(cudaStreamSynchronize(st), "D2H raw");
+    return forward_rows(m, prec, host.data(), raw, B, cols, out, st);
+}
+
+SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision prec, const double* cloud, int64_t P,
+                                            const double* q0, const double* q1, int32_t dof, double* min_out,
+                                            int32_t* argmin_out) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (3 + 2 * dof != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: motion dof does not match model");
+    if (!cloud || !q0 || !q1 || !min_out || !argmin_out)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null buffer");
+    // nn.cpp:469-473: every coordinate and joint value is cast to float
+    std::vector<float> pts(static_cast<size_t>(3 * P)), q(static_cast<size_t>(2 * dof));
+    for (int64_t i = 0; i < 3 * P; ++i) pts[i] = static_cast<float>(cloud[i]);
+    for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
+    for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+    float mn = 0.f;
+    int32_t idx = 0;
+    uint8_t fr = 0;
+    svn_status s = svn_query_min(m, prec, pts.data(), P, q.data(), 1, 0.0, &mn, &idx, &fr, nullptr);
+    if (s != SVN_OK) return s;
+    *min_out = static_cast<double>(mn);
+    *argmin_out = idx;
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_eval_grid(const svn_model* m, svn_precision prec, const double* origin, double voxel_size,
+                                 const int32_t* dims, const double* q0, const double* q1, int32_t dof, float* values) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null model");
+    if (!origin || !dims || !q0 || !q1 || !values) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null buffer");
+    if (3 + 2 * dof != m->in)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: q0/q1 must have one angle per joint");
+    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || !(voxel_size > 0))
+        return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: empty grid");
+    const int64_t P = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    std::vector<float> q(static_cast<size_t>(2 * dof));
+    for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
+    for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+    {
+        Scratch sc(st);
+        float *dp = nullptr, *dq = nullptr, *dmin = nullptr, *dvals = nullptr;
+        int32_t* darg = nullptr;
+        uint8_t* dfree = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * P), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * q.size()), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dmin), sizeof(float)), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&darg), sizeof(int32_t)), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dfree), 1), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dvals), sizeof(float) * P), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(dq, q.data(), sizeof(float) * q.size(), cudaMemcpyHostToDevice, st), "H2D q");
+        SVN_CUDA(launch_grid_points(origin, voxel_size, dims, dp, st), "grid_points kernel");
+        ++g_launches;
+        svn_status s = query_dense(m, prec, dp, P, 0, dq, 1, 0.0, dmin, darg, dfree, dvals, nullptr, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(values, dvals, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "D2H values");
+        SVN_CUDA(cudaStreamSynchronize(st), "eval_grid");
+    }
+    return SVN_OK;
+}
+
+
+}  // extern "C"

@@ -250,7 +250,7 @@ def test_fp32_split_unsupported_at_width_512():
 @pytest.mark.parametrize("neg", [None, 2])
 def test_fig2_bf16_affine_fold_with_trained_like_bn(width, blocks, neg):
     """The bf16 kernels fold each block's BN affine into its weights and carry the shifts as an
-    offset (svn_abi.cu fold_affine_bf16).  With non-trivial BN statistics — and a layer with
+    offset (abi_model.cu fold_affine_bf16).  With non-trivial BN statistics — and a layer with
     negative gamma columns, which is kept unfolded — the result stays within the network's
     frozen bf16 bound of the oracle."""
     from fig2_bn import randomize_bn
