@@ -88,7 +88,10 @@ class Model:
     def query_min(self, points: np.ndarray, q01: np.ndarray, margin: float, precision: str = "bf16",
                   per_point: bool = False) -> QueryResult:
         """Every (point x motion) pair -> per-motion min, argmin, `min > margin`.
-        points float [P, 3]; q01 float [M, 2*dof] = (q0 | q1)."""
+        points float [P, 3]; q01 float [M, 2*dof] = (q0 | q1).
+        precision: "bf16" (tcgen05, per-network stated bound), "fp32" / "fp32_exact" (the FP32
+        path: FFMA in the reference's order, bit-identical to the oracle), "fp32_split"
+        (width 256: fp32-grade split-fp16 on tcgen05, its own stated bound)."""
         pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
         q = np.ascontiguousarray(q01, dtype=np.float32).reshape(-1, 2 * self.program.dof)
         P, M = pts.shape[0], q.shape[0]
