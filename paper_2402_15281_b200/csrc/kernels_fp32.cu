@@ -5,7 +5,7 @@
 // plus the argmin of predict_min_distance (nn.cpp:476-478) and the margin test
 // (collision.cpp:68).  Each CTA owns a 64-row tile of one motion.  Activations stay
 // in shared memory, transposed (actT[k][row]), between layers; weight rows stream
-// through a 4-stage ring of 16 KiB bulk copies (cp.async.bulk, TMA engine).  Each
+// through a 2-stage ring of 32 KiB bulk copies (cp.async.bulk, TMA engine).  Each
 // output is one sequential fmaf chain over k ascending — the same order as the
 // reference's column axpy — so with `exact` set (no q-fold: bias, h part, x, q0,
 // q1) the per-point delta matches the CPU restatement bit for bit.
@@ -106,6 +106,19 @@ __device__ __forceinline__ void tile_done(const FusedArgs& a, int32_t motion) {
 }
 
 // ------------------------------------------------------------------ K1f -----
+// Weight chunks of 32 KiB, double-buffered, and the k loop unrolled 8: one barrier per 32
+// (width 256) or 16 (width 512) k steps.  Measured against 4 x 16 KiB stages with unroll 4:
+// +6 % on c2 and on c3's network in fp32 (scripts/gpu_ab.sh; the -D overrides are A/B hooks).
+#ifndef SVN_FP32_UNROLL
+#define SVN_FP32_UNROLL 8
+#endif
+constexpr int kFp32Unroll = SVN_FP32_UNROLL;
+#ifndef SVN_FP32_STAGES
+#define SVN_FP32_STAGES 2
+#endif
+#ifndef SVN_FP32_CHUNK
+#define SVN_FP32_CHUNK 8192  // floats per weight chunk
+#endif
 template <int N, int CG = 32, int TMO = 0>
 struct Fp32Cfg {
     // rows per tile (activations must fit in smem); TMO = 32 for workloads with fewer tiles
@@ -113,8 +126,8 @@ struct Fp32Cfg {
     static constexpr int TM = TMO ? TMO : (N >= 512 ? 64 : 128);
     static constexpr int THREADS = TM / 8 * CG;     // TM/8 row groups x CG column groups
     static constexpr int NC = N / CG;               // columns per thread (8 x NC register tile)
-    static constexpr int KS = 4096 / N;           // weight rows per 16 KiB chunk
-    static constexpr int STAGES = 4;
+    static constexpr int KS = SVN_FP32_CHUNK / N;  // weight rows per chunk
+    static constexpr int STAGES = SVN_FP32_STAGES;
     static constexpr int ACT_ROWS = N + kMaxIn;   // h rows then z rows
     static constexpr size_t ACT_BYTES = static_cast<size_t>(ACT_ROWS) * TM * 4;
     static constexpr size_t STAGE_BYTES = static_cast<size_t>(KS) * N * 4;
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                 if (nk == C::KS) {
                     // full chunk: unrolled so the next k's shared-memory loads are scheduled
                     // under the current k's FMAs (each output keeps its own k-ordered chain)
-#pragma unroll 4
+#pragma unroll kFp32Unroll
                     for (int kk = 0; kk < C::KS; ++kk) kstep(kk);
                 } else {
                     for (int kk = 0; kk < nk; ++kk) kstep(kk);

@@ -1,4 +1,4 @@
-for m in 64 128 256 512 1024; do
+for m in ${MS:-16 32 64 128 256 512 1024}; do
   timeout 300 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-e2e --config c2 --precision bf16 --motions $m > gpurun_out/sw_$m.log 2>&1
   python - "$m" <<'PY'
 import json,sys
