@@ -1,6 +1,7 @@
+# ncu --set full of the three width-256 kernels on c2 (FP32 path, fp32_split, bf16 ping-pong)
 set -x
-C1="python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
-C2="python bench.py --config c2 --precision bf16 --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
-timeout 300 $C1 > gpurun_out/p1.log 2>&1 && timeout 300 $C2 > gpurun_out/p2.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_split -s 1 -c 1 -o gpurun_out/prof_split $C1 > gpurun_out/ncu_split.log 2>&1; echo "ncu split rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_bf16_pp -s 1 -c 1 -o gpurun_out/prof_pp $C2 > gpurun_out/ncu_pp.log 2>&1; echo "ncu pp rc=$?"
+for p in fp32 fp32_split bf16; do
+  C="python bench.py --config c2 --precision $p --steps 1 --warmup 3 --no-cpu-baseline --no-e2e"
+  timeout 300 $C > gpurun_out/pw_$p.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused_ -s 1 -c 1 -o gpurun_out/prof_c2_$p $C > gpurun_out/ncu_c2_$p.log 2>&1; echo "ncu $p rc=$?"
+done

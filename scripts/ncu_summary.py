@@ -23,6 +23,15 @@ for k in keys:
     if k in h:
         i = h.index(k)
         print(f"{k} = {v[i]} {units[i]}")
+# cycles where no instruction issued, by the reason the sampled warp was stalled
+ni = {k[len("smsp__pcsamp_warps_issue_stalled_"):-len("_not_issued")]: float(x or 0)
+      for k, x in zip(h, v) if k.startswith("smsp__pcsamp_warps_issue_stalled_") and k.endswith("_not_issued")}
+sel = float(v[h.index("smsp__pcsamp_warps_issue_stalled_selected")] or 0) if "smsp__pcsamp_warps_issue_stalled_selected" in h else 0
+if ni and sel:
+    tot_ni = sum(ni.values())
+    print(f"issue samples: selected {sel:.0f}, not issued {tot_ni:.0f}; not-issued by stall reason (% of all):")
+    for k2, x in sorted(ni.items(), key=lambda t: -t[1])[:8]:
+        print(f"  {k2:22s} {x / (sel + tot_ni) * 100:5.1f}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
