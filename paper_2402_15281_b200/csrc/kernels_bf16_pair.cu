@@ -411,15 +411,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                         const int c0 = j * C::NH + ch * C::COLS;
                         constexpr int NCH = C::COLS / 32;
                         uint32_t ra[32], rb[32];
-                        tmem_ld32_async(tmem + t_lane + static_cast<uint32_t>(c0), ra);
-                        tmem_wait_tied(ra);
+                        const uint32_t tb = tmem + t_lane;
+                        tmem_ld32_async(tb + static_cast<uint32_t>(c0), ra);
+                        tmem_ld32_async(tb + static_cast<uint32_t>(c0 + 32), rb);
+                        tmem_wait_tied2(ra, rb);
 #pragma unroll
-                        for (int q = 0; q < NCH; ++q) {
-                            uint32_t(&cur)[32] = (q & 1) ? rb : ra;
-                            uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
-                            if (q + 1 < NCH) tmem_ld32_async(tmem + t_lane + static_cast<uint32_t>(c0 + 32 * (q + 1)), nxt);
-                            pair_epi32<N>(ld, l, last, reinterpret_cast<float*>(cur), c0 + 32 * q, row, A, wo_s, dot);
-                            if (q + 1 < NCH) tmem_wait_tied(nxt);
+                        for (int q = 0; q < NCH; q += 2) {
+                            pair_epi32<N>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot);
+                            if (q + 2 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(c0 + 32 * (q + 2)), ra);
+                            pair_epi32<N>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot);
+                            if (q + 3 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(c0 + 32 * (q + 3)), rb);
+                            if (q + 2 < NCH) tmem_wait_tied2(ra, rb);
                         }
                     }
                     const unsigned long long c2 = prof_clock();

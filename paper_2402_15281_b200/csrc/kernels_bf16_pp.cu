@@ -39,8 +39,9 @@ constexpr bool kTimeline = false;
 #endif
 constexpr int XSTAGES = 2;
 constexpr int EPI_WARPS = 8;
-constexpr int OUT_WARP = 2 + EPI_WARPS;    // keys / per-point outputs / next tile's A extension
-constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
+constexpr int OUT_WARP = 2 + EPI_WARPS;    // first output warp: keys / per-point outputs / next tile's A extension
+constexpr int OUT_WARPS = 2;              // one per slot
+constexpr int THREADS = 64 + EPI_WARPS * 32 + OUT_WARPS * 32;
 constexpr int COLS = N / 2;                // columns per epilogue thread
 constexpr uint32_t OFF_AX = 2 * A_BYTES;
 constexpr uint32_t OFF_W = OFF_AX + 2 * AX_BYTES;
@@ -453,15 +454,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
             atomicAdd(a.prof + kProfEpiOut, pe_o);
         }
     } else {
-        // ---------------------------------------------------------------- output warp --
-        // Per finished tile of slot s: delta = dot + bo for this CTA's 128 rows, per-point
-        // stores, one packed-key atomicMin, the per-motion completion counter; and the A
-        // extension (bias / x columns) of the slot's next tile, whose point loads are issued
-        // before waiting so they land while the tile is still in the tensor core.
+        // ---------------------------------------------------------------- output warps --
+        // One warp per slot.  Per finished tile of its slot: delta = dot + bo for this CTA's
+        // 128 rows, per-point stores, one packed-key atomicMin, the per-motion completion
+        // counter; and the A extension (bias / x columns) of the slot's next tile.  The point
+        // loads run a whole round ahead (tile j+2 of the slot is loaded when tile j+1's AX is
+        // written), and the two slots never queue behind each other's atomics, so AX_s is
+        // ready as soon as the slot's last epilogue has finished.
+        const int s = warp - OUT_WARP;
         const uint32_t ax_ready0 = mapa_shared(smem_u32(ax_ready), 0);
-        uint32_t of_ph[2] = {0u, 0u};
-        float px[2][4][3];
-        auto load_points = [&](int64_t t, int s) {
+        uint32_t of_ph = 0u;
+        float px[4][3];
+        auto load_points = [&](int64_t t) {
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
@@ -469,77 +473,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
             for (int k = 0; k < 4; ++k) {
                 const int32_t r = static_cast<int32_t>(rank * TM + k * 32 + lane);
                 const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
-                px[s][k][0] = xp[0];
-                px[s][k][1] = xp[1];
-                px[s][k][2] = xp[2];
+                px[k][0] = xp[0];
+                px[k][1] = xp[1];
+                px[k][2] = xp[2];
             }
         };
-        auto store_ax = [&](int s) {
+        auto store_ax = [&]() {
 #pragma unroll
             for (int k = 0; k < 4; ++k)
-                write_ax(AX + s * AX_BYTES, static_cast<uint32_t>(k * 32) + lane, (px[s][k][0] - a.shift[0]) * a.scale[0],
-                         (px[s][k][1] - a.shift[1]) * a.scale[1], (px[s][k][2] - a.shift[2]) * a.scale[2]);
+                write_ax(AX + s * AX_BYTES, static_cast<uint32_t>(k * 32) + lane, (px[k][0] - a.shift[0]) * a.scale[0],
+                         (px[k][1] - a.shift[1]) * a.scale[1], (px[k][2] - a.shift[2]) * a.scale[2]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(ax_ready0 + s * 8u);
         };
         unsigned long long pe_x = 0;
-        for (int s = 0; s < 2; ++s)
-            if (has(0, s)) {
-                load_points(tile_of(0, s), s);
-                store_ax(s);
+        if (has(0, s)) {
+            load_points(tile_of(0, s));
+            store_ax();
+            if (has(1, s)) load_points(tile_of(1, s));
+        }
+        for (int64_t j = 0; j < R && has(j, s); ++j) {
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
+            mbar_wait(&out_full[s], of_ph);
+            of_ph ^= 1u;
+            const unsigned long long c0 = prof_clock();
+            // every MMA of tile (j, s) has completed, so AX_s is free for the next tile
+            if (has(j + 1, s)) {
+                store_ax();
+                if (has(j + 2, s)) load_points(tile_of(j + 2, s));
             }
-        for (int64_t j = 0; j < R; ++j) {
-            const int nslots = has(j, 1) ? 2 : 1;
-            for (int s = 0; s < nslots; ++s) {
-                const bool next = has(j + 1, s);
-                if (next) load_points(tile_of(j + 1, s), s);
-                int32_t motion, nrows;
-                int64_t pbase, obase;
-                tile_decode(a, tile_of(j, s), 2 * TM, motion, pbase, obase, nrows);
-                mbar_wait(&out_full[s], of_ph[s]);
-                of_ph[s] ^= 1u;
-                const unsigned long long c0 = prof_clock();
-                // every MMA of tile (j, s) has completed, so AX_s is free for the next tile
-                if (next) store_ax(s);
-                float delta[4];
+            float delta[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int r = k * 32 + static_cast<int>(lane);
-                    delta[k] = (dotbuf[(s * 2) * TM + r] + dotbuf[(s * 2 + 1) * TM + r]) + a.bo;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&out_empty[s]);
-                unsigned long long key = ~0ull;
+            for (int k = 0; k < 4; ++k) {
+                const int r = k * 32 + static_cast<int>(lane);
+                delta[k] = (dotbuf[(s * 2) * TM + r] + dotbuf[(s * 2 + 1) * TM + r]) + a.bo;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&out_empty[s]);
+            unsigned long long key = ~0ull;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int32_t rr = static_cast<int32_t>(rank * TM + k * 32 + lane);
-                    if (rr < nrows) {
-                        if (a.per_point) a.per_point[obase + rr] = delta[k];
-                        const unsigned long long kk = row_key(delta[k], a.index_offset + pbase + rr);
-                        key = kk < key ? kk : key;
-                    }
+            for (int k = 0; k < 4; ++k) {
+                const int32_t rr = static_cast<int32_t>(rank * TM + k * 32 + lane);
+                if (rr < nrows) {
+                    if (a.per_point) a.per_point[obase + rr] = delta[k];
+                    const unsigned long long kk = row_key(delta[k], a.index_offset + pbase + rr);
+                    key = kk < key ? kk : key;
                 }
-                if (a.keys) {
-                    key = warp_min_u64(key);
-                    if (lane == 0) {
-                        atomicMin(a.keys + motion, key);
-                        if (a.counters) {
+            }
+            if (a.keys) {
+                key = warp_min_u64(key);
+                if (lane == 0) {
+                    atomicMin(a.keys + motion, key);
+                    if (a.counters) {
+                        __threadfence();
+                        const unsigned int prev = atomicAdd(a.counters + motion, 1u);
+                        if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
                             __threadfence();
-                            const unsigned int prev = atomicAdd(a.counters + motion, 1u);
-                            if (prev + 1 == 2u * static_cast<unsigned int>(a.tiles_per_motion)) {
-                                __threadfence();
-                                const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
-                                decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion,
-                                           a.free_out + motion);
-                            }
+                            const unsigned long long kk = atomicOr(a.keys + motion, 0ull);
+                            decode_key(kk, a.margin, a.min_out + motion, a.argmin_out + motion, a.free_out + motion);
                         }
                     }
                 }
-                pe_x += prof_clock() - c0;
             }
+            pe_x += prof_clock() - c0;
         }
-        if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
+        if (a.prof && lane == 0 && rank == 0 && s == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
     }
 
     tc_fence_before();
