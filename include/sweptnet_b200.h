@@ -53,7 +53,8 @@ typedef enum {
     SVN_ERR_IO = 5,          /* IoError          errors.hpp:8  */
     SVN_ERR_FORMAT = 6,      /* FormatError      errors.hpp:13 */
     SVN_ERR_TRUNCATION = 7,  /* TruncationError  errors.hpp:18 */
-    SVN_ERR_VERSION = 8      /* VersionError     errors.hpp:23 */
+    SVN_ERR_VERSION = 8,     /* VersionError     errors.hpp:23 */
+    SVN_ERR_NCCL = 9         /* NCCL communicator / collective failure (multi-GPU) */
 } svn_status;
 
 /* Arithmetic of the fused MLP kernel.
@@ -237,6 +238,28 @@ typedef struct {
 SVN_API svn_status svn_gcc_nn_search(const svn_model* model, svn_precision prec, const svn_robot_desc* robot,
                                      const double* cloud, int64_t P, const double* q01, int64_t M, int32_t steps,
                                      double margin, int32_t batch, svn_search_result* out);
+
+/* Several GPUs of one box from one host process (the reference's callers
+ * run predict_min_distance from parallel_for workers in one process, bench.cpp:156,193).
+ * svn_multi_create builds one model per listed device and one persistent worker thread per
+ * device; with distinct devices it also opens an NCCL communicator over them.
+ * svn_query_min_multi has svn_query_min's contract (HOST buffers, synchronous), split:
+ *   SVN_SHARD_MOTIONS  device d takes motions [d*M/G, (d+1)*M/G); no communication;
+ *   SVN_SHARD_POINTS   device d takes points [d*P/G, (d+1)*P/G); one NCCL u64 MIN
+ *                      all-reduce of the packed (delta, index) keys, 8 B per motion;
+ *                      needs distinct devices (UNSUPPORTED otherwise);
+ *   SVN_SHARD_AUTO     points when M < G, else motions.
+ * Results are bit-identical to one device in every mode.  Calls on one svn_multi are
+ * serialised. */
+typedef struct svn_multi svn_multi;
+typedef enum { SVN_SHARD_AUTO = 0, SVN_SHARD_MOTIONS = 1, SVN_SHARD_POINTS = 2 } svn_shard_mode;
+SVN_API svn_status svn_multi_create(const svn_model_desc* desc, const float* params, int64_t n_params,
+                                    const int32_t* devices, int32_t n_devices, svn_multi** out);
+SVN_API svn_status svn_multi_destroy(svn_multi* multi);
+SVN_API int32_t svn_multi_device_count(const svn_multi* multi);
+SVN_API svn_status svn_query_min_multi(svn_multi* multi, svn_precision prec, const float* points, int64_t P,
+                                       const float* q01, int64_t M, double margin, svn_shard_mode mode,
+                                       float* min_out, int32_t* argmin_out, uint8_t* free_out);
 
 /* Kernel launches issued by this thread since the last reset (evidence for bench.py). */
 SVN_API int64_t svn_launch_count(void);

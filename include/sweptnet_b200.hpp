@@ -170,4 +170,42 @@ inline std::function<double(int)> batched_proxy(const Model& m, const std::vecto
     return [mins](int j) { return static_cast<double>((*mins)[static_cast<size_t>(j)]); };
 }
 
+// Several GPUs of this box from one process (svn_multi_*): one model copy and one worker
+// thread per device.  query_min shards motions (no communication) or, for batches with
+// fewer motions than devices, points (one NCCL u64 MIN all-reduce); bit-identical to Model.
+enum class Shard { AUTO = SVN_SHARD_AUTO, MOTIONS = SVN_SHARD_MOTIONS, POINTS = SVN_SHARD_POINTS };
+
+struct MinResult {
+    std::vector<float> min;
+    std::vector<int32_t> argmin;
+    std::vector<uint8_t> free;
+};
+
+class MultiModel {
+public:
+    MultiModel(const Program& prog, const std::vector<float>& params, const std::vector<int32_t>& devices)
+        : prog_(prog) {
+        const svn_model_desc d = prog_.desc();
+        svn_multi* h = nullptr;
+        check(svn_multi_create(&d, params.data(), static_cast<int64_t>(params.size()), devices.data(),
+                               static_cast<int32_t>(devices.size()), &h));
+        h_.reset(h, svn_multi_destroy);
+    }
+    // points float [P x 3], q01 float [M x 2 dof] (q0 | q1), as svn_query_min.
+    MinResult query_min(const std::vector<float>& points, const std::vector<float>& q01, double margin,
+                        Precision prec = Precision::BF16, Shard shard = Shard::AUTO) const {
+        const int64_t P = static_cast<int64_t>(points.size() / 3), M = static_cast<int64_t>(q01.size() / (2 * prog_.dof));
+        MinResult r{std::vector<float>(static_cast<size_t>(M)), std::vector<int32_t>(static_cast<size_t>(M)),
+                    std::vector<uint8_t>(static_cast<size_t>(M))};
+        check(svn_query_min_multi(h_.get(), static_cast<svn_precision>(prec), points.data(), P, q01.data(), M, margin,
+                                  static_cast<svn_shard_mode>(shard), r.min.data(), r.argmin.data(), r.free.data()));
+        return r;
+    }
+    int devices() const { return svn_multi_device_count(h_.get()); }
+
+private:
+    Program prog_;
+    std::shared_ptr<svn_multi> h_;
+};
+
 }  // namespace sweptnet_b200

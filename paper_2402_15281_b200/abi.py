@@ -15,7 +15,8 @@ from . import build as _build
 LIB_PATH = _build.LIB
 
 # svn_status
-OK, INVALID_ARGUMENT, CUDA_ERROR, OUT_OF_MEMORY, UNSUPPORTED, IO, FORMAT, TRUNCATION, VERSION = range(9)
+OK, INVALID_ARGUMENT, CUDA_ERROR, OUT_OF_MEMORY, UNSUPPORTED, IO, FORMAT, TRUNCATION, VERSION, NCCL_ERROR = range(10)
+SHARD_MODES = {"auto": 0, "motions": 1, "points": 2}
 # svn_precision
 PREC_BF16, PREC_FP32, PREC_FP32_EXACT, PREC_FP32_SPLIT = 0, 1, 2, 3
 PRECISIONS = {"bf16": PREC_BF16, "fp32": PREC_FP32, "fp32_exact": PREC_FP32_EXACT, "fp32_split": PREC_FP32_SPLIT}
@@ -110,6 +111,10 @@ def _finish(L):
         "svn_gcc_min_distance": (C.c_int, [P, P, I64, P, I64, I32, D, I32, P, P]),
         "svn_gcc_min_distance_device": (C.c_int, [P, P, I64, P, I64, I32, D, P, P, VP]),
         "svn_gcc_nn_search": (C.c_int, [P, C.c_int, P, P, I64, P, I64, I32, D, I32, C.POINTER(SvnSearchResult)]),
+        "svn_multi_create": (C.c_int, [desc_p, P, I64, P, I32, C.POINTER(VP)]),
+        "svn_multi_destroy": (C.c_int, [VP]),
+        "svn_multi_device_count": (I32, [VP]),
+        "svn_query_min_multi": (C.c_int, [VP, C.c_int, P, I64, P, I64, D, C.c_int, P, P, P]),
         "svn_launch_count": (I64, []),
         "svn_launch_count_reset": (None, []),
         "svn_kernel_timing_begin": (None, []),
@@ -129,7 +134,8 @@ EXPORTED = ("svn_param_count", "svn_trainable_param_count", "svn_init_params", "
             "svn_model_load_checkpoint", "svn_model_destroy", "svn_query_min_device", "svn_query_min",
             "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
             "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_gcc_min_distance",
-            "svn_gcc_min_distance_device", "svn_gcc_nn_search", "svn_launch_count",
+            "svn_gcc_min_distance_device", "svn_gcc_nn_search", "svn_multi_create", "svn_multi_destroy",
+            "svn_multi_device_count", "svn_query_min_multi", "svn_launch_count",
             "svn_launch_count_reset",
             "svn_kernel_timing_begin", "svn_kernel_timing_end", "svn_last_error", "svn_version")
 

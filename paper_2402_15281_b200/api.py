@@ -155,6 +155,51 @@ class Model:
                                                       q01.shape[0], abi.ptr(keys), st))
 
 
+class MultiModel:
+    """One model per listed GPU of this box, driven from this process by one native worker
+    thread per device (svn_multi_*).  query_min has Model.query_min's
+    contract; shard = "motions" (no communication), "points" (one NCCL u64 MIN all-reduce of
+    8 B per motion; distinct devices only) or "auto" (points when there are fewer motions
+    than devices).  Results are bit-identical to a single Model."""
+
+    def __init__(self, program: LayerProgram, params: np.ndarray, devices=(0,)):
+        params = np.ascontiguousarray(params, dtype=np.float32)
+        if params.size != program.param_floats():
+            raise abi.ReferenceInvalidArgument(abi.INVALID_ARGUMENT, "model: parameter count mismatch")
+        self.program = program
+        self.devices = tuple(int(d) for d in devices)
+        desc, keep = abi.make_desc(program)
+        devs = np.asarray(self.devices, dtype=np.int32)
+        h = C.c_void_p()
+        abi.check(abi.lib().svn_multi_create(C.byref(desc), abi.ptr(params), params.size, abi.ptr(devs),
+                                             len(self.devices), C.byref(h)))
+        self._h = h
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            abi.lib().svn_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def query_min(self, points: np.ndarray, q01: np.ndarray, margin: float, precision: str = "bf16",
+                  shard: str = "auto") -> QueryResult:
+        pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+        q = np.ascontiguousarray(q01, dtype=np.float32).reshape(-1, 2 * self.program.dof)
+        P, M = pts.shape[0], q.shape[0]
+        mn = np.empty(M, np.float32)
+        am = np.empty(M, np.int32)
+        fr = np.empty(M, np.uint8)
+        abi.check(abi.lib().svn_query_min_multi(self._h, abi.PRECISIONS[precision], abi.ptr(pts), P, abi.ptr(q), M,
+                                                float(margin), abi.SHARD_MODES[shard], abi.ptr(mn), abi.ptr(am),
+                                                abi.ptr(fr)))
+        return QueryResult(mn, am, fr.astype(bool), None)
+
+
 def keys_init_device(keys, stream=None) -> None:
     st = C.c_void_p(stream.cuda_stream if stream is not None else 0)
     abi.check(abi.lib().svn_keys_init_device(abi.ptr(keys), keys.numel(), st))

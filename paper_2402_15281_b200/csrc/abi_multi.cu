@@ -1,0 +1,328 @@
+// abi_multi.cu — several GPUs of one box from one host process: one
+// persistent worker thread per device, each with its own model copy, stream and staging.
+//
+//   motions sharding (default): worker d evaluates motions [d*M/G, (d+1)*M/G) against the
+//     whole cloud through the single-GPU path and writes its slice of the outputs; no
+//     communication, results bit-identical to one GPU.
+//   points sharding (single-motion batches, M < G): worker d evaluates the point chunk
+//     [d*P/G, (d+1)*P/G) into packed u64 keys with global point indices, the shards meet in
+//     one NCCL MIN all-reduce of 8 B per motion, and device 0 decodes (min, argmin, class);
+//     bit-identical to one GPU by construction (min is order-free, ties keep the lowest index).
+//
+// The reference's callers are C++ in one process: run_box_world calls predict_min_distance
+// from parallel_for workers (bench.cpp:156,193), so this is the entry a drop-in C++ host uses
+// to spread a scene's motions over the box.  NCCL is opened with dlopen on first use
+// (libnccl.so.2: the system 2.27 here, or the copy a host process has already loaded).
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <condition_variable>
+#include <functional>
+#include <memory>
+#include <thread>
+
+#include "abi_internal.cuh"
+
+namespace svn {
+namespace abi {
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*comm_init_all)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    std::string why;
+    bool ok() const { return comm_init_all && all_reduce && comm_destroy && error_string; }
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("NCCL not loadable: ") + dlerror();
+            return a;
+        }
+        a.comm_init_all = reinterpret_cast<decltype(a.comm_init_all)>(dlsym(h, "ncclCommInitAll"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!a.ok()) a.why = "NCCL library lacks ncclCommInitAll / ncclAllReduce";
+        return a;
+    }();
+    return api;
+}
+
+// A worker thread pinned to one device: runs one job at a time, posted by the caller.
+class Worker {
+  public:
+    Worker() : th_([this] { loop(); }) {}
+    ~Worker() {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            quit_ = true;
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    void post(std::function<void()> job) {
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            job_ = std::move(job);
+            busy_ = true;
+        }
+        cv_.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [this] { return !busy_; });
+    }
+
+  private:
+    void loop() {
+        for (;;) {
+            std::function<void()> job;
+            {
+                std::unique_lock<std::mutex> l(mu_);
+                cv_.wait(l, [this] { return quit_ || (busy_ && job_); });
+                if (quit_) return;
+                job = std::move(job_);
+                job_ = nullptr;
+            }
+            job();
+            {
+                std::lock_guard<std::mutex> l(mu_);
+                busy_ = false;
+            }
+            cv_.notify_all();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::function<void()> job_;
+    bool busy_ = false, quit_ = false;
+    std::thread th_;
+};
+
+// Workers meet here before the collective, so no rank enters the all-reduce when another
+// one has already failed (it would wait for it forever).
+class Rendezvous {
+  public:
+    explicit Rendezvous(int n) : n_(n) {}
+    bool arrive_all_ok(bool ok) {
+        std::unique_lock<std::mutex> l(mu_);
+        ok_ = ok_ && ok;
+        const int gen = gen_;
+        if (++count_ == n_) {
+            count_ = 0;
+            ++gen_;
+            result_ = ok_;
+            ok_ = true;
+            cv_.notify_all();
+            return result_;
+        }
+        cv_.wait(l, [&] { return gen_ != gen; });
+        return result_;
+    }
+
+  private:
+    std::mutex mu_;
+    std::condition_variable cv_;
+    int n_, count_ = 0, gen_ = 0;
+    bool ok_ = true, result_ = true;
+};
+
+struct Outcome {
+    svn_status status = SVN_OK;
+    std::string msg;
+    int64_t launches = 0;
+};
+
+}  // namespace
+}  // namespace abi
+}  // namespace svn
+
+struct svn_multi {
+    std::vector<int32_t> devices;
+    std::vector<svn_model*> models;
+    std::vector<ncclComm_t> comms;  // empty unless every device is distinct and NCCL loads
+    std::string no_comm_why;
+    std::vector<std::unique_ptr<svn::abi::Worker>> workers;
+    std::mutex call_mu;  // one call at a time: collectives of two calls must not interleave
+    ~svn_multi() {
+        workers.clear();
+        if (!comms.empty())
+            for (ncclComm_t c : comms) svn::abi::nccl_api().comm_destroy(c);
+        for (svn_model* m : models) svn_model_destroy(m);
+    }
+};
+
+namespace svn {
+namespace abi {
+namespace {
+
+// Run job(d) on every worker and collect the outcomes (status, message, launches) in the
+// caller's thread-local error / launch state.
+svn_status run_all(svn_multi* mg, const std::function<void(int, Outcome&)>& job) {
+    const int G = static_cast<int>(mg->devices.size());
+    std::vector<Outcome> out(static_cast<size_t>(G));
+    for (int d = 0; d < G; ++d)
+        mg->workers[d]->post([&, d] {
+            const int64_t l0 = g_launches;
+            job(d, out[d]);
+            out[d].launches = g_launches - l0;
+        });
+    for (int d = 0; d < G; ++d) mg->workers[d]->wait();
+    for (const Outcome& o : out) g_launches += o.launches;
+    for (const Outcome& o : out)
+        if (o.status != SVN_OK) return fail(o.status, o.msg);
+    return SVN_OK;
+}
+
+void record(Outcome& o, svn_status s) {
+    if (s != SVN_OK && o.status == SVN_OK) {
+        o.status = s;
+        o.msg = svn_last_error();
+    }
+}
+
+}  // namespace
+}  // namespace abi
+}  // namespace svn
+
+using namespace svn::abi;
+
+extern "C" {
+
+SVN_API svn_status svn_multi_create(const svn_model_desc* desc, const float* params, int64_t n_params,
+                                    const int32_t* devices, int32_t n_devices, svn_multi** out) {
+    if (!out) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: null output");
+    *out = nullptr;
+    if (!devices || n_devices < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: no devices");
+    int count = 0;
+    SVN_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    for (int d = 0; d < n_devices; ++d)
+        if (devices[d] < 0 || devices[d] >= count) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: no such device");
+    std::unique_ptr<svn_multi> mg(new svn_multi);
+    mg->devices.assign(devices, devices + n_devices);
+    for (int d = 0; d < n_devices; ++d) {
+        svn_model* m = nullptr;
+        const svn_status s = svn_model_create(desc, params, n_params, devices[d], &m);
+        if (s != SVN_OK) return s;
+        mg->models.push_back(m);
+    }
+    bool distinct = true;
+    for (int i = 0; i < n_devices; ++i)
+        for (int j = 0; j < i; ++j)
+            if (devices[i] == devices[j]) distinct = false;
+    if (!distinct) {
+        mg->no_comm_why = "point sharding needs distinct devices (one NCCL rank per GPU)";
+    } else if (!nccl_api().ok()) {
+        mg->no_comm_why = nccl_api().why;
+    } else {
+        mg->comms.resize(static_cast<size_t>(n_devices));
+        const ncclResult_t r = nccl_api().comm_init_all(mg->comms.data(), n_devices, mg->devices.data());
+        if (r != ncclSuccess) {
+            mg->comms.clear();
+            return fail(SVN_ERR_NCCL, std::string("ncclCommInitAll: ") + nccl_api().error_string(r));
+        }
+    }
+    for (int d = 0; d < n_devices; ++d) mg->workers.emplace_back(new Worker);
+    *out = mg.release();
+    return SVN_OK;
+}
+
+SVN_API svn_status svn_multi_destroy(svn_multi* mg) {
+    delete mg;
+    return SVN_OK;
+}
+
+SVN_API int32_t svn_multi_device_count(const svn_multi* mg) {
+    return mg ? static_cast<int32_t>(mg->devices.size()) : 0;
+}
+
+SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const float* points, int64_t P,
+                                       const float* q01, int64_t M, double margin, svn_shard_mode mode,
+                                       float* min_out, int32_t* argmin_out, uint8_t* free_out) {
+    if (!mg) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    if (!points || !q01 || !min_out || !argmin_out || !free_out)
+        return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+    NvtxRange nvtx("svn query_min_multi");
+    std::lock_guard<std::mutex> lock(mg->call_mu);
+    const int G = static_cast<int>(mg->devices.size());
+    if (mode == SVN_SHARD_AUTO) mode = M < G ? SVN_SHARD_POINTS : SVN_SHARD_MOTIONS;
+    const int64_t nq = 2 * static_cast<int64_t>(mg->models[0]->dof);
+
+    if (mode == SVN_SHARD_MOTIONS) {
+        return run_all(mg, [&](int d, Outcome& o) {
+            const int64_t b = d * M / G, e = (d + 1) * M / G;
+            if (e > b)
+                record(o, svn_query_min(mg->models[d], prec, points, P, q01 + b * nq, e - b, margin, min_out + b,
+                                        argmin_out + b, free_out + b, nullptr));
+        });
+    }
+    if (mode != SVN_SHARD_POINTS) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: unknown shard mode");
+    if (mg->comms.empty()) return fail(SVN_ERR_UNSUPPORTED, "multi: " + mg->no_comm_why);
+    Rendezvous meet(G);
+    return run_all(mg, [&](int d, Outcome& o) {
+        const svn_model* m = mg->models[d];
+        const int64_t pb = d * P / G, pe = (d + 1) * P / G;
+        DeviceGuard guard(m->device);
+        ensure_pool(m->device);
+        cudaStream_t st = thread_stream(m->device);
+        float *dp = nullptr, *dq = nullptr, *dmin = nullptr;
+        uint64_t* keys = nullptr;
+        int32_t* darg = nullptr;
+        uint8_t* dfree = nullptr;
+        auto cu = [&](cudaError_t e, const char* what) {
+            if (e != cudaSuccess) record(o, cuda_fail(e, what));
+            return e == cudaSuccess;
+        };
+        bool ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dq), sizeof(float) * nq * M, st), "cudaMallocAsync") &&
+                  cu(cudaMallocAsync(reinterpret_cast<void**>(&keys), sizeof(uint64_t) * M, st), "cudaMallocAsync") &&
+                  cu(cudaMallocAsync(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * (pe > pb ? pe - pb : 1), st),
+                     "cudaMallocAsync") &&
+                  cu(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions") &&
+                  cu(cudaMemcpyAsync(dp, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
+                     "H2D point chunk");
+        if (ok) {
+            record(o, svn_keys_init_device(keys, M, st));
+            if (o.status == SVN_OK && pe > pb) record(o, svn_query_min_keys_device(m, prec, dp, pe - pb, pb, dq, M, keys, st));
+            ok = o.status == SVN_OK && cu(cudaStreamSynchronize(st), "point-shard kernels");
+        }
+        if (meet.arrive_all_ok(ok)) {
+            // the one exchange of the path: 8 B per motion, u64 MIN over NVLink
+            const ncclResult_t r = nccl_api().all_reduce(keys, keys, static_cast<size_t>(M), ncclUint64, ncclMin,
+                                                         mg->comms[d], st);
+            if (r != ncclSuccess) {
+                o.status = SVN_ERR_NCCL;
+                o.msg = std::string("ncclAllReduce: ") + nccl_api().error_string(r);
+            } else if (d == 0) {
+                ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dmin), sizeof(float) * M, st), "cudaMallocAsync") &&
+                     cu(cudaMallocAsync(reinterpret_cast<void**>(&darg), sizeof(int32_t) * M, st), "cudaMallocAsync") &&
+                     cu(cudaMallocAsync(reinterpret_cast<void**>(&dfree), M, st), "cudaMallocAsync");
+                if (ok) record(o, svn_keys_finalize_device(keys, M, margin, dmin, darg, dfree, st));
+                if (ok && o.status == SVN_OK)
+                    ok = cu(cudaMemcpyAsync(min_out, dmin, sizeof(float) * M, cudaMemcpyDeviceToHost, st), "D2H min") &&
+                         cu(cudaMemcpyAsync(argmin_out, darg, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st),
+                            "D2H argmin") &&
+                         cu(cudaMemcpyAsync(free_out, dfree, M, cudaMemcpyDeviceToHost, st), "D2H free");
+            }
+            cu(cudaStreamSynchronize(st), "all-reduce");
+        } else if (o.status == SVN_OK) {
+            o.status = SVN_ERR_CUDA;
+            o.msg = "multi: another device failed before the all-reduce";
+        }
+        for (void* p : {static_cast<void*>(dp), static_cast<void*>(dq), static_cast<void*>(keys),
+                        static_cast<void*>(dmin), static_cast<void*>(darg), static_cast<void*>(dfree)})
+            if (p) cudaFreeAsync(p, st);
+        cudaStreamSynchronize(st);
+    });
+}
+
+}  // extern "C"

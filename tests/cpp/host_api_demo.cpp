@@ -31,7 +31,22 @@ int main() {
     } catch (const std::invalid_argument& e) {
         threw = std::string(e.what()) == "predict_min_distance: empty point cloud";
     }
-    std::printf("min %.9g idx %d | forward argmin %d %.9g | proxy %.9g | empty-cloud error %d\n", mn, idx, best,
-                static_cast<double>(d[best]), proxy(1), threw ? 1 : 0);
-    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw) ? 0 : 1;
+    // the same motion batch spread over "two GPUs" (device 0 twice: one worker thread each)
+    std::vector<float> pts, q01;
+    for (const Vec3& p : cloud)
+        for (double c : p) pts.push_back(static_cast<float>(c));
+    for (int j = 0; j < 3; ++j) {
+        for (double v : mo.q0) q01.push_back(static_cast<float>(v) + 0.1f * j);
+        for (double v : mo.q1) q01.push_back(static_cast<float>(v));
+    }
+    const svn_model_desc dd = prog.desc();
+    std::vector<float> params(static_cast<size_t>(svn_param_count(&dd)));
+    check(svn_init_params(&dd, 7, 0, params.data()));
+    MultiModel mg(prog, params, {0, 0});
+    const MinResult r = mg.query_min(pts, q01, 0.02, Precision::FP32_EXACT, Shard::MOTIONS);
+    const bool multi_ok = mg.devices() == 2 && r.min.size() == 3 && static_cast<double>(r.min[0]) == mn && r.argmin[0] == idx;
+    std::printf("min %.9g idx %d | forward argmin %d %.9g | proxy %.9g | empty-cloud error %d | multi %.9g %d\n", mn,
+                idx, best, static_cast<double>(d[best]), proxy(1), threw ? 1 : 0, static_cast<double>(r.min[0]),
+                multi_ok ? 1 : 0);
+    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw && multi_ok) ? 0 : 1;
 }
