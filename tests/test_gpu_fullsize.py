@@ -1,0 +1,142 @@
+"""Parity at BASELINE.json's full sizes, through properties that do not depend on size.
+
+The small-case tests compare every per-point delta with the oracle; at the full configs that
+is hours of CPU work (c3 is 247 TFLOP), so here the GPU result of the whole workload is
+checked through:
+  - c2 (64 x 16384, the FP32 path): the complete oracle run, bit for bit (0.4 TFLOP of CPU work);
+  - batch invariance: a slice of the motions evaluated alone gives the same bits
+    as the same motions inside the full launch;
+  - point-shard invariance: the cloud cut into chunks, keys folded per chunk and combined,
+    equals the one-launch result bit for bit (the multi-GPU point-sharding identity);
+  - full-cloud oracle on a few motions (point chunks on all host cores): per-motion min within
+    the stated bound, class equal outside the ambiguous band, argmin within the bound;
+  - a lower-bound property over every motion: min_gpu[m] <= delta_oracle(m, p) + bound for
+    thousands of random (motion, point) pairs drawn from the whole workload.
+"""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2402_15281_b200 as S
+from oracle import oracle as O
+from paper_2402_15281_b200.workloads import WORKLOADS
+from test_gpu_parity import BF16_BOUND
+
+pytestmark = pytest.mark.gpu
+CORES = os.cpu_count() or 1
+
+
+def _oracle_min_one_motion(program, params, pts, q_row, margin):
+    """The oracle's predict_min_distance of one motion over the whole cloud, the cloud split
+    into chunks on all host cores; lowest index on ties (nn.cpp:476-478: strict <)."""
+    chunks = np.array_split(np.arange(pts.shape[0]), CORES)
+
+    def run(idx):
+        mn, am, _, _ = O.query_min(program, params, pts[idx], q_row[None, :], margin)
+        return float(mn[0]), int(idx[0] + am[0])
+
+    with ThreadPoolExecutor(CORES) as ex:
+        parts = list(ex.map(run, [c for c in chunks if c.size]))
+    best = parts[0]
+    for p in parts[1:]:
+        if p[0] < best[0]:
+            best = p
+    return best
+
+
+def test_c2_full_size_bit_identical():
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 0, w.bound)
+    pts, q = w.make(seed=0)
+    assert q.shape[0] == w.motions and pts.shape[0] == w.points
+    r = S.Model(w.program, params).query_min(pts, q, w.margin, precision="fp32")
+    omin, oarg, ofree, _ = O.query_min(w.program, params, pts, q, w.margin, threads=CORES)
+    assert np.array_equal(r.min, omin) and np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
+
+
+@pytest.mark.parametrize("key", ["c3", "c4", "c5"])
+def test_full_size_bf16_properties(key):
+    w = WORKLOADS[key]
+    params = S.init_params(w.program, 0, w.bound)
+    pts, q = w.make(seed=0)
+    M, P = q.shape[0], pts.shape[0]
+    assert M == w.motions and P == w.points
+    model = S.Model(w.program, params)
+    r = model.query_min(pts, q, w.margin, precision="bf16")
+    bound = BF16_BOUND[w.program.name]
+    assert np.isfinite(r.min).all() and (r.argmin >= 0).all() and (r.argmin < P).all()
+
+    # batch invariance: motions evaluated alone == the same motions inside the full launch
+    for a, b in ((0, 1), (M // 2, M // 2 + 37), (M - 5, M)):
+        s = model.query_min(pts, q[a:b], w.margin, precision="bf16")
+        assert np.array_equal(s.min, r.min[a:b]) and np.array_equal(s.argmin, r.argmin[a:b])
+        assert np.array_equal(s.free, r.free[a:b])
+
+    # point-shard invariance over the full cloud (the multi-GPU point-sharding identity)
+    dev = torch.device("cuda:0")
+    tq = torch.from_numpy(q).to(dev)
+    keys = torch.empty(M, dtype=torch.int64, device=dev)
+    S.keys_init_device(keys)
+    cuts = [0, P // 3 + 17, (2 * P) // 3 - 5, P]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        model.query_keys_device(torch.from_numpy(pts[a:b]).to(dev), a, tq, keys, precision="bf16")
+    mn = torch.empty(M, dtype=torch.float32, device=dev)
+    am = torch.empty(M, dtype=torch.int32, device=dev)
+    fr = torch.empty(M, dtype=torch.uint8, device=dev)
+    S.keys_finalize_device(keys, w.margin, mn, am, fr)
+    torch.cuda.synchronize()
+    assert np.array_equal(mn.cpu().numpy(), r.min) and np.array_equal(am.cpu().numpy(), r.argmin)
+    assert np.array_equal(fr.cpu().numpy().astype(bool), r.free)
+
+    # full-cloud oracle on a few motions
+    rng = np.random.default_rng(1)
+    for m in rng.choice(M, size=2, replace=False):
+        omin, oarg = _oracle_min_one_motion(w.program, params, pts, q[m], w.margin)
+        assert abs(float(r.min[m]) - omin) <= bound, (m, r.min[m], omin)
+        if abs(omin - w.margin) > bound:
+            assert bool(r.free[m]) == (omin > w.margin)
+        d_at = O.forward_eval(w.program, params, np.concatenate([pts[r.argmin[m]], q[m]])[None, :])[0]
+        assert r.argmin[m] == oarg or float(d_at) - omin <= bound
+
+    # lower bound over the whole workload: min_gpu[m] <= delta_oracle(m, p) + bound
+    n = 4000
+    ms, ps = rng.integers(0, M, n), rng.integers(0, P, n)
+    raw = np.concatenate([pts[ps], q[ms]], axis=1).astype(np.float32)
+    order = np.argsort(ms, kind="stable")  # rows grouped by motion (forward_eval segments)
+    d = np.empty(n, np.float32)
+    d[order] = O.forward_eval(w.program, params, raw[order])
+    assert np.all(r.min[ms].astype(np.float64) <= d.astype(np.float64) + bound)
+
+
+def test_c5single_full_size_point_shards():
+    """1 motion x 2^24 points (the point-sharded multi-GPU case): 8 point chunks folded into
+    one key equal the single launch, and a sampled lower bound holds."""
+    w = WORKLOADS["c5single"]
+    params = S.init_params(w.program, 0, w.bound)
+    pts, q = w.make(seed=0)
+    P = pts.shape[0]
+    assert P == w.points and q.shape[0] == 1
+    model = S.Model(w.program, params)
+    r = model.query_min(pts, q, w.margin, precision="bf16")
+    dev = torch.device("cuda:0")
+    tq = torch.from_numpy(q).to(dev)
+    tp = torch.from_numpy(pts).to(dev)
+    keys = torch.empty(1, dtype=torch.int64, device=dev)
+    S.keys_init_device(keys)
+    cuts = [i * P // 8 for i in range(9)]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        model.query_keys_device(tp[a:b], a, tq, keys, precision="bf16")
+    mn = torch.empty(1, dtype=torch.float32, device=dev)
+    am = torch.empty(1, dtype=torch.int32, device=dev)
+    fr = torch.empty(1, dtype=torch.uint8, device=dev)
+    S.keys_finalize_device(keys, w.margin, mn, am, fr)
+    torch.cuda.synchronize()
+    assert mn.item() == r.min[0] and am.item() == r.argmin[0] and bool(fr.item()) == bool(r.free[0])
+    bound = BF16_BOUND[w.program.name]
+    ps = np.random.default_rng(2).integers(0, P, 2000)
+    raw = np.concatenate([pts[ps], np.repeat(q, ps.size, axis=0)], axis=1).astype(np.float32)
+    d = O.forward_eval(w.program, params, raw)
+    assert np.all(float(r.min[0]) <= d.astype(np.float64) + bound)
