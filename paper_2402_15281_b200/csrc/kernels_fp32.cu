@@ -131,7 +131,7 @@ struct Fp32Cfg {
     static constexpr int ACT_ROWS = N + kMaxIn;   // h rows then z rows
     static constexpr size_t ACT_BYTES = static_cast<size_t>(ACT_ROWS) * TM * 4;
     static constexpr size_t STAGE_BYTES = static_cast<size_t>(KS) * N * 4;
-    static constexpr size_t SMEM = ACT_BYTES + STAGES * STAGE_BYTES + 64;
+    static constexpr size_t SMEM = ACT_BYTES + STAGES * STAGE_BYTES + 64 + N * 4;  // + w_o
 };
 
 struct ChunkIter {
@@ -152,9 +152,20 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
     float* actT = reinterpret_cast<float*>(smem);
     float* wst = reinterpret_cast<float*>(smem + C::ACT_BYTES);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::ACT_BYTES + C::STAGES * C::STAGE_BYTES);
+    float* wo_s = reinterpret_cast<float*>(smem + C::ACT_BYTES + C::STAGES * C::STAGE_BYTES + 64);
 
     const int tid = threadIdx.x;
     const int cg = tid % CG, rg = tid / CG;
+    // actT[k][row]: at width <= 256 the 16-byte chunks of row k are XOR-swizzled by
+    // (k / 4) mod 8, so the epilogue's float4 stores (lanes of a warp 4 columns = 4 rows of
+    // actT apart) hit 8 distinct bank groups instead of one (c2 +2.4 %); the k loop's loads
+    // are warp broadcasts either way, and with 32-row weight chunks the XOR folds into the
+    // unrolled k loop's constant offsets.  At width 512 (16-row chunks) it does not fold and
+    // costs more than the conflicts (-7 %), so that layout stays plain.
+    constexpr bool kSwizzle = N <= 256;
+    auto act_at = [&](int k, int r) {
+        return actT + k * C::TM + (kSwizzle ? (r ^ (((k >> 2) & 7) << 2)) : r);
+    };
     const int L = a.L;
 
     // chunks per tile
@@ -164,6 +175,7 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
     if (blockIdx.x < a.n_tiles) my_tiles = (a.n_tiles - 1 - blockIdx.x) / gridDim.x + 1;
     const int64_t total_chunks = my_tiles * chunks_per_tile;
 
+    for (int k = tid; k < N; k += C::THREADS) wo_s[k] = a.wo[k];
     if (tid == 0) {
         for (int s = 0; s < C::STAGES; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
@@ -206,11 +218,11 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
             const float* xp = a.points + pr * a.point_stride;
 #pragma unroll
             for (int k = 0; k < 3; ++k)
-                actT[(N + k) * C::TM + tid] = __fmul_rn(__fsub_rn(xp[k], a.shift[k]), a.scale[k]);
+                *act_at(N + k, tid) = __fmul_rn(__fsub_rn(xp[k], a.shift[k]), a.scale[k]);
             if (a.exact) {
                 const float* q = a.q01 + static_cast<int64_t>(motion) * 2 * a.dof;
                 for (int k = 0; k < 2 * a.dof; ++k)
-                    actT[(N + 3 + k) * C::TM + tid] = __fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]);
+                    *act_at(N + 3 + k, tid) = __fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]);
             }
         }
         __syncthreads();
@@ -241,9 +253,8 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                 const float* w = wst + static_cast<size_t>(s) * C::KS * N;
                 const int nk = rows - r0 < C::KS ? rows - r0 : C::KS;
                 auto kstep = [&](int kk) {
-                    const float* arow = actT + (a_off + r0 + kk) * C::TM + rg * 8;
-                    const float4 a0 = *reinterpret_cast<const float4*>(arow);
-                    const float4 a1 = *reinterpret_cast<const float4*>(arow + 4);
+                    const float4 a0 = *reinterpret_cast<const float4*>(act_at(a_off + r0 + kk, rg * 8));
+                    const float4 a1 = *reinterpret_cast<const float4*>(act_at(a_off + r0 + kk, rg * 8 + 4));
                     const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
                     float wv[C::NC];
 #pragma unroll
@@ -280,11 +291,12 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                 for (int jj = 0; jj < 4; ++jj) {
                     const int col = cg * 4 + j4 * CG * 4 + jj;
                     const float sv = aff ? ld.s[col] : 0.f, tv = aff ? ld.t[col] : 0.f;
-                    float* hrow = actT + col * C::TM + rg * 8;
+                    float* hlo = act_at(col, rg * 8);
+                    float* hhi = act_at(col, rg * 8 + 4);
                     float hv[8];
                     if (res) {
-                        const float4 h0 = *reinterpret_cast<const float4*>(hrow);
-                        const float4 h1 = *reinterpret_cast<const float4*>(hrow + 4);
+                        const float4 h0 = *reinterpret_cast<const float4*>(hlo);
+                        const float4 h1 = *reinterpret_cast<const float4*>(hhi);
                         hv[0] = h0.x, hv[1] = h0.y, hv[2] = h0.z, hv[3] = h0.w;
                         hv[4] = h1.x, hv[5] = h1.y, hv[6] = h1.z, hv[7] = h1.w;
                     }
@@ -295,8 +307,8 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                         if (aff) r = __fmaf_rn(r, sv, tv);
                         hv[i] = res ? __fadd_rn(hv[i], r) : r;
                     }
-                    *reinterpret_cast<float4*>(hrow) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-                    *reinterpret_cast<float4*>(hrow + 4) = make_float4(hv[4], hv[5], hv[6], hv[7]);
+                    *reinterpret_cast<float4*>(hlo) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+                    *reinterpret_cast<float4*>(hhi) = make_float4(hv[4], hv[5], hv[6], hv[7]);
                 }
             }
             __syncthreads();
@@ -305,7 +317,9 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
         // output layer: delta = sum_k w_o[k] h[k] (sequential fmaf) + b_o; min/argmin
         if (tid < C::TM) {
             float acc = 0.f;
-            for (int k = 0; k < N; ++k) acc = __fmaf_rn(a.wo[k], actT[k * C::TM + tid], acc);
+            // one k-ordered chain; unrolled so the shared loads run ahead of the FMAs
+#pragma unroll 16
+            for (int k = 0; k < N; ++k) acc = __fmaf_rn(wo_s[k], *act_at(k, tid), acc);
             const float delta = __fadd_rn(acc, a.bo);
             const bool valid = tid < nrows;
             if (valid && a.per_point) a.per_point[obase + tid] = delta;
