@@ -207,6 +207,9 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
         while (g_prod < total_chunks && g_prod < C::STAGES) issue();
 
     int64_t g = 0;  // consumer chunk counter
+    // phase accounting of thread 0 (SVN_KERNEL_PROF builds, scripts/fp32prof.py; zero otherwise)
+    unsigned long long t_full = 0, t_bar = 0, t_epi = 0, t_out = 0;
+    const unsigned long long t_start = prof_clock();
     for (int64_t t = blockIdx.x; t < a.n_tiles; t += gridDim.x) {
         int32_t motion, nrows;
         int64_t pbase, obase;
@@ -249,7 +252,9 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
             const int a_off = (l == 0) ? N : 0;
             for (int r0 = 0; r0 < rows; r0 += C::KS) {
                 const int s = static_cast<int>(g % C::STAGES);
+                const unsigned long long w0 = prof_clock();
                 mbar_wait(&full[s], static_cast<uint32_t>((g / C::STAGES) & 1));
+                t_full += prof_clock() - w0;
                 const float* w = wst + static_cast<size_t>(s) * C::KS * N;
                 const int nk = rows - r0 < C::KS ? rows - r0 : C::KS;
                 auto kstep = [&](int kk) {
@@ -278,10 +283,13 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                 } else {
                     for (int kk = 0; kk < nk; ++kk) kstep(kk);
                 }
+                const unsigned long long b0 = prof_clock();
                 __syncthreads();  // every thread is done with stage s
+                t_bar += prof_clock() - b0;
                 if (tid == 0 && g_prod < total_chunks) issue();
                 ++g;
             }
+            const unsigned long long e0 = prof_clock();
             // epilogue: activation / folded BN / residual, written back in place
             const int fl = ld.flags;
             const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
@@ -312,7 +320,9 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                 }
             }
             __syncthreads();
+            t_epi += prof_clock() - e0;
         }
+        const unsigned long long o0 = prof_clock();
 
         // output layer: delta = sum_k w_o[k] h[k] (sequential fmaf) + b_o; min/argmin
         if (tid < C::TM) {
@@ -331,6 +341,14 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
         }
         __syncthreads();
         if (tid == 0 && a.keys) tile_done(a, motion);
+        t_out += prof_clock() - o0;
+    }
+    if (a.prof && tid == 0) {  // slots: total, weight wait, chunk barrier, epilogue, output layer
+        atomicAdd(a.prof + 0, prof_clock() - t_start);
+        atomicAdd(a.prof + 1, t_full);
+        atomicAdd(a.prof + 2, t_bar);
+        atomicAdd(a.prof + 3, t_epi);
+        atomicAdd(a.prof + 4, t_out);
     }
 }
 

@@ -1,7 +1,8 @@
-"""Print the FP32 kernel phase counters (scripts/ab/fp32_prof.cu build, SVN_PROF=1 run)."""
+"""Print the FP32 kernel's phase split (thread 0 of every CTA, summed): run bench.py with
+SVN_PROF=1 on a library built with SVN_NVCC_DEFINES=SVN_KERNEL_PROF (scripts/build_variant.py)."""
 import sys
 line = [l for l in open(sys.argv[1]) if 'svn prof' in l][-1]
 v = [int(x) for x in line.split(']')[1].split()]
-for o, who in ((0, "thread 0"), (8, "thread 160")):
-    tot = v[o] or 1
-    print(who, " ".join(f"{n} {v[o + i] / tot * 100:5.1f}%" for i, n in enumerate(["total", "wait_full", "barrier", "epilogue+last_sync", "output"])))
+tot = v[0] or 1
+print(" ".join(f"{n} {v[i] / tot * 100:5.1f}%" for i, n in
+               enumerate(["total", "weight_wait", "chunk_barrier", "epilogue", "output_layer"])))
