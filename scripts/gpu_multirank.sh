@@ -11,3 +11,8 @@ tail -1 gpurun_out/mr_point.log | cut -c1-600
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29535 \
   bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > gpurun_out/mr_ref.log 2>&1; echo "reference rc=$?"
 tail -1 gpurun_out/mr_ref.log | cut -c1-300
+# the driver's own launch line at N=1 (NCCL, device_id from LOCAL_RANK)
+unset SVN_BENCH_BACKEND SVN_BENCH_DEVICE
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29536 \
+  bench.py --gpus 1 --steps 2 --warmup 3 > gpurun_out/mr_nccl1.log 2>&1; echo "nccl N=1 rc=$?"
+tail -1 gpurun_out/mr_nccl1.log | cut -c1-300
