@@ -54,7 +54,8 @@ typedef enum {
     SVN_ERR_FORMAT = 6,      /* FormatError      errors.hpp:13 */
     SVN_ERR_TRUNCATION = 7,  /* TruncationError  errors.hpp:18 */
     SVN_ERR_VERSION = 8,     /* VersionError     errors.hpp:23 */
-    SVN_ERR_NCCL = 9         /* NCCL communicator / collective failure (multi-GPU) */
+    SVN_ERR_NCCL = 9,        /* NCCL communicator / collective failure (multi-GPU) */
+    SVN_ERR_HOST = 10        /* other host-side failure (e.g. a worker thread could not start) */
 } svn_status;
 
 /* Arithmetic of the fused MLP kernel.

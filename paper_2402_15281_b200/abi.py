@@ -15,7 +15,7 @@ from . import build as _build
 LIB_PATH = _build.LIB
 
 # svn_status
-OK, INVALID_ARGUMENT, CUDA_ERROR, OUT_OF_MEMORY, UNSUPPORTED, IO, FORMAT, TRUNCATION, VERSION, NCCL_ERROR = range(10)
+OK, INVALID_ARGUMENT, CUDA_ERROR, OUT_OF_MEMORY, UNSUPPORTED, IO, FORMAT, TRUNCATION, VERSION, NCCL_ERROR, HOST_ERROR = range(11)
 SHARD_MODES = {"auto": 0, "motions": 1, "points": 2}
 # svn_precision
 PREC_BF16, PREC_FP32, PREC_FP32_EXACT, PREC_FP32_SPLIT = 0, 1, 2, 3

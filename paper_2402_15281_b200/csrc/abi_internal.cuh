@@ -41,6 +41,7 @@ extern thread_local unsigned long long g_prof[kProfSlots];
 bool prof_enabled();
 svn_status fail(svn_status code, const std::string& msg);
 svn_status cuda_fail(cudaError_t e, const char* what);
+svn_status host_exception();  // call from a catch (...) block
 
 #define SVN_CUDA(call, what)                       \
     do {                                           \

@@ -34,6 +34,20 @@ svn_status cuda_fail(cudaError_t e, const char* what) {
     return fail(code, std::string("CUDA error in ") + what + ": " + cudaGetErrorName(e) + ": " + cudaGetErrorString(e));
 }
 
+// Every C-ABI entry point catches what its C++ body may throw (host allocations, worker
+// threads) and reports it as a status: no exception crosses the C boundary.
+svn_status host_exception() {
+    try {
+        throw;
+    } catch (const std::bad_alloc&) {
+        return fail(SVN_ERR_OUT_OF_MEMORY, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(SVN_ERR_HOST, std::string("host error: ") + e.what());
+    } catch (...) {
+        return fail(SVN_ERR_HOST, "host error");
+    }
+}
+
 int layer_k(const svn_layer* layers, int l, int N, int in) {
     if (l == 0) return in;
     return N + (layers[l].concat ? in : 0);
@@ -158,20 +172,24 @@ SVN_API void svn_kernel_timing_begin(void) {
 }
 
 SVN_API svn_status svn_kernel_timing_end(double* total_ms, int64_t* launches) {
-    g_timing = false;
-    double sum = 0.0;
-    for (auto& ev : g_events) {
-        SVN_CUDA(cudaEventSynchronize(ev.second), "cudaEventSynchronize");
-        float ms = 0.f;
-        SVN_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second), "cudaEventElapsedTime");
-        sum += ms;
-        cudaEventDestroy(ev.first);
-        cudaEventDestroy(ev.second);
+    try {
+        g_timing = false;
+        double sum = 0.0;
+        for (auto& ev : g_events) {
+            SVN_CUDA(cudaEventSynchronize(ev.second), "cudaEventSynchronize");
+            float ms = 0.f;
+            SVN_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second), "cudaEventElapsedTime");
+            sum += ms;
+            cudaEventDestroy(ev.first);
+            cudaEventDestroy(ev.second);
+        }
+        if (total_ms) *total_ms = sum;
+        if (launches) *launches = static_cast<int64_t>(g_events.size());
+        g_events.clear();
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    if (total_ms) *total_ms = sum;
-    if (launches) *launches = static_cast<int64_t>(g_events.size());
-    g_events.clear();
-    return SVN_OK;
 }
 
 SVN_API int64_t svn_param_count(const svn_model_desc* d) {
@@ -200,321 +218,333 @@ SVN_API int64_t svn_trainable_param_count(const svn_model_desc* d) {
 // hidden W's, output W; each drawn row-major over [out x in] (nn.cpp:70-71) with
 // Rng::uniform (rng.hpp:21-23) and stored column-major.
 SVN_API svn_status svn_init_params(const svn_model_desc* d, uint64_t seed, int32_t bound_mode, float* p) {
-    svn_status st = validate_desc(d);
-    if (st != SVN_OK) return st;
-    if (!p) return fail(SVN_ERR_INVALID_ARGUMENT, "init_params: null output");
-    const int N = d->width, in = 3 + 2 * d->dof;
-    std::mt19937_64 eng(seed);
-    auto uniform = [&](double lo, double hi) {
-        const double u = static_cast<double>(eng() >> 11) * 0x1.0p-53;
-        return std::fma(hi - lo, u, lo);
-    };
-    float* q = p;
-    for (int i = 0; i < in; ++i) *q++ = 0.0f;
-    for (int i = 0; i < in; ++i) *q++ = 1.0f;
-    for (int l = 0; l < d->n_layers; ++l) {
-        const int K = layer_k(d->layers, l, N, in);
-        const double bound = bound_mode ? std::sqrt(6.0 / K) : 1.0 / std::sqrt(static_cast<double>(K));
-        for (int r = 0; r < N; ++r)
-            for (int c = 0; c < K; ++c) q[static_cast<int64_t>(c) * N + r] = static_cast<float>(uniform(-bound, bound));
-        q += static_cast<int64_t>(N) * K;
-        for (int i = 0; i < N; ++i) *q++ = 0.0f;
-        if (d->layers[l].affine) {
-            for (int i = 0; i < N; ++i) *q++ = 1.0f;
+    try {
+        svn_status st = validate_desc(d);
+        if (st != SVN_OK) return st;
+        if (!p) return fail(SVN_ERR_INVALID_ARGUMENT, "init_params: null output");
+        const int N = d->width, in = 3 + 2 * d->dof;
+        std::mt19937_64 eng(seed);
+        auto uniform = [&](double lo, double hi) {
+            const double u = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+            return std::fma(hi - lo, u, lo);
+        };
+        float* q = p;
+        for (int i = 0; i < in; ++i) *q++ = 0.0f;
+        for (int i = 0; i < in; ++i) *q++ = 1.0f;
+        for (int l = 0; l < d->n_layers; ++l) {
+            const int K = layer_k(d->layers, l, N, in);
+            const double bound = bound_mode ? std::sqrt(6.0 / K) : 1.0 / std::sqrt(static_cast<double>(K));
+            for (int r = 0; r < N; ++r)
+                for (int c = 0; c < K; ++c) q[static_cast<int64_t>(c) * N + r] = static_cast<float>(uniform(-bound, bound));
+            q += static_cast<int64_t>(N) * K;
             for (int i = 0; i < N; ++i) *q++ = 0.0f;
-            for (int i = 0; i < N; ++i) *q++ = 0.0f;
-            for (int i = 0; i < N; ++i) *q++ = 1.0f;
+            if (d->layers[l].affine) {
+                for (int i = 0; i < N; ++i) *q++ = 1.0f;
+                for (int i = 0; i < N; ++i) *q++ = 0.0f;
+                for (int i = 0; i < N; ++i) *q++ = 0.0f;
+                for (int i = 0; i < N; ++i) *q++ = 1.0f;
+            }
         }
+        const double bound = bound_mode ? std::sqrt(6.0 / N) : 1.0 / std::sqrt(static_cast<double>(N));
+        for (int c = 0; c < N; ++c) *q++ = static_cast<float>(uniform(-bound, bound));
+        *q = 0.0f;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    const double bound = bound_mode ? std::sqrt(6.0 / N) : 1.0 / std::sqrt(static_cast<double>(N));
-    for (int c = 0; c < N; ++c) *q++ = static_cast<float>(uniform(-bound, bound));
-    *q = 0.0f;
-    return SVN_OK;
 }
 
 SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params, int64_t n_params, int32_t device,
                                     svn_model** out) {
-    svn_status st = validate_desc(d);
-    if (st != SVN_OK) return st;
-    if (!params || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "model: null params/out");
-    if (n_params != svn_param_count(d)) return fail(SVN_ERR_INVALID_ARGUMENT, "model: parameter count mismatch");
-    int ndev = 0;
-    SVN_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
-    if (device < 0 || device >= ndev) return fail(SVN_ERR_INVALID_ARGUMENT, "model: no such CUDA device");
-    DeviceGuard guard(device);
+    try {
+        svn_status st = validate_desc(d);
+        if (st != SVN_OK) return st;
+        if (!params || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "model: null params/out");
+        if (n_params != svn_param_count(d)) return fail(SVN_ERR_INVALID_ARGUMENT, "model: parameter count mismatch");
+        int ndev = 0;
+        SVN_CUDA(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) return fail(SVN_ERR_INVALID_ARGUMENT, "model: no such CUDA device");
+        DeviceGuard guard(device);
 
-    auto m = new svn_model();
-    m->device = device;
-    m->L = d->n_layers;
-    m->N = d->width;
-    m->dof = d->dof;
-    m->in = 3 + 2 * d->dof;
-    m->layers.assign(d->layers, d->layers + d->n_layers);
-    cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
-    const int N = m->N, in = m->in, L = m->L, nq = 2 * m->dof;
-    FusedArgs& a = m->base;
-    a.L = L;
-    a.N = N;
-    a.dof = m->dof;
-    a.in = in;
+        auto m = new svn_model();
+        m->device = device;
+        m->L = d->n_layers;
+        m->N = d->width;
+        m->dof = d->dof;
+        m->in = 3 + 2 * d->dof;
+        m->layers.assign(d->layers, d->layers + d->n_layers);
+        cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, device);
+        const int N = m->N, in = m->in, L = m->L, nq = 2 * m->dof;
+        FusedArgs& a = m->base;
+        a.L = L;
+        a.N = N;
+        a.dof = m->dof;
+        a.in = in;
 
-    // parse the parameter buffer (layout: include/sweptnet_b200.h)
-    const float* q = params;
-    for (int k = 0; k < in; ++k) a.shift[k] = q[k];
-    q += in;
-    for (int k = 0; k < in; ++k) a.scale[k] = q[k];
-    q += in;
-    std::vector<float> wq_host, mbbase_host, wx_host;
-    auto cleanup_fail = [&](svn_status s) {
-        delete m;
-        return s;
-    };
-    for (int l = 0; l < L; ++l) {
-        const svn_layer& ly = m->layers[l];
-        const int K = layer_k(d->layers, l, N, in);
-        const float* W = q;  // column-major [N x K]: column k contiguous == row k of W^T
-        q += static_cast<int64_t>(N) * K;
-        const float* b = q;
-        q += N;
-        LayerDev& ld = a.layer[l];
-        ld.flags = (ly.concat || l == 0 ? kConcat : 0) | (ly.act ? kAct : 0) | (ly.affine ? kAffine : 0) |
-                   (ly.residual && l > 0 ? kResidual : 0);
-        float* dW = nullptr;
-        if ((st = m->upload(W, static_cast<size_t>(N) * K, &dW)) != SVN_OK) return cleanup_fail(st);
-        a.wt[l] = dW;
-        a.wt_rows[l] = K;
-        float* db = nullptr;
-        if ((st = m->upload(b, N, &db)) != SVN_OK) return cleanup_fail(st);
-        ld.bias = db;
-        ld.mb_slot = -1;
-        ld.bias_zero = 1;
-        for (int i = 0; i < N; ++i)
-            if (b[i] != 0.0f) ld.bias_zero = 0;
-        ld.wx = nullptr;
-        if (ld.flags & kConcat) {
-            const int xoff = (l == 0) ? 0 : N;
-            ld.wx = dW + static_cast<int64_t>(xoff) * N;  // rows x0, x1, x2 of W^T
-            ld.mb_slot = m->n_mb++;
-            ld.bias_zero = 0;
-            wq_host.insert(wq_host.end(), W + static_cast<int64_t>(xoff + 3) * N,
-                           W + static_cast<int64_t>(xoff + 3 + nq) * N);
-            wx_host.insert(wx_host.end(), W + static_cast<int64_t>(xoff) * N, W + static_cast<int64_t>(xoff + 3) * N);
-            mbbase_host.insert(mbbase_host.end(), b, b + N);
-        }
-        ld.s = ld.t = nullptr;
-        if (ly.affine) {
-            const float *gamma = q, *beta = q + N, *mean = q + 2 * N, *var = q + 3 * N;
-            q += 4 * N;
-            // nn.cpp:108-110 in float: s = gamma / sqrt(var + eps); t = beta - mean * s
-            std::vector<float> s(N), t(N);
-            for (int i = 0; i < N; ++i) {
-                s[i] = gamma[i] / std::sqrt(var[i] + 1e-5f);
-                t[i] = std::fma(-mean[i], s[i], beta[i]);
-            }
-            float *ds = nullptr, *dt = nullptr;
-            if ((st = m->upload(s.data(), N, &ds)) != SVN_OK) return cleanup_fail(st);
-            if ((st = m->upload(t.data(), N, &dt)) != SVN_OK) return cleanup_fail(st);
-            ld.s = ds;
-            ld.t = dt;
-        }
-    }
-    {
-        float* dwo = nullptr;
-        if ((st = m->upload(q, N, &dwo)) != SVN_OK) return cleanup_fail(st);
-        a.wo = dwo;
-        a.bo = q[N];
-    }
-    if ((st = m->upload(wq_host.data(), wq_host.size(), &m->d_wq)) != SVN_OK) return cleanup_fail(st);
-    if ((st = m->upload(mbbase_host.data(), mbbase_host.size(), &m->d_mbbase)) != SVN_OK) return cleanup_fail(st);
-    if ((st = m->upload(wx_host.data(), wx_host.size(), &m->d_wxslots)) != SVN_OK) return cleanup_fail(st);
-    a.n_mb = m->n_mb;
-
-    // bf16 tcgen05 weight stream for layers 1..L-1: h part only, per layer the
-    // quarter-steps (n-half, k-half) = (0,0) (1,0) (0,1) (1,1), each as K/2/64 chunks
-    // of (N/2 rows x 64 k) in the SW128 K-major image the MMA descriptors expect.
-    if (N == 256 || N == 512) {
-        const int NH = N / 2, KSL = NH / 64;
-        const size_t chunk_elems = static_cast<size_t>(NH) * 64;
-        std::vector<char> folded;
-        const std::vector<float> pbf = fold_affine_bf16(d, params, n_params, folded);
-        std::vector<__nv_bfloat16> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * N * N);
-        const float* Wl = pbf.data() + 2 * in;
-        size_t pos = 0;
+        // parse the parameter buffer (layout: include/sweptnet_b200.h)
+        const float* q = params;
+        for (int k = 0; k < in; ++k) a.shift[k] = q[k];
+        q += in;
+        for (int k = 0; k < in; ++k) a.scale[k] = q[k];
+        q += in;
+        std::vector<float> wq_host, mbbase_host, wx_host;
+        auto cleanup_fail = [&](svn_status s) {
+            delete m;
+            return s;
+        };
         for (int l = 0; l < L; ++l) {
+            const svn_layer& ly = m->layers[l];
             const int K = layer_k(d->layers, l, N, in);
-            if (l > 0 && N == 256) {
-                // ping-pong kernel (width 256): per layer 4 K slabs, each [CTA r: 128 rows] x 64 k
-                for (int ks = 0; ks < N / 64; ++ks)
-                    for (int r = 0; r < 2; ++r) {
-                        uint8_t* blob = reinterpret_cast<uint8_t*>(ws.data() + pos);
-                        for (int nr = 0; nr < 128; ++nr)
-                            for (int kc = 0; kc < 64; ++kc) {
-                                const int n = r * 128 + nr, k = ks * 64 + kc;
-                                *reinterpret_cast<__nv_bfloat16*>(blob + sw128_offset(nr, kc, 128)) =
-                                    __float2bfloat16_rn(Wl[static_cast<int64_t>(k) * N + n]);
-                            }
-                        pos += 128 * 64;
-                    }
-            } else if (l > 0) {
-                for (int step = 0; step < 4; ++step) {
-                    const int nh = step & 1, kh = step >> 1;
-                    for (int ks = 0; ks < KSL; ++ks) {
-                        uint8_t* chunk = reinterpret_cast<uint8_t*>(ws.data() + pos);
-                        for (int nr = 0; nr < NH; ++nr)
-                            for (int kc = 0; kc < 64; ++kc) {
-                                const int n = nh * NH + nr, k = (kh * KSL + ks) * 64 + kc;
-                                const float w = Wl[static_cast<int64_t>(k) * N + n];
-                                *reinterpret_cast<__nv_bfloat16*>(chunk + sw128_offset(nr, kc, NH)) =
-                                    __float2bfloat16_rn(w);
-                            }
-                        pos += chunk_elems;
-                    }
-                }
-            }
-            Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
-        }
-        __nv_bfloat16* dws = nullptr;
-        if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return cleanup_fail(st);
-        a.wstream = dws;
-        // CTA-pair kernel: TMA views of the weight stream and of the model-constant
-        // K=16 extension rows (bias hi/lo of non-concat layers with a nonzero bias).
-        const int BR = N == 256 ? N / 2 : N / 4;  // B rows per CTA per TMA box (128 for both kernels)
-        if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return cleanup_fail(st);
-        std::vector<uint8_t> xm;
-        const float* Wb = pbf.data() + 2 * in;
-        std::vector<float> wq_bf, mbbase_bf, wx_bf;  // K0 inputs from the folded parameters
-        for (int l = 0; l < L; ++l) {
-            const int K = layer_k(d->layers, l, N, in);
-            const float* Wfull = Wb;
-            const float* b = Wb + static_cast<int64_t>(N) * K;
+            const float* W = q;  // column-major [N x K]: column k contiguous == row k of W^T
+            q += static_cast<int64_t>(N) * K;
+            const float* b = q;
+            q += N;
             LayerDev& ld = a.layer[l];
-            ld.ext = 0;
-            ld.ext_row = 0;
-            bool bias_zero = true;
-            for (int n = 0; n < N; ++n)
-                if (b[n] != 0.0f) bias_zero = false;
-            if (ld.mb_slot >= 0) {
-                ld.ext = 2;
+            ld.flags = (ly.concat || l == 0 ? kConcat : 0) | (ly.act ? kAct : 0) | (ly.affine ? kAffine : 0) |
+                       (ly.residual && l > 0 ? kResidual : 0);
+            float* dW = nullptr;
+            if ((st = m->upload(W, static_cast<size_t>(N) * K, &dW)) != SVN_OK) return cleanup_fail(st);
+            a.wt[l] = dW;
+            a.wt_rows[l] = K;
+            float* db = nullptr;
+            if ((st = m->upload(b, N, &db)) != SVN_OK) return cleanup_fail(st);
+            ld.bias = db;
+            ld.mb_slot = -1;
+            ld.bias_zero = 1;
+            for (int i = 0; i < N; ++i)
+                if (b[i] != 0.0f) ld.bias_zero = 0;
+            ld.wx = nullptr;
+            if (ld.flags & kConcat) {
                 const int xoff = (l == 0) ? 0 : N;
-                wq_bf.insert(wq_bf.end(), Wfull + static_cast<int64_t>(xoff + 3) * N,
-                             Wfull + static_cast<int64_t>(xoff + 3 + nq) * N);
-                wx_bf.insert(wx_bf.end(), Wfull + static_cast<int64_t>(xoff) * N, Wfull + static_cast<int64_t>(xoff + 3) * N);
-                mbbase_bf.insert(mbbase_bf.end(), b, b + N);
-            } else if (!bias_zero) {
-                ld.ext = 1;
-                ld.ext_row = static_cast<int64_t>(xm.size() / 32);
-                const size_t base = xm.size();
-                xm.resize(base + static_cast<size_t>(N) * 32, 0);
-                for (int n = 0; n < N; ++n) {
-                    int blob_i, rr;
-                    if (N == 256) {  // ping-pong layout: blobs [r] of N/2 rows
-                        blob_i = n / BR;
-                        rr = n % BR;
-                    } else {         // pair layout: blobs [n-half][r] of N/4 rows
-                        const int nh = n / (N / 2), wi = n % (N / 2);
-                        blob_i = nh * 2 + wi / BR;
-                        rr = wi % BR;
-                    }
-                    uint8_t* blob = xm.data() + base + static_cast<size_t>(blob_i * BR) * 32;
-                    __nv_bfloat16 hi, lo;
-                    split_bf16_host(b[n], hi, lo);
-                    *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 0)) = hi;
-                    *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 1)) = lo;
-                }
+                ld.wx = dW + static_cast<int64_t>(xoff) * N;  // rows x0, x1, x2 of W^T
+                ld.mb_slot = m->n_mb++;
+                ld.bias_zero = 0;
+                wq_host.insert(wq_host.end(), W + static_cast<int64_t>(xoff + 3) * N,
+                               W + static_cast<int64_t>(xoff + 3 + nq) * N);
+                wx_host.insert(wx_host.end(), W + static_cast<int64_t>(xoff) * N, W + static_cast<int64_t>(xoff + 3) * N);
+                mbbase_host.insert(mbbase_host.end(), b, b + N);
             }
-            Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+            ld.s = ld.t = nullptr;
+            if (ly.affine) {
+                const float *gamma = q, *beta = q + N, *mean = q + 2 * N, *var = q + 3 * N;
+                q += 4 * N;
+                // nn.cpp:108-110 in float: s = gamma / sqrt(var + eps); t = beta - mean * s
+                std::vector<float> s(N), t(N);
+                for (int i = 0; i < N; ++i) {
+                    s[i] = gamma[i] / std::sqrt(var[i] + 1e-5f);
+                    t[i] = std::fma(-mean[i], s[i], beta[i]);
+                }
+                float *ds = nullptr, *dt = nullptr;
+                if ((st = m->upload(s.data(), N, &ds)) != SVN_OK) return cleanup_fail(st);
+                if ((st = m->upload(t.data(), N, &dt)) != SVN_OK) return cleanup_fail(st);
+                ld.s = ds;
+                ld.t = dt;
+            }
         }
-        if (xm.empty()) xm.resize(static_cast<size_t>(BR) * 32, 0);
-        uint8_t* dxm = nullptr;
-        if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
-        if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return cleanup_fail(st);
-        if ((st = m->upload(wq_bf.data(), wq_bf.size(), &m->d_wq_bf)) != SVN_OK) return cleanup_fail(st);
-        if ((st = m->upload(mbbase_bf.data(), mbbase_bf.size(), &m->d_mbbase_bf)) != SVN_OK) return cleanup_fail(st);
-        if ((st = m->upload(wx_bf.data(), wx_bf.size(), &m->d_wxslots_bf)) != SVN_OK) return cleanup_fail(st);
-        m->base_bf16 = a;
-        for (int l = 0; l < L; ++l)
-            if (folded[static_cast<size_t>(l)]) m->base_bf16.layer[l].flags &= ~kAffine;
-        m->base_bf16.bo = pbf[static_cast<size_t>(n_params - 1)];
-        m->has_bf16 = true;
-    }
+        {
+            float* dwo = nullptr;
+            if ((st = m->upload(q, N, &dwo)) != SVN_OK) return cleanup_fail(st);
+            a.wo = dwo;
+            a.bo = q[N];
+        }
+        if ((st = m->upload(wq_host.data(), wq_host.size(), &m->d_wq)) != SVN_OK) return cleanup_fail(st);
+        if ((st = m->upload(mbbase_host.data(), mbbase_host.size(), &m->d_mbbase)) != SVN_OK) return cleanup_fail(st);
+        if ((st = m->upload(wx_host.data(), wx_host.size(), &m->d_wxslots)) != SVN_OK) return cleanup_fail(st);
+        a.n_mb = m->n_mb;
 
-    // fp32-accurate tensor-core path (width 256): every weight split into fp16 hi and
-    // 2^11-scaled lo' planes, per (layer, quarter step, 64-wide K slab, CTA half r) a
-    // [hi: 64 rows][lo': 64 rows] SW128 image; extension rows [main 64][corr 64] per
-    // (n-half, r).  Needs |W|, |b| well inside the fp16 range.
-    if (N == 256) {
-        float wmax = 0.f;
-        for (int64_t i = 2 * in; i < n_params; ++i) wmax = std::max(wmax, std::fabs(params[i]));
-        if (wmax < 1.0e4f) {
-            FusedArgs sa = a;
-            auto split_h = [](float x, __half& hi, __half& lo) {
-                hi = __float2half_rn(x);
-                lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
-            };
-            std::vector<uint8_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * 4 * 2 * 2 * 2 * 64 * 128);
-            uint8_t* out = ws.data();
-            const float* Wl = params + 2 * in;
+        // bf16 tcgen05 weight stream for layers 1..L-1: h part only, per layer the
+        // quarter-steps (n-half, k-half) = (0,0) (1,0) (0,1) (1,1), each as K/2/64 chunks
+        // of (N/2 rows x 64 k) in the SW128 K-major image the MMA descriptors expect.
+        if (N == 256 || N == 512) {
+            const int NH = N / 2, KSL = NH / 64;
+            const size_t chunk_elems = static_cast<size_t>(NH) * 64;
+            std::vector<char> folded;
+            const std::vector<float> pbf = fold_affine_bf16(d, params, n_params, folded);
+            std::vector<__nv_bfloat16> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * N * N);
+            const float* Wl = pbf.data() + 2 * in;
+            size_t pos = 0;
             for (int l = 0; l < L; ++l) {
                 const int K = layer_k(d->layers, l, N, in);
-                if (l > 0) {
+                if (l > 0 && N == 256) {
+                    // ping-pong kernel (width 256): per layer 4 K slabs, each [CTA r: 128 rows] x 64 k
+                    for (int ks = 0; ks < N / 64; ++ks)
+                        for (int r = 0; r < 2; ++r) {
+                            uint8_t* blob = reinterpret_cast<uint8_t*>(ws.data() + pos);
+                            for (int nr = 0; nr < 128; ++nr)
+                                for (int kc = 0; kc < 64; ++kc) {
+                                    const int n = r * 128 + nr, k = ks * 64 + kc;
+                                    *reinterpret_cast<__nv_bfloat16*>(blob + sw128_offset(nr, kc, 128)) =
+                                        __float2bfloat16_rn(Wl[static_cast<int64_t>(k) * N + n]);
+                                }
+                            pos += 128 * 64;
+                        }
+                } else if (l > 0) {
                     for (int step = 0; step < 4; ++step) {
                         const int nh = step & 1, kh = step >> 1;
-                        for (int ks = 0; ks < 2; ++ks)
-                            for (int r = 0; r < 2; ++r) {
-                                for (int nr = 0; nr < 64; ++nr)
-                                    for (int kc = 0; kc < 64; ++kc) {
-                                        const int n = nh * 128 + r * 64 + nr, k = (kh * 2 + ks) * 64 + kc;
-                                        __half hi, lo;
-                                        split_h(Wl[static_cast<int64_t>(k) * N + n], hi, lo);
-                                        *reinterpret_cast<__half*>(out + sw128_offset(nr, kc, 64)) = hi;
-                                        *reinterpret_cast<__half*>(out + 8192 + sw128_offset(nr, kc, 64)) = lo;
-                                    }
-                                out += 16384;
-                            }
+                        for (int ks = 0; ks < KSL; ++ks) {
+                            uint8_t* chunk = reinterpret_cast<uint8_t*>(ws.data() + pos);
+                            for (int nr = 0; nr < NH; ++nr)
+                                for (int kc = 0; kc < 64; ++kc) {
+                                    const int n = nh * NH + nr, k = (kh * KSL + ks) * 64 + kc;
+                                    const float w = Wl[static_cast<int64_t>(k) * N + n];
+                                    *reinterpret_cast<__nv_bfloat16*>(chunk + sw128_offset(nr, kc, NH)) =
+                                        __float2bfloat16_rn(w);
+                                }
+                            pos += chunk_elems;
+                        }
                     }
                 }
                 Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
             }
-            uint8_t* dws = nullptr;
+            __nv_bfloat16* dws = nullptr;
             if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return cleanup_fail(st);
-            if ((st = encode_blob_map(&sa.tmap_w, dws, 128, ws.size() / 128, 128)) != SVN_OK) return cleanup_fail(st);
+            a.wstream = dws;
+            // CTA-pair kernel: TMA views of the weight stream and of the model-constant
+            // K=16 extension rows (bias hi/lo of non-concat layers with a nonzero bias).
+            const int BR = N == 256 ? N / 2 : N / 4;  // B rows per CTA per TMA box (128 for both kernels)
+            if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return cleanup_fail(st);
             std::vector<uint8_t> xm;
-            const float* Wb = params + 2 * in;
+            const float* Wb = pbf.data() + 2 * in;
+            std::vector<float> wq_bf, mbbase_bf, wx_bf;  // K0 inputs from the folded parameters
             for (int l = 0; l < L; ++l) {
                 const int K = layer_k(d->layers, l, N, in);
+                const float* Wfull = Wb;
                 const float* b = Wb + static_cast<int64_t>(N) * K;
-                LayerDev& ld = sa.layer[l];
+                LayerDev& ld = a.layer[l];
+                ld.ext = 0;
                 ld.ext_row = 0;
-                if (ld.ext == 1) {
+                bool bias_zero = true;
+                for (int n = 0; n < N; ++n)
+                    if (b[n] != 0.0f) bias_zero = false;
+                if (ld.mb_slot >= 0) {
+                    ld.ext = 2;
+                    const int xoff = (l == 0) ? 0 : N;
+                    wq_bf.insert(wq_bf.end(), Wfull + static_cast<int64_t>(xoff + 3) * N,
+                                 Wfull + static_cast<int64_t>(xoff + 3 + nq) * N);
+                    wx_bf.insert(wx_bf.end(), Wfull + static_cast<int64_t>(xoff) * N, Wfull + static_cast<int64_t>(xoff + 3) * N);
+                    mbbase_bf.insert(mbbase_bf.end(), b, b + N);
+                } else if (!bias_zero) {
+                    ld.ext = 1;
                     ld.ext_row = static_cast<int64_t>(xm.size() / 32);
                     const size_t base = xm.size();
-                    xm.resize(base + static_cast<size_t>(N) * 2 * 32, 0);
+                    xm.resize(base + static_cast<size_t>(N) * 32, 0);
                     for (int n = 0; n < N; ++n) {
-                        const int nh = n / 128, wi = n % 128, r = wi / 64, rr = wi % 64;
-                        uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * 128) * 32;
-                        __half hi, lo;
-                        split_h(b[n], hi, lo);
-                        *reinterpret_cast<__half*>(blob + ext_offset(rr, 0)) = hi;         // main: b_h
-                        *reinterpret_cast<__half*>(blob + 2048 + ext_offset(rr, 0)) = lo;  // corr: b_l'
+                        int blob_i, rr;
+                        if (N == 256) {  // ping-pong layout: blobs [r] of N/2 rows
+                            blob_i = n / BR;
+                            rr = n % BR;
+                        } else {         // pair layout: blobs [n-half][r] of N/4 rows
+                            const int nh = n / (N / 2), wi = n % (N / 2);
+                            blob_i = nh * 2 + wi / BR;
+                            rr = wi % BR;
+                        }
+                        uint8_t* blob = xm.data() + base + static_cast<size_t>(blob_i * BR) * 32;
+                        __nv_bfloat16 hi, lo;
+                        split_bf16_host(b[n], hi, lo);
+                        *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 0)) = hi;
+                        *reinterpret_cast<__nv_bfloat16*>(blob + ext_offset(rr, 1)) = lo;
                     }
                 }
                 Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
             }
-            if (xm.empty()) xm.resize(128 * 32, 0);
+            if (xm.empty()) xm.resize(static_cast<size_t>(BR) * 32, 0);
             uint8_t* dxm = nullptr;
             if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
-            if ((st = encode_blob_map(&sa.tmap_xm, dxm, 32, xm.size() / 32, 128)) != SVN_OK) return cleanup_fail(st);
-            m->base_split = sa;
-            m->has_split = true;
+            if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return cleanup_fail(st);
+            if ((st = m->upload(wq_bf.data(), wq_bf.size(), &m->d_wq_bf)) != SVN_OK) return cleanup_fail(st);
+            if ((st = m->upload(mbbase_bf.data(), mbbase_bf.size(), &m->d_mbbase_bf)) != SVN_OK) return cleanup_fail(st);
+            if ((st = m->upload(wx_bf.data(), wx_bf.size(), &m->d_wxslots_bf)) != SVN_OK) return cleanup_fail(st);
+            m->base_bf16 = a;
+            for (int l = 0; l < L; ++l)
+                if (folded[static_cast<size_t>(l)]) m->base_bf16.layer[l].flags &= ~kAffine;
+            m->base_bf16.bo = pbf[static_cast<size_t>(n_params - 1)];
+            m->has_bf16 = true;
         }
+
+        // fp32-accurate tensor-core path (width 256): every weight split into fp16 hi and
+        // 2^11-scaled lo' planes, per (layer, quarter step, 64-wide K slab, CTA half r) a
+        // [hi: 64 rows][lo': 64 rows] SW128 image; extension rows [main 64][corr 64] per
+        // (n-half, r).  Needs |W|, |b| well inside the fp16 range.
+        if (N == 256) {
+            float wmax = 0.f;
+            for (int64_t i = 2 * in; i < n_params; ++i) wmax = std::max(wmax, std::fabs(params[i]));
+            if (wmax < 1.0e4f) {
+                FusedArgs sa = a;
+                auto split_h = [](float x, __half& hi, __half& lo) {
+                    hi = __float2half_rn(x);
+                    lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
+                };
+                std::vector<uint8_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * 4 * 2 * 2 * 2 * 64 * 128);
+                uint8_t* out = ws.data();
+                const float* Wl = params + 2 * in;
+                for (int l = 0; l < L; ++l) {
+                    const int K = layer_k(d->layers, l, N, in);
+                    if (l > 0) {
+                        for (int step = 0; step < 4; ++step) {
+                            const int nh = step & 1, kh = step >> 1;
+                            for (int ks = 0; ks < 2; ++ks)
+                                for (int r = 0; r < 2; ++r) {
+                                    for (int nr = 0; nr < 64; ++nr)
+                                        for (int kc = 0; kc < 64; ++kc) {
+                                            const int n = nh * 128 + r * 64 + nr, k = (kh * 2 + ks) * 64 + kc;
+                                            __half hi, lo;
+                                            split_h(Wl[static_cast<int64_t>(k) * N + n], hi, lo);
+                                            *reinterpret_cast<__half*>(out + sw128_offset(nr, kc, 64)) = hi;
+                                            *reinterpret_cast<__half*>(out + 8192 + sw128_offset(nr, kc, 64)) = lo;
+                                        }
+                                    out += 16384;
+                                }
+                        }
+                    }
+                    Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+                }
+                uint8_t* dws = nullptr;
+                if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return cleanup_fail(st);
+                if ((st = encode_blob_map(&sa.tmap_w, dws, 128, ws.size() / 128, 128)) != SVN_OK) return cleanup_fail(st);
+                std::vector<uint8_t> xm;
+                const float* Wb = params + 2 * in;
+                for (int l = 0; l < L; ++l) {
+                    const int K = layer_k(d->layers, l, N, in);
+                    const float* b = Wb + static_cast<int64_t>(N) * K;
+                    LayerDev& ld = sa.layer[l];
+                    ld.ext_row = 0;
+                    if (ld.ext == 1) {
+                        ld.ext_row = static_cast<int64_t>(xm.size() / 32);
+                        const size_t base = xm.size();
+                        xm.resize(base + static_cast<size_t>(N) * 2 * 32, 0);
+                        for (int n = 0; n < N; ++n) {
+                            const int nh = n / 128, wi = n % 128, r = wi / 64, rr = wi % 64;
+                            uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * 128) * 32;
+                            __half hi, lo;
+                            split_h(b[n], hi, lo);
+                            *reinterpret_cast<__half*>(blob + ext_offset(rr, 0)) = hi;         // main: b_h
+                            *reinterpret_cast<__half*>(blob + 2048 + ext_offset(rr, 0)) = lo;  // corr: b_l'
+                        }
+                    }
+                    Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
+                }
+                if (xm.empty()) xm.resize(128 * 32, 0);
+                uint8_t* dxm = nullptr;
+                if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
+                if ((st = encode_blob_map(&sa.tmap_xm, dxm, 32, xm.size() / 32, 128)) != SVN_OK) return cleanup_fail(st);
+                m->base_split = sa;
+                m->has_split = true;
+            }
+        }
+        *out = m;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    *out = m;
-    return SVN_OK;
 }
 
 SVN_API svn_status svn_model_destroy(svn_model* m) {
-    delete m;
-    return SVN_OK;
+    try {
+        delete m;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 }  // extern "C"
@@ -523,46 +553,50 @@ extern "C" {
 // SVCKPT01 (nn.cpp:482-576): magic, u32 {version, n_blocks, block_dim, input_dim},
 // then the Fig. 2 parameter body; strict trailing-byte check.
 SVN_API svn_status svn_model_load_checkpoint(const char* path, int32_t device, svn_model** out) {
-    if (!path || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "load_checkpoint: null argument");
-    const std::string p(path);
-    FILE* f = std::fopen(path, "rb");
-    if (!f) return fail(SVN_ERR_IO, "cannot open checkpoint: " + p);
-    char magic[8];
-    if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, "SVCKPT01", 8) != 0) {
+    try {
+        if (!path || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "load_checkpoint: null argument");
+        const std::string p(path);
+        FILE* f = std::fopen(path, "rb");
+        if (!f) return fail(SVN_ERR_IO, "cannot open checkpoint: " + p);
+        char magic[8];
+        if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, "SVCKPT01", 8) != 0) {
+            std::fclose(f);
+            return fail(SVN_ERR_FORMAT, p + ": not a sweptnet checkpoint");
+        }
+        uint32_t hdr[4];
+        if (std::fread(hdr, sizeof(uint32_t), 4, f) != 4) {
+            std::fclose(f);
+            return fail(SVN_ERR_TRUNCATION, p + ": file ends inside header");
+        }
+        if (hdr[0] != 1u) {
+            std::fclose(f);
+            return fail(SVN_ERR_VERSION, p + ": checkpoint version " + std::to_string(hdr[0]) +
+                                             " not supported (expected 1)");
+        }
+        const int n_blocks = static_cast<int>(hdr[1]), block_dim = static_cast<int>(hdr[2]),
+                  input_dim = static_cast<int>(hdr[3]);
+        if (n_blocks < 1 || block_dim < 1 || input_dim < 5 || (input_dim - 3) % 2 != 0 || n_blocks + 1 > kMaxLayers ||
+            input_dim > kMaxIn) {
+            std::fclose(f);
+            return fail(SVN_ERR_FORMAT, p + ": implausible architecture header");
+        }
+        std::vector<svn_layer> layers(static_cast<size_t>(n_blocks + 1), svn_layer{1, 1, 1, 1});
+        layers[0] = svn_layer{1, 0, 0, 0};
+        svn_model_desc d{n_blocks + 1, block_dim, (input_dim - 3) / 2, layers.data()};
+        const int64_t n = svn_param_count(&d);
+        std::vector<float> params(static_cast<size_t>(n));
+        if (std::fread(params.data(), sizeof(float), static_cast<size_t>(n), f) != static_cast<size_t>(n)) {
+            std::fclose(f);
+            return fail(SVN_ERR_TRUNCATION, p + ": file ends inside tensor data");
+        }
+        char extra;
+        const bool trailing = std::fread(&extra, 1, 1, f) == 1;
         std::fclose(f);
-        return fail(SVN_ERR_FORMAT, p + ": not a sweptnet checkpoint");
+        if (trailing) return fail(SVN_ERR_FORMAT, p + ": trailing bytes after parameters");
+        return svn_model_create(&d, params.data(), n, device, out);
+    } catch (...) {
+        return host_exception();
     }
-    uint32_t hdr[4];
-    if (std::fread(hdr, sizeof(uint32_t), 4, f) != 4) {
-        std::fclose(f);
-        return fail(SVN_ERR_TRUNCATION, p + ": file ends inside header");
-    }
-    if (hdr[0] != 1u) {
-        std::fclose(f);
-        return fail(SVN_ERR_VERSION, p + ": checkpoint version " + std::to_string(hdr[0]) +
-                                         " not supported (expected 1)");
-    }
-    const int n_blocks = static_cast<int>(hdr[1]), block_dim = static_cast<int>(hdr[2]),
-              input_dim = static_cast<int>(hdr[3]);
-    if (n_blocks < 1 || block_dim < 1 || input_dim < 5 || (input_dim - 3) % 2 != 0 || n_blocks + 1 > kMaxLayers ||
-        input_dim > kMaxIn) {
-        std::fclose(f);
-        return fail(SVN_ERR_FORMAT, p + ": implausible architecture header");
-    }
-    std::vector<svn_layer> layers(static_cast<size_t>(n_blocks + 1), svn_layer{1, 1, 1, 1});
-    layers[0] = svn_layer{1, 0, 0, 0};
-    svn_model_desc d{n_blocks + 1, block_dim, (input_dim - 3) / 2, layers.data()};
-    const int64_t n = svn_param_count(&d);
-    std::vector<float> params(static_cast<size_t>(n));
-    if (std::fread(params.data(), sizeof(float), static_cast<size_t>(n), f) != static_cast<size_t>(n)) {
-        std::fclose(f);
-        return fail(SVN_ERR_TRUNCATION, p + ": file ends inside tensor data");
-    }
-    char extra;
-    const bool trailing = std::fread(&extra, 1, 1, f) == 1;
-    std::fclose(f);
-    if (trailing) return fail(SVN_ERR_FORMAT, p + ": trailing bytes after parameters");
-    return svn_model_create(&d, params.data(), n, device, out);
 }
 
 }  // extern "C"

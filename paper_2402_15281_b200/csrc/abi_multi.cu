@@ -164,6 +164,13 @@ namespace svn {
 namespace abi {
 namespace {
 
+void record(Outcome& o, svn_status s) {
+    if (s != SVN_OK && o.status == SVN_OK) {
+        o.status = s;
+        o.msg = svn_last_error();
+    }
+}
+
 // Run job(d) on every worker and collect the outcomes (status, message, launches) in the
 // caller's thread-local error / launch state.
 svn_status run_all(svn_multi* mg, const std::function<void(int, Outcome&)>& job) {
@@ -172,7 +179,11 @@ svn_status run_all(svn_multi* mg, const std::function<void(int, Outcome&)>& job)
     for (int d = 0; d < G; ++d)
         mg->workers[d]->post([&, d] {
             const int64_t l0 = g_launches;
-            job(d, out[d]);
+            try {
+                job(d, out[d]);
+            } catch (...) {
+                record(out[d], host_exception());
+            }
             out[d].launches = g_launches - l0;
         });
     for (int d = 0; d < G; ++d) mg->workers[d]->wait();
@@ -180,13 +191,6 @@ svn_status run_all(svn_multi* mg, const std::function<void(int, Outcome&)>& job)
     for (const Outcome& o : out)
         if (o.status != SVN_OK) return fail(o.status, o.msg);
     return SVN_OK;
-}
-
-void record(Outcome& o, svn_status s) {
-    if (s != SVN_OK && o.status == SVN_OK) {
-        o.status = s;
-        o.msg = svn_last_error();
-    }
 }
 
 }  // namespace
@@ -199,45 +203,53 @@ extern "C" {
 
 SVN_API svn_status svn_multi_create(const svn_model_desc* desc, const float* params, int64_t n_params,
                                     const int32_t* devices, int32_t n_devices, svn_multi** out) {
-    if (!out) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: null output");
-    *out = nullptr;
-    if (!devices || n_devices < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: no devices");
-    int count = 0;
-    SVN_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
-    for (int d = 0; d < n_devices; ++d)
-        if (devices[d] < 0 || devices[d] >= count) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: no such device");
-    std::unique_ptr<svn_multi> mg(new svn_multi);
-    mg->devices.assign(devices, devices + n_devices);
-    for (int d = 0; d < n_devices; ++d) {
-        svn_model* m = nullptr;
-        const svn_status s = svn_model_create(desc, params, n_params, devices[d], &m);
-        if (s != SVN_OK) return s;
-        mg->models.push_back(m);
-    }
-    bool distinct = true;
-    for (int i = 0; i < n_devices; ++i)
-        for (int j = 0; j < i; ++j)
-            if (devices[i] == devices[j]) distinct = false;
-    if (!distinct) {
-        mg->no_comm_why = "point sharding needs distinct devices (one NCCL rank per GPU)";
-    } else if (!nccl_api().ok()) {
-        mg->no_comm_why = nccl_api().why;
-    } else {
-        mg->comms.resize(static_cast<size_t>(n_devices));
-        const ncclResult_t r = nccl_api().comm_init_all(mg->comms.data(), n_devices, mg->devices.data());
-        if (r != ncclSuccess) {
-            mg->comms.clear();
-            return fail(SVN_ERR_NCCL, std::string("ncclCommInitAll: ") + nccl_api().error_string(r));
+    try {
+        if (!out) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: null output");
+        *out = nullptr;
+        if (!devices || n_devices < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: no devices");
+        int count = 0;
+        SVN_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+        for (int d = 0; d < n_devices; ++d)
+            if (devices[d] < 0 || devices[d] >= count) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: no such device");
+        std::unique_ptr<svn_multi> mg(new svn_multi);
+        mg->devices.assign(devices, devices + n_devices);
+        for (int d = 0; d < n_devices; ++d) {
+            svn_model* m = nullptr;
+            const svn_status s = svn_model_create(desc, params, n_params, devices[d], &m);
+            if (s != SVN_OK) return s;
+            mg->models.push_back(m);
         }
+        bool distinct = true;
+        for (int i = 0; i < n_devices; ++i)
+            for (int j = 0; j < i; ++j)
+                if (devices[i] == devices[j]) distinct = false;
+        if (!distinct) {
+            mg->no_comm_why = "point sharding needs distinct devices (one NCCL rank per GPU)";
+        } else if (!nccl_api().ok()) {
+            mg->no_comm_why = nccl_api().why;
+        } else {
+            mg->comms.resize(static_cast<size_t>(n_devices));
+            const ncclResult_t r = nccl_api().comm_init_all(mg->comms.data(), n_devices, mg->devices.data());
+            if (r != ncclSuccess) {
+                mg->comms.clear();
+                return fail(SVN_ERR_NCCL, std::string("ncclCommInitAll: ") + nccl_api().error_string(r));
+            }
+        }
+        for (int d = 0; d < n_devices; ++d) mg->workers.emplace_back(new Worker);
+        *out = mg.release();
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    for (int d = 0; d < n_devices; ++d) mg->workers.emplace_back(new Worker);
-    *out = mg.release();
-    return SVN_OK;
 }
 
 SVN_API svn_status svn_multi_destroy(svn_multi* mg) {
-    delete mg;
-    return SVN_OK;
+    try {
+        delete mg;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API int32_t svn_multi_device_count(const svn_multi* mg) {
@@ -247,82 +259,86 @@ SVN_API int32_t svn_multi_device_count(const svn_multi* mg) {
 SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const float* points, int64_t P,
                                        const float* q01, int64_t M, double margin, svn_shard_mode mode,
                                        float* min_out, int32_t* argmin_out, uint8_t* free_out) {
-    if (!mg) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
-    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
-    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
-    if (!points || !q01 || !min_out || !argmin_out || !free_out)
-        return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
-    NvtxRange nvtx("svn query_min_multi");
-    std::lock_guard<std::mutex> lock(mg->call_mu);
-    const int G = static_cast<int>(mg->devices.size());
-    if (mode == SVN_SHARD_AUTO) mode = M < G ? SVN_SHARD_POINTS : SVN_SHARD_MOTIONS;
-    const int64_t nq = 2 * static_cast<int64_t>(mg->models[0]->dof);
+    try {
+        if (!mg) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+        if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+        if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+        if (!points || !q01 || !min_out || !argmin_out || !free_out)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+        NvtxRange nvtx("svn query_min_multi");
+        std::lock_guard<std::mutex> lock(mg->call_mu);
+        const int G = static_cast<int>(mg->devices.size());
+        if (mode == SVN_SHARD_AUTO) mode = M < G ? SVN_SHARD_POINTS : SVN_SHARD_MOTIONS;
+        const int64_t nq = 2 * static_cast<int64_t>(mg->models[0]->dof);
 
-    if (mode == SVN_SHARD_MOTIONS) {
+        if (mode == SVN_SHARD_MOTIONS) {
+            return run_all(mg, [&](int d, Outcome& o) {
+                const int64_t b = d * M / G, e = (d + 1) * M / G;
+                if (e > b)
+                    record(o, svn_query_min(mg->models[d], prec, points, P, q01 + b * nq, e - b, margin, min_out + b,
+                                            argmin_out + b, free_out + b, nullptr));
+            });
+        }
+        if (mode != SVN_SHARD_POINTS) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: unknown shard mode");
+        if (mg->comms.empty()) return fail(SVN_ERR_UNSUPPORTED, "multi: " + mg->no_comm_why);
+        Rendezvous meet(G);
         return run_all(mg, [&](int d, Outcome& o) {
-            const int64_t b = d * M / G, e = (d + 1) * M / G;
-            if (e > b)
-                record(o, svn_query_min(mg->models[d], prec, points, P, q01 + b * nq, e - b, margin, min_out + b,
-                                        argmin_out + b, free_out + b, nullptr));
-        });
-    }
-    if (mode != SVN_SHARD_POINTS) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: unknown shard mode");
-    if (mg->comms.empty()) return fail(SVN_ERR_UNSUPPORTED, "multi: " + mg->no_comm_why);
-    Rendezvous meet(G);
-    return run_all(mg, [&](int d, Outcome& o) {
-        const svn_model* m = mg->models[d];
-        const int64_t pb = d * P / G, pe = (d + 1) * P / G;
-        DeviceGuard guard(m->device);
-        ensure_pool(m->device);
-        cudaStream_t st = thread_stream(m->device);
-        float *dp = nullptr, *dq = nullptr, *dmin = nullptr;
-        uint64_t* keys = nullptr;
-        int32_t* darg = nullptr;
-        uint8_t* dfree = nullptr;
-        auto cu = [&](cudaError_t e, const char* what) {
-            if (e != cudaSuccess) record(o, cuda_fail(e, what));
-            return e == cudaSuccess;
-        };
-        bool ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dq), sizeof(float) * nq * M, st), "cudaMallocAsync") &&
-                  cu(cudaMallocAsync(reinterpret_cast<void**>(&keys), sizeof(uint64_t) * M, st), "cudaMallocAsync") &&
-                  cu(cudaMallocAsync(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * (pe > pb ? pe - pb : 1), st),
-                     "cudaMallocAsync") &&
-                  cu(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions") &&
-                  cu(cudaMemcpyAsync(dp, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
-                     "H2D point chunk");
-        if (ok) {
-            record(o, svn_keys_init_device(keys, M, st));
-            if (o.status == SVN_OK && pe > pb) record(o, svn_query_min_keys_device(m, prec, dp, pe - pb, pb, dq, M, keys, st));
-            ok = o.status == SVN_OK && cu(cudaStreamSynchronize(st), "point-shard kernels");
-        }
-        if (meet.arrive_all_ok(ok)) {
-            // the one exchange of the path: 8 B per motion, u64 MIN over NVLink
-            const ncclResult_t r = nccl_api().all_reduce(keys, keys, static_cast<size_t>(M), ncclUint64, ncclMin,
-                                                         mg->comms[d], st);
-            if (r != ncclSuccess) {
-                o.status = SVN_ERR_NCCL;
-                o.msg = std::string("ncclAllReduce: ") + nccl_api().error_string(r);
-            } else if (d == 0) {
-                ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dmin), sizeof(float) * M, st), "cudaMallocAsync") &&
-                     cu(cudaMallocAsync(reinterpret_cast<void**>(&darg), sizeof(int32_t) * M, st), "cudaMallocAsync") &&
-                     cu(cudaMallocAsync(reinterpret_cast<void**>(&dfree), M, st), "cudaMallocAsync");
-                if (ok) record(o, svn_keys_finalize_device(keys, M, margin, dmin, darg, dfree, st));
-                if (ok && o.status == SVN_OK)
-                    ok = cu(cudaMemcpyAsync(min_out, dmin, sizeof(float) * M, cudaMemcpyDeviceToHost, st), "D2H min") &&
-                         cu(cudaMemcpyAsync(argmin_out, darg, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st),
-                            "D2H argmin") &&
-                         cu(cudaMemcpyAsync(free_out, dfree, M, cudaMemcpyDeviceToHost, st), "D2H free");
+            const svn_model* m = mg->models[d];
+            const int64_t pb = d * P / G, pe = (d + 1) * P / G;
+            DeviceGuard guard(m->device);
+            ensure_pool(m->device);
+            cudaStream_t st = thread_stream(m->device);
+            float *dp = nullptr, *dq = nullptr, *dmin = nullptr;
+            uint64_t* keys = nullptr;
+            int32_t* darg = nullptr;
+            uint8_t* dfree = nullptr;
+            auto cu = [&](cudaError_t e, const char* what) {
+                if (e != cudaSuccess) record(o, cuda_fail(e, what));
+                return e == cudaSuccess;
+            };
+            bool ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dq), sizeof(float) * nq * M, st), "cudaMallocAsync") &&
+                      cu(cudaMallocAsync(reinterpret_cast<void**>(&keys), sizeof(uint64_t) * M, st), "cudaMallocAsync") &&
+                      cu(cudaMallocAsync(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * (pe > pb ? pe - pb : 1), st),
+                         "cudaMallocAsync") &&
+                      cu(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions") &&
+                      cu(cudaMemcpyAsync(dp, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
+                         "H2D point chunk");
+            if (ok) {
+                record(o, svn_keys_init_device(keys, M, st));
+                if (o.status == SVN_OK && pe > pb) record(o, svn_query_min_keys_device(m, prec, dp, pe - pb, pb, dq, M, keys, st));
+                ok = o.status == SVN_OK && cu(cudaStreamSynchronize(st), "point-shard kernels");
             }
-            cu(cudaStreamSynchronize(st), "all-reduce");
-        } else if (o.status == SVN_OK) {
-            o.status = SVN_ERR_CUDA;
-            o.msg = "multi: another device failed before the all-reduce";
-        }
-        for (void* p : {static_cast<void*>(dp), static_cast<void*>(dq), static_cast<void*>(keys),
-                        static_cast<void*>(dmin), static_cast<void*>(darg), static_cast<void*>(dfree)})
-            if (p) cudaFreeAsync(p, st);
-        cudaStreamSynchronize(st);
-    });
+            if (meet.arrive_all_ok(ok)) {
+                // the one exchange of the path: 8 B per motion, u64 MIN over NVLink
+                const ncclResult_t r = nccl_api().all_reduce(keys, keys, static_cast<size_t>(M), ncclUint64, ncclMin,
+                                                             mg->comms[d], st);
+                if (r != ncclSuccess) {
+                    o.status = SVN_ERR_NCCL;
+                    o.msg = std::string("ncclAllReduce: ") + nccl_api().error_string(r);
+                } else if (d == 0) {
+                    ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dmin), sizeof(float) * M, st), "cudaMallocAsync") &&
+                         cu(cudaMallocAsync(reinterpret_cast<void**>(&darg), sizeof(int32_t) * M, st), "cudaMallocAsync") &&
+                         cu(cudaMallocAsync(reinterpret_cast<void**>(&dfree), M, st), "cudaMallocAsync");
+                    if (ok) record(o, svn_keys_finalize_device(keys, M, margin, dmin, darg, dfree, st));
+                    if (ok && o.status == SVN_OK)
+                        ok = cu(cudaMemcpyAsync(min_out, dmin, sizeof(float) * M, cudaMemcpyDeviceToHost, st), "D2H min") &&
+                             cu(cudaMemcpyAsync(argmin_out, darg, sizeof(int32_t) * M, cudaMemcpyDeviceToHost, st),
+                                "D2H argmin") &&
+                             cu(cudaMemcpyAsync(free_out, dfree, M, cudaMemcpyDeviceToHost, st), "D2H free");
+                }
+                cu(cudaStreamSynchronize(st), "all-reduce");
+            } else if (o.status == SVN_OK) {
+                o.status = SVN_ERR_CUDA;
+                o.msg = "multi: another device failed before the all-reduce";
+            }
+            for (void* p : {static_cast<void*>(dp), static_cast<void*>(dq), static_cast<void*>(keys),
+                            static_cast<void*>(dmin), static_cast<void*>(darg), static_cast<void*>(dfree)})
+                if (p) cudaFreeAsync(p, st);
+            cudaStreamSynchronize(st);
+        });
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 }  // extern "C"

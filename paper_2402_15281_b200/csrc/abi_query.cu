@@ -341,175 +341,211 @@ extern "C" {
 SVN_API svn_status svn_query_min_device(const svn_model* m, svn_precision prec, const float* points, int64_t P,
                                         const float* q01, int64_t M, double margin, float* min_out,
                                         int32_t* argmin_out, uint8_t* free_out, float* per_point, void* stream) {
-    if (!min_out || !argmin_out || !free_out) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null output");
-    return query_dense(m, prec, points, P, 0, q01, M, margin, min_out, argmin_out, free_out, per_point, nullptr,
-                       static_cast<cudaStream_t>(stream));
+    try {
+        if (!min_out || !argmin_out || !free_out) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null output");
+        return query_dense(m, prec, points, P, 0, q01, M, margin, min_out, argmin_out, free_out, per_point, nullptr,
+                           static_cast<cudaStream_t>(stream));
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API svn_status svn_keys_init_device(uint64_t* keys, int64_t M, void* stream) {
-    SVN_CUDA(launch_keys_init(reinterpret_cast<unsigned long long*>(keys), M, static_cast<cudaStream_t>(stream)),
-             "keys_init kernel");
-    ++g_launches;
-    return SVN_OK;
+    try {
+        SVN_CUDA(launch_keys_init(reinterpret_cast<unsigned long long*>(keys), M, static_cast<cudaStream_t>(stream)),
+                 "keys_init kernel");
+        ++g_launches;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API svn_status svn_query_min_keys_device(const svn_model* m, svn_precision prec, const float* points, int64_t P,
                                              int64_t index_offset, const float* q01, int64_t M, uint64_t* keys,
                                              void* stream) {
-    if (!keys) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null keys");
-    return query_dense(m, prec, points, P, index_offset, q01, M, 0.0, nullptr, nullptr, nullptr, nullptr, keys,
-                       static_cast<cudaStream_t>(stream));
+    try {
+        if (!keys) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null keys");
+        return query_dense(m, prec, points, P, index_offset, q01, M, 0.0, nullptr, nullptr, nullptr, nullptr, keys,
+                           static_cast<cudaStream_t>(stream));
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API svn_status svn_keys_finalize_device(const uint64_t* keys, int64_t M, double margin, float* min_out,
                                             int32_t* argmin_out, uint8_t* free_out, void* stream) {
-    SVN_CUDA(launch_keys_finalize(reinterpret_cast<const unsigned long long*>(keys), M, margin, min_out, argmin_out,
-                                  free_out, static_cast<cudaStream_t>(stream)),
-             "keys_finalize kernel");
-    ++g_launches;
-    return SVN_OK;
+    try {
+        SVN_CUDA(launch_keys_finalize(reinterpret_cast<const unsigned long long*>(keys), M, margin, min_out, argmin_out,
+                                      free_out, static_cast<cudaStream_t>(stream)),
+                 "keys_finalize kernel");
+        ++g_launches;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const float* points, int64_t P,
                                  const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
                                  uint8_t* free_out, float* per_point) {
-    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
-    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
-    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
-    if (!points || !q01 || !min_out || !argmin_out || !free_out)
-        return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
-    DeviceGuard guard(m->device);
-    ensure_pool(m->device);
-    cudaStream_t st = thread_stream(m->device);
-    const int nq = 2 * m->dof;
-    // staged layout: [points | q01] in, [min | argmin | free] out
-    const size_t o_q = align256(sizeof(float) * 3 * P), o_min = align256(o_q + sizeof(float) * nq * M);
-    const size_t o_arg = align256(o_min + sizeof(float) * M), o_free = align256(o_arg + sizeof(int32_t) * M);
-    const size_t total = align256(o_free + M);
-    Staging& sg = thread_staging(m->device);
-    SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
-    std::memcpy(sg.host, points, sizeof(float) * 3 * P);
-    std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
-    svn_status s;
-    {
-        Scratch sc(st);
-        float* dpp = nullptr;
-        if (per_point)
-            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
-        SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
-        s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
-                        reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
-                        reinterpret_cast<float*>(sg.dev + o_min), reinterpret_cast<int32_t*>(sg.dev + o_arg),
-                        sg.dev + o_free, dpp, nullptr, st);
-        if (s != SVN_OK) return s;
-        SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
-                 "D2H min/argmin/free");
-        if (per_point)
-            SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
+    try {
+        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+        if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+        if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+        if (!points || !q01 || !min_out || !argmin_out || !free_out)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+        DeviceGuard guard(m->device);
+        ensure_pool(m->device);
+        cudaStream_t st = thread_stream(m->device);
+        const int nq = 2 * m->dof;
+        // staged layout: [points | q01] in, [min | argmin | free] out
+        const size_t o_q = align256(sizeof(float) * 3 * P), o_min = align256(o_q + sizeof(float) * nq * M);
+        const size_t o_arg = align256(o_min + sizeof(float) * M), o_free = align256(o_arg + sizeof(int32_t) * M);
+        const size_t total = align256(o_free + M);
+        Staging& sg = thread_staging(m->device);
+        SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
+        std::memcpy(sg.host, points, sizeof(float) * 3 * P);
+        std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
+        svn_status s;
+        {
+            Scratch sc(st);
+            float* dpp = nullptr;
+            if (per_point)
+                SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
+            SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
+            s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
+                            reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
+                            reinterpret_cast<float*>(sg.dev + o_min), reinterpret_cast<int32_t*>(sg.dev + o_arg),
+                            sg.dev + o_free, dpp, nullptr, st);
+            if (s != SVN_OK) return s;
+            SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
+                     "D2H min/argmin/free");
+            if (per_point)
+                SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
+        }
+        SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+        std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
+        std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
+        std::memcpy(free_out, sg.host + o_free, M);
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
-    std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
-    std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
-    std::memcpy(free_out, sg.host + o_free, M);
-    return SVN_OK;
 }
 
 SVN_API svn_status svn_forward_eval(const svn_model* m, svn_precision prec, const float* raw, int64_t B, int64_t cols,
                                     float* out) {
-    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
-    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
-    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
-    if (!raw || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null buffer");
-    DeviceGuard guard(m->device);
-    ensure_pool(m->device);
-    cudaStream_t st = thread_stream(m->device);
-    float *draw = nullptr, *dout = nullptr;
-    {
-        Scratch sc(st);
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&draw), sizeof(float) * B * cols), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dout), sizeof(float) * B), "cudaMallocAsync");
-        SVN_CUDA(cudaMemcpyAsync(draw, raw, sizeof(float) * B * cols, cudaMemcpyHostToDevice, st), "H2D raw");
-        svn_status s = forward_rows(m, prec, raw, draw, B, cols, dout, st);
-        if (s != SVN_OK) return s;
-        SVN_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * B, cudaMemcpyDeviceToHost, st), "D2H out");
+    try {
+        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+        if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+        if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+        if (!raw || !out) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null buffer");
+        DeviceGuard guard(m->device);
+        ensure_pool(m->device);
+        cudaStream_t st = thread_stream(m->device);
+        float *draw = nullptr, *dout = nullptr;
+        {
+            Scratch sc(st);
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&draw), sizeof(float) * B * cols), "cudaMallocAsync");
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dout), sizeof(float) * B), "cudaMallocAsync");
+            SVN_CUDA(cudaMemcpyAsync(draw, raw, sizeof(float) * B * cols, cudaMemcpyHostToDevice, st), "H2D raw");
+            svn_status s = forward_rows(m, prec, raw, draw, B, cols, dout, st);
+            if (s != SVN_OK) return s;
+            SVN_CUDA(cudaMemcpyAsync(out, dout, sizeof(float) * B, cudaMemcpyDeviceToHost, st), "D2H out");
+        }
+        SVN_CUDA(cudaStreamSynchronize(st), "forward");
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    SVN_CUDA(cudaStreamSynchronize(st), "forward");
-    return SVN_OK;
 }
 
 SVN_API svn_status svn_forward_eval_device(const svn_model* m, svn_precision prec, const float* raw, int64_t B,
                                            int64_t cols, float* out, void* stream) {
-    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
-    if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
-    if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
-    DeviceGuard guard(m->device);
-    ensure_pool(m->device);
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    // segmenting needs the q columns on the host
-    std::vector<float> host(static_cast<size_t>(B * cols));
-    SVN_CUDA(cudaMemcpyAsync(host.data(), raw, sizeof(float) * B * cols, cudaMemcpyDeviceToHost, st), "D2H raw");
-    SVN_CUDA(cudaStreamSynchronize(st), "D2H raw");
-    return forward_rows(m, prec, host.data(), raw, B, cols, out, st);
+    try {
+        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: null model");
+        if (cols != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: input width mismatch");
+        if (B < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "forward: batch must be non-empty");
+        DeviceGuard guard(m->device);
+        ensure_pool(m->device);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        // segmenting needs the q columns on the host
+        std::vector<float> host(static_cast<size_t>(B * cols));
+        SVN_CUDA(cudaMemcpyAsync(host.data(), raw, sizeof(float) * B * cols, cudaMemcpyDeviceToHost, st), "D2H raw");
+        SVN_CUDA(cudaStreamSynchronize(st), "D2H raw");
+        return forward_rows(m, prec, host.data(), raw, B, cols, out, st);
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision prec, const double* cloud, int64_t P,
                                             const double* q0, const double* q1, int32_t dof, double* min_out,
                                             int32_t* argmin_out) {
-    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null model");
-    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
-    if (3 + 2 * dof != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: motion dof does not match model");
-    if (!cloud || !q0 || !q1 || !min_out || !argmin_out)
-        return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null buffer");
-    // nn.cpp:469-473: every coordinate and joint value is cast to float
-    std::vector<float> pts(static_cast<size_t>(3 * P)), q(static_cast<size_t>(2 * dof));
-    for (int64_t i = 0; i < 3 * P; ++i) pts[i] = static_cast<float>(cloud[i]);
-    for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
-    for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
-    float mn = 0.f;
-    int32_t idx = 0;
-    uint8_t fr = 0;
-    svn_status s = svn_query_min(m, prec, pts.data(), P, q.data(), 1, 0.0, &mn, &idx, &fr, nullptr);
-    if (s != SVN_OK) return s;
-    *min_out = static_cast<double>(mn);
-    *argmin_out = idx;
-    return SVN_OK;
+    try {
+        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null model");
+        if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+        if (3 + 2 * dof != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: motion dof does not match model");
+        if (!cloud || !q0 || !q1 || !min_out || !argmin_out)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null buffer");
+        // nn.cpp:469-473: every coordinate and joint value is cast to float
+        std::vector<float> pts(static_cast<size_t>(3 * P)), q(static_cast<size_t>(2 * dof));
+        for (int64_t i = 0; i < 3 * P; ++i) pts[i] = static_cast<float>(cloud[i]);
+        for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
+        for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+        float mn = 0.f;
+        int32_t idx = 0;
+        uint8_t fr = 0;
+        svn_status s = svn_query_min(m, prec, pts.data(), P, q.data(), 1, 0.0, &mn, &idx, &fr, nullptr);
+        if (s != SVN_OK) return s;
+        *min_out = static_cast<double>(mn);
+        *argmin_out = idx;
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
 }
 
 SVN_API svn_status svn_eval_grid(const svn_model* m, svn_precision prec, const double* origin, double voxel_size,
                                  const int32_t* dims, const double* q0, const double* q1, int32_t dof, float* values) {
-    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null model");
-    if (!origin || !dims || !q0 || !q1 || !values) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null buffer");
-    if (3 + 2 * dof != m->in)
-        return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: q0/q1 must have one angle per joint");
-    if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || !(voxel_size > 0))
-        return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: empty grid");
-    const int64_t P = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
-    DeviceGuard guard(m->device);
-    ensure_pool(m->device);
-    cudaStream_t st = thread_stream(m->device);
-    std::vector<float> q(static_cast<size_t>(2 * dof));
-    for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
-    for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
-    {
-        Scratch sc(st);
-        float *dp = nullptr, *dq = nullptr, *dmin = nullptr, *dvals = nullptr;
-        int32_t* darg = nullptr;
-        uint8_t* dfree = nullptr;
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * P), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * q.size()), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dmin), sizeof(float)), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&darg), sizeof(int32_t)), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dfree), 1), "cudaMallocAsync");
-        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dvals), sizeof(float) * P), "cudaMallocAsync");
-        SVN_CUDA(cudaMemcpyAsync(dq, q.data(), sizeof(float) * q.size(), cudaMemcpyHostToDevice, st), "H2D q");
-        SVN_CUDA(launch_grid_points(origin, voxel_size, dims, dp, st), "grid_points kernel");
-        ++g_launches;
-        svn_status s = query_dense(m, prec, dp, P, 0, dq, 1, 0.0, dmin, darg, dfree, dvals, nullptr, st);
-        if (s != SVN_OK) return s;
-        SVN_CUDA(cudaMemcpyAsync(values, dvals, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "D2H values");
-        SVN_CUDA(cudaStreamSynchronize(st), "eval_grid");
+    try {
+        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null model");
+        if (!origin || !dims || !q0 || !q1 || !values) return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: null buffer");
+        if (3 + 2 * dof != m->in)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: q0/q1 must have one angle per joint");
+        if (dims[0] < 1 || dims[1] < 1 || dims[2] < 1 || !(voxel_size > 0))
+            return fail(SVN_ERR_INVALID_ARGUMENT, "reconstruct: empty grid");
+        const int64_t P = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+        DeviceGuard guard(m->device);
+        ensure_pool(m->device);
+        cudaStream_t st = thread_stream(m->device);
+        std::vector<float> q(static_cast<size_t>(2 * dof));
+        for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
+        for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+        {
+            Scratch sc(st);
+            float *dp = nullptr, *dq = nullptr, *dmin = nullptr, *dvals = nullptr;
+            int32_t* darg = nullptr;
+            uint8_t* dfree = nullptr;
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * P), "cudaMallocAsync");
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dq), sizeof(float) * q.size()), "cudaMallocAsync");
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dmin), sizeof(float)), "cudaMallocAsync");
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&darg), sizeof(int32_t)), "cudaMallocAsync");
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dfree), 1), "cudaMallocAsync");
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dvals), sizeof(float) * P), "cudaMallocAsync");
+            SVN_CUDA(cudaMemcpyAsync(dq, q.data(), sizeof(float) * q.size(), cudaMemcpyHostToDevice, st), "H2D q");
+            SVN_CUDA(launch_grid_points(origin, voxel_size, dims, dp, st), "grid_points kernel");
+            ++g_launches;
+            svn_status s = query_dense(m, prec, dp, P, 0, dq, 1, 0.0, dmin, darg, dfree, dvals, nullptr, st);
+            if (s != SVN_OK) return s;
+            SVN_CUDA(cudaMemcpyAsync(values, dvals, sizeof(float) * P, cudaMemcpyDeviceToHost, st), "D2H values");
+            SVN_CUDA(cudaStreamSynchronize(st), "eval_grid");
+        }
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
     }
-    return SVN_OK;
 }
 
 
