@@ -194,14 +194,18 @@ def main():
         steps, warm = max(1, args.steps), max(0, min(args.warmup, 1))
         per_step = max(2.0, min(10.0, 120.0 / (steps + warm)))  # whole arm within ~2 minutes
         val, sample = run_cpu(w, params, args.seed, threads, lib, steps, warm, per_step)
+        med_ms = getattr(run_cpu, "last_ms", None)
+        # the reference's own call is single-threaded (nn.cpp:116): one thread, ~5 s sample
+        v1, s1 = run_cpu(w, params, args.seed, 1, lib, 1, 0, 5.0)
         line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": getattr(run_cpu, "last_ms", None),
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": med_ms,
                 "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
                 "config": {"workload": w.key, "description": w.description, "network": w.program.name},
                 "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
                                  "sample": sample + f"; oracle restatement of nn.cpp:95-130 (-O3 -march={march}), "
-                                                    f"{threads} threads on {cpu_model()}"},
+                                                    f"{threads} threads on {cpu_model()}",
+                                 "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": s1}},
                 "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
