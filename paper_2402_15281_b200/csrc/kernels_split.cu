@@ -261,10 +261,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
+            unsigned long long pw_a = 0, pw_f = 0, pw_x = 0;  // SVN_KERNEL_PROF wait accounting
+            const unsigned long long p_start = prof_clock();
             int64_t k = 0;
             for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
                 const int b = static_cast<int>(k & 1);
+                const unsigned long long cx = prof_clock();
                 mbar_wait(&ax_full[b], ax_ph[b]);
+                pw_x += prof_clock() - cx;
                 ax_ph[b] ^= 1u;
                 for (int l = 0; l < L; ++l) {
                     const LayerDev& ld = a.layer[l];
@@ -272,7 +276,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     for (int step = 0; step < steps; ++step) {
                         const int nh = step & 1, kh = step >> 1;
                         if (kh == 0 && (k > 0 || l > 0)) {
+                            const unsigned long long c0 = prof_clock();
                             mbar_wait(&a_ready[nh], ar_ph[nh]);
+                            pw_a += prof_clock() - c0;
                             ar_ph[nh] ^= 1u;
                         }
                         tc_fence_after();
@@ -280,7 +286,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                         const uint32_t d_corr = d_main + 128;
                         bool acc = false;
                         if (kh == 0 && ld.ext) {
+                            const unsigned long long c0 = prof_clock();
                             mbar_wait(&full[stage], phase);
+                            pw_f += prof_clock() - c0;
                             tc_fence_after();
                             const uint32_t xs = s_base + stage * CHUNK;
                             const uint64_t adesc = noswz_desc(ax_base + b * AX_BYTES, 128, 256);
@@ -292,7 +300,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                         }
                         if (l > 0) {
                             for (int ks = 0; ks < KSL; ++ks) {
+                                const unsigned long long c0 = prof_clock();
                                 mbar_wait(&full[stage], phase);
+                                pw_f += prof_clock() - c0;
                                 tc_fence_after();
                                 const uint32_t aoff = static_cast<uint32_t>(kh * KSL + ks) * A_SLAB;
                                 const uint32_t bhi = s_base + static_cast<uint32_t>(stage) * CHUNK, blo = bhi + B_HALF;
@@ -314,6 +324,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     }
                 }
             }
+            if (a.prof) {
+                atomicAdd(a.prof + kProfMmaWaitA, pw_a);
+                atomicAdd(a.prof + kProfMmaWaitFull, pw_f);
+                atomicAdd(a.prof + kProfMmaWaitAx, pw_x);
+                atomicAdd(a.prof + kProfMmaTotal, prof_clock() - p_start);
+            }
         }
     } else if (warp < OUT_WARP) {
         // ---------------------------------------------------------------- epilogue --
@@ -324,6 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
         uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
+        unsigned long long pe_d = 0, pe_w = 0, pe_o = 0;  // SVN_KERNEL_PROF accounting
         int64_t k = 0;
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
             float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -331,7 +348,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
                 for (int j = 0; j < 2; ++j) {
+                    const unsigned long long c0 = prof_clock();
                     mbar_wait(&d_full[j], dp[j]);
+                    const unsigned long long c1 = prof_clock();
+                    pe_d += c1 - c0;
                     dp[j] ^= 1u;
                     tc_fence_after();
                     const uint32_t tb = tmem + t_lane + static_cast<uint32_t>(j * 256 + ch * COLS);
@@ -356,6 +376,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc2[i]), LO_INV, __uint_as_float(rm2[i]));
                     epi32(ld, l, last, v, j * NHO + ch * COLS + 32, row, Ahi, Alo, wo_s, dot);
+                    pe_w += prof_clock() - c1;
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
                     __syncwarp();
@@ -363,6 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                 }
             }
             // hand the row's partial dot to the output warp (dotbuf[parity] is reused two tiles later)
+            const unsigned long long c3 = prof_clock();
             const int b = static_cast<int>(k & 1);
             if (k >= 2) {
                 mbar_wait(&out_empty[b], oe_ph[b]);
@@ -371,6 +393,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
             dotbuf[(b * 2 + ch) * TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
+            pe_o += prof_clock() - c3;
+        }
+        if (a.prof && e == 0 && lane == 0 && rank == 0) {
+            atomicAdd(a.prof + kProfEpiWaitD, pe_d);
+            atomicAdd(a.prof + kProfEpiWork, pe_w);
+            atomicAdd(a.prof + kProfEpiOut, pe_o);
         }
     } else {
         // ------------------------------------------------------------- output warp --
