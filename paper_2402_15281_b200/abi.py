@@ -123,6 +123,8 @@ def _finish(L):
         "svn_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("SVN_LIB") and not hasattr(L, name):
+            continue  # A/B build of an older revision (SVN_LIB): entry points added since are absent
         fn = getattr(L, name)
         fn.restype = res
         fn.argtypes = args
