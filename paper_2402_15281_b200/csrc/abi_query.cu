@@ -113,7 +113,10 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
     svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N == 256 ? m->N / 2 : m->N / 4));
     if (s != SVN_OK) return s;
-    SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, ext, keys, counters, n_keys, st),
+    unsigned int* sched = nullptr;  // dynamic tile counter of the width-512 kernel, zeroed by K0
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&sched), sizeof(unsigned int)), "cudaMallocAsync(tile counter)");
+    a.sched = sched;
+    SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, ext, keys, counters, n_keys, sched, st),
              "motion_ext kernel");
     ++g_launches;
     return SVN_OK;

@@ -62,6 +62,7 @@ struct FusedArgs {
     const TileDesc* tiles;     // non-null: explicit tile table (forward_eval segments)
     int exact;                 // fp32 exact order (no q fold)
     int tile_rows;             // rows per work item the host cut the tiles with (SIMT: 128/64, or 32)
+    unsigned int* sched;       // width-512 bf16 kernel: dynamic tile counter (zeroed by K0)
     // outputs
     unsigned long long* keys;  // [M] packed (orderable(delta) << 32 | index), or null
     unsigned int* counters;    // [M] tiles done, for the fused finaliser, or null
@@ -203,6 +204,6 @@ cudaError_t launch_split_ext(const FusedArgs& a, const float* wq, const float* m
                              cudaStream_t st);
 cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
                               uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,
-                              int64_t n_keys, cudaStream_t st);
+                              int64_t n_keys, unsigned int* sched_reset, cudaStream_t st);
 
 }  // namespace svn

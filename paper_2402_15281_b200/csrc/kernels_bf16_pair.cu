@@ -53,7 +53,8 @@ struct PairCfg {
     static constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * CHUNK;
     static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
     static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
-    static constexpr uint32_t SMEM = OFF_BAR + 256;
+    static constexpr int TQ = 8;                     // tile queue entries (dynamic schedule)
+    static constexpr uint32_t SMEM = OFF_BAR + 384;  // 20 + TQ barriers, TQ tile ids, TMEM slot
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(COLS % 32 == 0, "epilogue works in 32-column TMEM loads");
 };
@@ -214,7 +215,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     uint64_t* ax_full = a_ready + 2;            // [2] leader: A extension buffer b written (2 output warps)
     uint64_t* out_full = ax_full + 2;           // [tile parity] each CTA: dotbuf holds a finished tile (8 warps)
     uint64_t* out_empty = out_full + 2;         // [tile parity] each CTA: output warp has read dotbuf
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(out_empty + 2);
+    uint64_t* tq_full = out_empty + 2;          // [TQ] each CTA: tile queue entry published
+    long long* tq = reinterpret_cast<long long*>(tq_full + C::TQ);  // [TQ] each CTA: tile ids
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + C::TQ);
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = lane_id();
@@ -222,6 +225,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     const int L = a.L;
     const int64_t pair = blockIdx.x >> 1;
     const int64_t npairs = gridDim.x >> 1;
+    // Dynamic tile schedule: the pair's k-th tile is entry k of a queue that the leader's
+    // output warp fills (tiles 0 and 1 = pair, pair + npairs; then the next unclaimed tile of
+    // a global counter, two tiles ahead of use) and publishes to both CTAs.  Pairs whose SMs
+    // run slower (e.g. farther from the L2 slices holding the weights) take fewer tiles
+    // instead of finishing last; an id >= n_tiles ends the sequence.
+    auto tile_at = [&](int64_t k) -> int64_t {
+        mbar_wait_cluster(&tq_full[k % C::TQ], static_cast<uint32_t>((k / C::TQ) & 1));
+        return *reinterpret_cast<volatile long long*>(&tq[k % C::TQ]);
+    };
 
     if (threadIdx.x == 0) {
         if (smem_u32(smem) & 1023u) __trap();
@@ -236,6 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             mbar_init(&out_full[j], C::EPI_WARPS);
             mbar_init(&out_empty[j], 1);
         }
+        for (int q = 0; q < C::TQ; ++q) mbar_init(&tq_full[q], 1);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < N; i += blockDim.x) wo_s[i] = a.wo[i];
@@ -268,7 +281,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             auto advance = [&]() {
                 if (++stage == C::STAGES) stage = 0, phase ^= 1u;
             };
-            for (int64_t t = pair; t < a.n_tiles; t += npairs) {
+            for (int64_t k = 0;; ++k) {
+                const int64_t t = tile_at(k);
+                if (t >= a.n_tiles) break;
                 int32_t motion, nrows;
                 int64_t pbase, obase;
                 tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
@@ -315,8 +330,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             uint32_t ar_ph[2] = {0u, 0u}, ax_ph[2] = {0u, 0u};
             unsigned long long pw_a = 0, pw_f = 0, pw_x = 0;
             const unsigned long long p_start = prof_clock();
-            int64_t k = 0;  // local tile counter
-            for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+            for (int64_t k = 0;; ++k) {  // local tile counter
+                if (tile_at(k) >= a.n_tiles) break;
                 const int b = static_cast<int>(k & 1);
                 {
                     const unsigned long long c0 = prof_clock();
@@ -392,8 +407,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
         uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
         unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0;
-        int64_t k = 0;
-        for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+        for (int64_t k = 0;; ++k) {
+            if (tile_at(k) >= a.n_tiles) break;
             float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
@@ -483,18 +498,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
         };
+        // the pair's scheduler: lane 0 of the leader's output warp
+        const bool sched = rank == 0 && lane == 0;
+        long long last_pub = 0;
+        auto publish = [&](int64_t k, long long t) {
+            const int q = static_cast<int>(k % C::TQ);
+            tq[q] = t;
+            st_cluster_s64(mapa_shared(smem_u32(&tq[q]), 1), t);
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tq_full[q]), 0));
+            mbar_arrive_cluster(mapa_shared(smem_u32(&tq_full[q]), 1));
+            last_pub = t;
+        };
+        if (sched) {
+            publish(0, pair);
+            publish(1, pair + npairs);
+        }
         for (int b = 0; b < 2; ++b) {
-            const int64_t t = pair + b * npairs;
+            const int64_t t = tile_at(b);
             if (t < a.n_tiles) {
                 load_points(t);
                 store_ax(b);
             }
         }
-        int64_t k = 0;
-        for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
+        for (int64_t k = 0;; ++k) {
+            const int64_t t = tile_at(k);
+            if (t >= a.n_tiles) break;
             const int b = static_cast<int>(k & 1);
-            const bool next = t + 2 * npairs < a.n_tiles;
-            if (next) load_points(t + 2 * npairs);
+            if (sched)  // tile k+2: the next unclaimed one, or the end marker once the counter ran out
+                publish(k + 2, last_pub >= a.n_tiles ? last_pub
+                                                     : 2 * npairs + static_cast<long long>(atomicAdd(a.sched, 1u)));
+            __syncwarp();
+            const int64_t t2 = tile_at(k + 2);
+            const bool next = t2 < a.n_tiles;
+            if (next) load_points(t2);
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
@@ -580,9 +616,11 @@ struct QNormX {
 __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N, int n_mb,
                                   const float* __restrict__ wq, const float* __restrict__ base_bias,
                                   const float* __restrict__ wx_slots, uint8_t* __restrict__ ext, const QNormX qn,
-                                  unsigned long long* keys, unsigned int* counters, int64_t n_keys, int pp_layout) {
+                                  unsigned long long* keys, unsigned int* counters, int64_t n_keys, int pp_layout,
+                                  unsigned int* sched) {
     const int64_t m = blockIdx.x;
     const int slot = blockIdx.y;
+    if (sched && m == 0 && slot == 0 && threadIdx.x == 0) *sched = 0u;  // the fused kernel's tile counter
     if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
         keys[m] = ~0ull;
         counters[m] = 0u;
@@ -630,7 +668,7 @@ namespace svn {
 
 cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
                               uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,
-                              int64_t n_keys, cudaStream_t st) {
+                              int64_t n_keys, unsigned int* sched_reset, cudaStream_t st) {
     if (a.M <= 0) return cudaSuccess;
     QNormX qn;
     for (int k = 0; k < 2 * a.dof && k < kMaxIn; ++k) {
@@ -639,7 +677,7 @@ cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* 
     }
     dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
     motion_ext_kernel<<<grid, 256, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn,
-                                             keys_init, counters_init, n_keys, a.N == 256 ? 1 : 0);
+                                             keys_init, counters_init, n_keys, a.N == 256 ? 1 : 0, sched_reset);
     return cudaGetLastError();
 }
 
