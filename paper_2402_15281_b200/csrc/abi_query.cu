@@ -408,15 +408,30 @@ SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const f
         const size_t total = align256(o_free + M);
         Staging& sg = thread_staging(m->device);
         SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
-        std::memcpy(sg.host, points, sizeof(float) * 3 * P);
-        std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
+        // inputs already in pinned memory go to the device directly; pageable ones through the
+        // pinned staging block (one host copy, then one H2D)
+        auto pinned = [](const void* p) {
+            cudaPointerAttributes at{};
+            return cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        };
+        const bool direct = pinned(points) && pinned(q01);
+        if (!direct) {
+            std::memcpy(sg.host, points, sizeof(float) * 3 * P);
+            std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
+        }
         svn_status s;
         {
             Scratch sc(st);
             float* dpp = nullptr;
             if (per_point)
                 SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
-            SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
+            if (direct) {
+                SVN_CUDA(cudaMemcpyAsync(sg.dev, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
+                SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),
+                         "H2D motions");
+            } else {
+                SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
+            }
             s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
                             reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
                             reinterpret_cast<float*>(sg.dev + o_min), reinterpret_cast<int32_t*>(sg.dev + o_arg),
