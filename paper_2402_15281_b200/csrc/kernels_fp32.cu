@@ -106,6 +106,20 @@ __device__ __forceinline__ void tile_done(const FusedArgs& a, int32_t motion) {
 }
 
 // ------------------------------------------------------------------ K1f -----
+// Packed fp32 pairs: fma.rn.f32x2 is two independent round-to-nearest fp32 FMAs, i.e. the
+// same bits as two fmaf calls, at half the issue slots (an 8 x 8 register tile reaches 126
+// FMA/clk/SM with it against 100 with FFMA, scripts/microbench_ffma2_tile.cu).
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float f2_lo(unsigned long long v) { return __uint_as_float(static_cast<uint32_t>(v)); }
+__device__ __forceinline__ float f2_hi(unsigned long long v) { return __uint_as_float(static_cast<uint32_t>(v >> 32)); }
+__device__ __forceinline__ void f2_fma(unsigned long long& d, unsigned long long a, unsigned long long b) {
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
+}
+
 // Weight chunks of 32 KiB, double-buffered, and the k loop unrolled 8: one barrier per 32
 // (width 256) or 16 (width 512) k steps.  Measured against 4 x 16 KiB stages with unroll 4:
 // +6 % on c2 and on c3's network in fp32 (scripts/gpu_ab.sh; the -D overrides are A/B hooks).
@@ -236,16 +250,15 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
             const float* bias = (!a.exact && concat && ld.mb_slot >= 0)
                                     ? a.motion_bias + (static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * N
                                     : ld.bias;
-            float acc[8][C::NC];
+            // acc[i][2p], acc[i][2p+1] as one packed pair (column pairs of the 8 x NC tile)
+            unsigned long long acc[8][C::NC / 2];
 #pragma unroll
             for (int j4 = 0; j4 < C::NC / 4; ++j4) {
                 const float4 b4 = *reinterpret_cast<const float4*>(bias + cg * 4 + j4 * CG * 4);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    acc[i][j4 * 4 + 0] = b4.x;
-                    acc[i][j4 * 4 + 1] = b4.y;
-                    acc[i][j4 * 4 + 2] = b4.z;
-                    acc[i][j4 * 4 + 3] = b4.w;
+                    acc[i][j4 * 2 + 0] = f2_pack(b4.x, b4.y);
+                    acc[i][j4 * 2 + 1] = f2_pack(b4.z, b4.w);
                 }
             }
             const int rows = layer_rows<N>(a, l);
@@ -261,19 +274,19 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                     const float4 a0 = *reinterpret_cast<const float4*>(act_at(a_off + r0 + kk, rg * 8));
                     const float4 a1 = *reinterpret_cast<const float4*>(act_at(a_off + r0 + kk, rg * 8 + 4));
                     const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-                    float wv[C::NC];
+                    unsigned long long wv[C::NC / 2];  // weight column pairs straight from a 16-byte load
 #pragma unroll
                     for (int j4 = 0; j4 < C::NC / 4; ++j4) {
-                        const float4 w4 = *reinterpret_cast<const float4*>(w + kk * N + cg * 4 + j4 * CG * 4);
-                        wv[j4 * 4 + 0] = w4.x;
-                        wv[j4 * 4 + 1] = w4.y;
-                        wv[j4 * 4 + 2] = w4.z;
-                        wv[j4 * 4 + 3] = w4.w;
+                        const ulonglong2 w2 = *reinterpret_cast<const ulonglong2*>(w + kk * N + cg * 4 + j4 * CG * 4);
+                        wv[j4 * 2 + 0] = w2.x;
+                        wv[j4 * 2 + 1] = w2.y;
                     }
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int i = 0; i < 8; ++i) {
+                        const unsigned long long ap = f2_pack(av[i], av[i]);
 #pragma unroll
-                        for (int j = 0; j < C::NC; ++j) acc[i][j] = __fmaf_rn(av[i], wv[j], acc[i][j]);
+                        for (int j = 0; j < C::NC / 2; ++j) f2_fma(acc[i][j], ap, wv[j]);
+                    }
                 };
                 if (nk == C::KS) {
                     // full chunk: unrolled so the next k's shared-memory loads are scheduled
@@ -310,7 +323,8 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
                     }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
-                        float r = acc[i][j4 * 4 + jj];
+                        const unsigned long long pr = acc[i][j4 * 2 + (jj >> 1)];
+                        float r = (jj & 1) ? f2_hi(pr) : f2_lo(pr);
                         if (act) r = r > 0.f ? r : 0.f;
                         if (aff) r = __fmaf_rn(r, sv, tv);
                         hv[i] = res ? __fadd_rn(hv[i], r) : r;
