@@ -314,8 +314,8 @@ def main():
         formula = 148 * 128 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
         fp = ROOT / "profiles" / "fp32_peak.json"
         if fp.exists():  # MEASURED_PEAKS.json has no FP32 figure: the highest FP32 FMA rate measured
-            peak = float(json.loads(fp.read_text())["ffma_tflops"])  # on the box (cuBLAS SGEMM, TF32 off)
-            src = "measured FP32 peak: cuBLAS SGEMM 8192^3, TF32 off (profiles/fp32_peak.json)"
+            peak = float(json.loads(fp.read_text())["ffma_tflops"])  # on the box (packed FFMA2 tile)
+            src = "measured FP32 peak: FFMA2 register-tile microbenchmark (profiles/fp32_peak.json)"
         else:
             peak, src = formula, "formula 148 SM x 128 FFMA lanes x 2 x sm_max_mhz"
         roof = {"bound": "fp32-simt", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
