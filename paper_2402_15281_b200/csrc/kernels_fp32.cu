@@ -120,11 +120,13 @@ __device__ __forceinline__ void f2_fma(unsigned long long& d, unsigned long long
     asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(a), "l"(b));
 }
 
-// Weight chunks of 32 KiB, double-buffered, and the k loop unrolled 8: one barrier per 32
-// (width 256) or 16 (width 512) k steps.  Measured against 4 x 16 KiB stages with unroll 4:
-// +6 % on c2 and on c3's network in fp32 (scripts/gpu_ab.sh; the -D overrides are A/B hooks).
+// Weight chunks of 32 KiB, double-buffered: one barrier per 32 (width 256) or 16 (width 512)
+// k steps, and the k loop over a full chunk unrolled completely.  Measured: 32 KiB x 2 with
+// unroll 8 +6 % over 16 KiB x 4 with unroll 4 (FFMA); with the packed FFMA2 loop, unrolling
+// the whole 32-step chunk +9 % on c2 over unroll 8 (+4 % on c3's network, where a chunk is
+// 16 steps) (scripts/gpu_ab_fp32.sh; the -D overrides are A/B hooks).
 #ifndef SVN_FP32_UNROLL
-#define SVN_FP32_UNROLL 8
+#define SVN_FP32_UNROLL 32
 #endif
 constexpr int kFp32Unroll = SVN_FP32_UNROLL;
 #ifndef SVN_FP32_STAGES
