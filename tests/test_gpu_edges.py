@@ -268,3 +268,21 @@ def test_many_short_lived_host_threads():
         assert np.array_equal(out[0].min, ref.min)
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20  # no per-thread growth
+
+
+@pytest.mark.parametrize("prog", [S.plain(3, 128, 6), S.fig2(2, 128, 7), S.deepsdf(6, 128, 6, 3)],
+                         ids=lambda p: p.name)
+@pytest.mark.parametrize("M,P", [(1, 300), (5, 2000)])
+def test_width_128_fp32_bit_identical(prog, M, P):
+    """Width 128 (FP32 path only: 4-column FFMA2 pairs per thread) against the oracle, both
+    tile sizes (32-row tiles when there are few, 128-row otherwise)."""
+    params = S.init_params(prog, 29, "he")
+    pts, q = WORKLOADS["c2"].make(seed=29, motions=M, points=P)
+    if prog.dof == 7:
+        q = np.concatenate([q[:, :6], q[:, :1], q[:, 6:], q[:, 6:7]], axis=1)
+    r = S.Model(prog, params).query_min(pts, q, 0.02, precision="fp32_exact", per_point=True)
+    omin, oarg, ofree, opp = O.query_min(prog, params, pts, q, 0.02, per_point=True, threads=8)
+    assert np.array_equal(r.per_point, opp)
+    assert np.array_equal(r.min, omin) and np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
+    with pytest.raises(S.SvnError):
+        S.Model(prog, params).query_min(pts, q, 0.02, precision="bf16")
