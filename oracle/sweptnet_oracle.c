@@ -6,15 +6,15 @@
  * and bench.py (cpu_baseline leg and --impl reference) may load it.  The
  * product library (paper_2402_15281_b200/) never links, loads or calls it.
  *
- * Parity status: UNPINNED by reference golden vectors.  The reference
- * (/root/reference/proj) needs Eigen3 (CMakeLists.txt:14) which is absent from
- * this image and from the GPU boxes, and it ships no tests or fixtures
- * (CMakeLists.txt:44 points at a missing tests/ dir).  This restatement is pinned
- * instead by (i) the C++ standard's mt19937_64 known answer and a std::mt19937_64
- * stream dump (oracle/pin_rng.cpp), (ii) the SPEC.md known-answer properties
- * (param count, zero-weight model, batch/row invariance, single-point and
- * duplicated-cloud min), and (iii) an independent torch fp64 implementation
- * (oracle/torch_fp64.py).  See DESIGN.md "Parity".
+ * Parity status: PINNED to the reference's own code.  oracle/ref/Makefile
+ * compiles the unmodified reference sources (src/nn.cpp, robot.cpp, geometry.cpp,
+ * sha256-checked) against an Eigen-API subset written for this repo
+ * (oracle/ref/eigen_subset; Eigen3 is absent here) into oracle/_ref/; its
+ * init_model, forward_eval<float/double>, predict_min_distance, make_normalizer and
+ * load_checkpoint produced tests/golden/ref_*.npz (tests/golden/make_ref_golden.py),
+ * and this file reproduces them bit for bit (tests/test_ref_oracle.py).  Also
+ * pinned by the std::mt19937_64 dump (oracle/pin_rng.cpp), the SPEC.md
+ * known-answer properties and an independent torch fp64 oracle.  See DESIGN.md §3.
  *
  * What it restates (reference file:line under /root/reference/proj):
  *   Rng / mt19937_64 / uniform      include/sweptnet/rng.hpp:14-26
@@ -47,9 +47,9 @@
  * contracted form GCC emits for -std=gnu++20 (CMAKE_CXX_STANDARD 20 with
  * extensions on): Rng::uniform = fma(hi-lo, u, lo) (rng.hpp:23), BN shift
  * t = fma(-mu, s, beta) (nn.cpp:110), block update h + fmaf(r, s, t)
- * (nn.cpp:125).  The output dot (nn.cpp:127) uses Eigen's vectorised tree whose
- * order is ISA-dependent; here it is a sequential fmaf over k ascending.  Those
- * choices move results by at most a few ulp.
+ * (nn.cpp:125).  The output dot (nn.cpp:127): rounded products summed in k order,
+ * which is what g++ -O3 makes of Eigen's scalar reduction (pinned below); Eigen's
+ * vectorised packet tree orders it differently (ISA-dependent, a few e-7 absolute).
  *
  * Parameter buffer layout (float, shared with the C-ABI svn_model_create):
  *   norm_shift[in], norm_scale[in],
@@ -319,8 +319,11 @@ OR_API void oracle_init_params(const int* flags, int L, int N, int dof, uint64_t
                 h[n] = res ? h[n] + r : r;                                                           \
             }                                                                                        \
         }                                                                                            \
-        S acc = (S)0;                                                                                \
-        for (int k = 0; k < N; ++k) acc = FMA(m->wo[k], h[k], acc);                                  \
+        /* nn.cpp:127 as the reference's own build evaluates it (oracle/ref): Eigen's scalar    \
+         * redux res = p0; res = res + p_k, whose loop g++ -O3 vectorises as rounded products   \
+         * added in k order (no contraction across the vector multiply).  Contract is off here. */ \
+        S acc = m->wo[0] * h[0];                                                                     \
+        for (int k = 1; k < N; ++k) acc = acc + m->wo[k] * h[k];                                     \
         return acc + m->bo;                                                                          \
     }
 

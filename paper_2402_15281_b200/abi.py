@@ -73,10 +73,13 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    override = os.environ.get("SVN_LIB")  # A/B experiments: load another build of the same ABI
+    override = os.environ.get("SVN_LIB")  # A/B experiments: another in-tree build of the same ABI
     if override:
-        L = C.CDLL(override)
-        return _finish(L)
+        ab_dir = (Path(__file__).resolve().parent.parent / "scripts" / "ab").resolve()
+        cand = Path(override).resolve()
+        if ab_dir not in cand.parents:
+            raise RuntimeError(f"SVN_LIB must name an A/B build under {ab_dir} (got {override})")
+        return _finish(C.CDLL(str(cand)))
     if os.environ.get("SVN_NO_BUILD") != "1":
         try:
             _build.build()

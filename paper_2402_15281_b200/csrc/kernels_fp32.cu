@@ -6,9 +6,10 @@
 // (collision.cpp:68).  Each CTA owns a 64-row tile of one motion.  Activations stay
 // in shared memory, transposed (actT[k][row]), between layers; weight rows stream
 // through a 2-stage ring of 32 KiB bulk copies (cp.async.bulk, TMA engine).  Each
-// output is one sequential fmaf chain over k ascending — the same order as the
-// reference's column axpy — so with `exact` set (no q-fold: bias, h part, x, q0,
-// q1) the per-point delta matches the CPU restatement bit for bit.
+// hidden output is one sequential fmaf chain over k ascending — the same order as the
+// reference's column axpy — and the output dot is the reference build's rounded-product
+// in-order sum, so with `exact` set (no q-fold: bias, h part, x, q0, q1) the per-point
+// delta matches the reference's own nn.cpp (oracle/ref) and the C restatement bit for bit.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
@@ -340,12 +341,14 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
         }
         const unsigned long long o0 = prof_clock();
 
-        // output layer: delta = sum_k w_o[k] h[k] (sequential fmaf) + b_o; min/argmin
+        // output layer: delta = sum_k w_o[k] h[k] + b_o; min/argmin.  nn.cpp:127's dot as the
+        // reference's own build computes it (oracle/ref, g++ -O3 on Eigen's scalar redux): the
+        // products rounded, then added in k order — no fused multiply-add in this chain
         if (tid < C::TM) {
-            float acc = 0.f;
-            // one k-ordered chain; unrolled so the shared loads run ahead of the FMAs
+            float acc = __fmul_rn(wo_s[0], *act_at(0, tid));
+            // one k-ordered chain; unrolled so the shared loads run ahead of the adds
 #pragma unroll 16
-            for (int k = 0; k < N; ++k) acc = __fmaf_rn(wo_s[k], *act_at(k, tid), acc);
+            for (int k = 1; k < N; ++k) acc = __fadd_rn(acc, __fmul_rn(wo_s[k], *act_at(k, tid)));
             const float delta = __fadd_rn(acc, a.bo);
             const bool valid = tid < nrows;
             if (valid && a.per_point) a.per_point[obase + tid] = delta;

@@ -8,9 +8,10 @@
                        independent torch fp64 oracle, per-motion min/argmin/free, and the
                        sha256 of the seeded parameter buffer.
 
-The reference itself cannot be built here (Eigen3 missing), so these
-fixtures freeze the restated oracle after it has been cross-checked against the
-standard-library RNG and the torch fp64 implementation.
+These freeze the restated oracle on the BASELINE configs (plain / DeepSDF networks have no
+reference implementation) after it has been checked against the reference's
+own nn.cpp on Fig. 2 networks (tests/golden/make_ref_golden.py -> ref_fig2.npz,
+tests/test_ref_oracle.py), the standard-library RNG and the torch fp64 implementation.
 """
 from __future__ import annotations
 

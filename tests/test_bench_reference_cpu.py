@@ -21,3 +21,13 @@ def test_reference_arm_json_line():
     assert line["e2e"] == {"value": line["value"], "unit": "queries/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["config"]["workload"] == "c1"
+
+
+def test_reference_arm_loads_no_product_library():
+    """The reference arm runs the oracle only: the product's native library must not be mapped."""
+    code = ("import runpy, sys; sys.argv = ['bench.py', '--impl', 'reference', '--config', 'c1', '--steps', '1', "
+            "'--warmup', '0']\ntry:\n    runpy.run_path('bench.py', run_name='__main__')\nexcept SystemExit:\n    pass\n"
+            "maps = open('/proc/self/maps').read()\nprint('PRODUCT_LOADED' if 'libsweptnet_b200' in maps else 'CLEAN')")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "CLEAN"

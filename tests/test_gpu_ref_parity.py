@@ -1,0 +1,128 @@
+"""GPU parity against the reference's OWN code, on inputs a trained model actually has.
+
+1. tests/golden/ref_fig2.npz (outputs of /root/reference/proj/src/nn.cpp itself, built by
+   oracle/ref/Makefile) on trained-like Fig. 2 checkpoints — the reference's make_normalizer
+   or a random non-identity shift/scale, nonzero biases, BN statistics with negative gammas —
+   loaded through svn_model_load_checkpoint (SVCKPT01):
+     fp32 / fp32_exact   forward_eval and predict_min_distance BIT-IDENTICAL to the reference
+     fp32_split, bf16    within the frozen per-network bounds
+2. The BASELINE networks (plain 4x256 = c1/c2, DeepSDF 8x512 = c3/c5, plain 6x512 7-DoF = c4)
+   with a make_normalizer-style normaliser and nonzero hidden biases (the bf16 kernels' model
+   extension MMA, ext==1) against the oracle (pinned to the reference by test_ref_oracle.py):
+   FP32 path bit-identical; bf16 / fp32_split within their bounds; classification equal
+   outside the ambiguous band.
+"""
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_2402_15281_b200 as S
+from oracle import oracle as O
+from paper_2402_15281_b200 import abi
+from paper_2402_15281_b200.workloads import WORKLOADS, limits_default
+
+import ref_golden as G
+
+pytestmark = pytest.mark.gpu
+
+Z, NAMES = G.load()
+_B = json.loads((Path(__file__).resolve().parent / "golden" / "bf16_bounds.json").read_text())
+BF16_BOUND = {k: v["bound"] for k, v in _B.items() if isinstance(v, dict)}
+_F = json.loads((Path(__file__).resolve().parent / "golden" / "fp32_split_bounds.json").read_text())
+SPLIT_BOUND = {k: v["bound"] for k, v in _F.items() if isinstance(v, dict)}
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint32)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_checkpoint_fp32_bit_identical_to_reference(name, tmp_path):
+    g, prog, _, p = G.params(Z, name)
+    ck = tmp_path / "m.ckpt"
+    G.write_checkpoint(ck, prog, p)
+    m = S.Model.from_checkpoint(str(ck))
+    if prog.width not in (128, 256, 512):  # device widths: the product refuses loudly
+        with pytest.raises(abi.SvnError):
+            m.forward_eval(g["raw"], precision="fp32")
+        return
+    for prec in ("fp32", "fp32_exact"):
+        out = m.forward_eval(g["raw"], precision=prec)
+        assert np.array_equal(bits(out), bits(g["forward_eval_f32"])), (prec, np.abs(out - g["forward_eval_f32"]).max())
+        assert m.predict_min_distance(g["cloud"], g["q0"], g["q1"], precision=prec) == \
+            (float(g["pmd"][0]), int(g["pmd"][1]))
+    # the same parameters handed over directly (svn_model_create) give the same bits
+    d = S.Model(prog, p)
+    assert np.array_equal(bits(d.forward_eval(g["raw"], precision="fp32")), bits(g["forward_eval_f32"]))
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_checkpoint_tensor_core_paths_within_bounds(name, tmp_path):
+    g, prog, _, p = G.params(Z, name)
+    key = f"fig2_{prog.n_layers - 1}x{prog.width}"
+    ck = tmp_path / "m.ckpt"
+    G.write_checkpoint(ck, prog, p)
+    m = S.Model.from_checkpoint(str(ck))
+    ref = g["forward_eval_f32"].astype(np.float64)
+    for prec, bounds in (("bf16", BF16_BOUND), ("fp32_split", SPLIT_BOUND)):
+        if key not in bounds:
+            with pytest.raises(abi.SvnError):  # no tensor-core kernel for this width: loud refusal
+                m.forward_eval(g["raw"], precision=prec)
+            continue
+        err = np.abs(m.forward_eval(g["raw"], precision=prec) - ref).max()
+        print(f"{name} {prec}: max|err| {err:.3e} (bound {bounds[key]})")
+        assert err <= bounds[key], (prec, err)
+
+
+def trained_like(program, params, pts, seed):
+    """A make_normalizer-style normaliser (nn.cpp:314-338: x centred on the cloud mean and
+    scaled 1/reach, joints mapped to [-1, 1] by their limits) and nonzero biases on every
+    layer, on top of seeded weights.  Layout: the svn_param_count buffer."""
+    rng = np.random.default_rng(seed)
+    p = params.copy()
+    dof, N = program.dof, program.width
+    in_ = 3 + 2 * dof
+    lim = limits_default(dof) if dof != 7 else np.full(7, np.float32(170 * np.pi / 180))
+    p[:3] = pts.mean(axis=0)
+    p[3:in_] = 0.0
+    p[in_:in_ + 3] = np.float32(1.0 / 0.9)
+    p[in_ + 3:2 * in_] = np.float32(1.0) / np.concatenate([lim, lim]).astype(np.float32)
+    off = 2 * in_
+    for l in range(program.n_layers):
+        off += N * program.layer_k(l)
+        p[off:off + N] = rng.uniform(-0.1, 0.1, N)
+        off += N
+        if program.layers[l].affine:
+            off += 4 * N
+    p[-1] = rng.uniform(-0.1, 0.1)
+    return p.astype(np.float32)
+
+
+@pytest.mark.parametrize("key,M,P", [("c2", 4, 1500), ("c3", 3, 900), ("c4", 3, 800)])
+def test_baseline_nets_with_normaliser_and_biases(key, M, P):
+    w = WORKLOADS[key]
+    pts, q = w.make(seed=21, motions=M, points=P)
+    p = trained_like(w.program, S.init_params(w.program, 21, w.bound), pts, 21)
+    model = S.Model(w.program, p)
+    omin, oarg, ofree, opp = O.query_min(w.program, p, pts, q, w.margin, per_point=True, threads=8)
+    for prec in ("fp32", "fp32_exact"):
+        r = model.query_min(pts, q, w.margin, precision=prec, per_point=True)
+        assert np.array_equal(bits(r.per_point), bits(opp)), (prec, np.abs(r.per_point - opp).max())
+        assert np.array_equal(r.min, omin) and np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
+    precs = [("bf16", BF16_BOUND[w.program.name])]
+    if w.program.name in SPLIT_BOUND:
+        precs.append(("fp32_split", SPLIT_BOUND[w.program.name]))
+    for prec, bound in precs:
+        r = model.query_min(pts, q, w.margin, precision=prec, per_point=True)
+        err = np.abs(r.per_point.astype(np.float64) - opp).max()
+        print(f"{key} {prec}: max|err| {err:.3e} (bound {bound})")
+        assert err <= bound, (prec, err)
+        amb = np.abs(omin.astype(np.float64) - w.margin) <= bound
+        assert np.array_equal(r.free[~amb], ofree[~amb])
+        d_at = opp[np.arange(M), r.argmin]
+        assert np.all((r.argmin == oarg) | (d_at - omin <= bound))
+    # rows of mixed motions through forward_eval (the a-8 path) with the same model
+    rows = np.concatenate([pts[:200], q[np.arange(200) % M]], axis=1).astype(np.float32)
+    assert np.array_equal(bits(model.forward_eval(rows, precision="fp32_exact")), bits(O.forward_eval(w.program, p, rows)))
