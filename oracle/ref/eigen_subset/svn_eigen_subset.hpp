@@ -15,7 +15,7 @@
 // Element-wise results do not depend on SIMD width, so they match Eigen's vectorised paths.
 // Reductions are where vectorisation changes the ORDER: Eigen's scalar (non-vectorised)
 // redux is sequential, `res = c0; res = res + c_k` (k ascending) — implemented here as the
-// default.  With SVN_EIGEN_PACKET_REDUX=W (W = 4, 8 or 16 lanes) `dot`/`sum` instead follow
+// default, every term rounded before it is added (see redux()).  With SVN_EIGEN_PACKET_REDUX=W (W = 4, 8 or 16 lanes) `dot`/`sum` instead follow
 // the structure of Eigen's linear-vectorised redux (two W-lane partial sums over the aligned
 // body, combined, then a horizontal tree and the scalar tail) so the ulp effect of the
 // ISA-dependent order at nn.cpp:127 can be measured (tests/test_ref_oracle.py).
@@ -23,6 +23,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstddef>
 #include <initializer_list>
@@ -56,6 +57,44 @@ template <class S, int R, int C, int O, int MR, int MC> struct is_plain<Matrix<S
 template <class T> using nested = std::conditional_t<is_plain<std::remove_cv_t<T>>::value, const T&, T>;
 template <class T> concept Expr = std::is_base_of_v<DenseBase<std::remove_cvref_t<T>>, std::remove_cvref_t<T>>;
 template <int R, int C> constexpr int default_opts() { return (R == 1 && C != 1) ? RowMajor : ColMajor; }
+
+// Coefficient storage.  Fixed sizes are stored inline with no other members, like Eigen's
+// (sizeof(Vector3d) == 24, so a std::vector<Vector3d> is a contiguous double [n x 3] — the
+// layout the reference's callers hand to the C-ABI); dynamic sizes on the heap.
+template <class S, int R, int C, bool Fixed = (R > 0 && C > 0)>
+struct DenseStorage {
+    std::array<S, static_cast<size_t>(R > 0 && C > 0 ? R * C : 1)> d{};
+    static constexpr Index rows() { return R; }
+    static constexpr Index cols() { return C; }
+    S* data() { return d.data(); }
+    const S* data() const { return d.data(); }
+    void set(Index r, Index c) {
+        if (r != R || c != C) throw std::invalid_argument("svn eigen subset: resizing a fixed-size matrix");
+        d.fill(S(0));
+    }
+    void swap(DenseStorage& o) noexcept { d.swap(o.d); }
+};
+template <class S, int R, int C>
+struct DenseStorage<S, R, C, false> {
+    Index r = R > 0 ? R : 0, c = C > 0 ? C : 0;  // declared before d: initialised first
+    std::vector<S> d;
+    DenseStorage() : d(static_cast<size_t>(r * c)) {}
+    Index rows() const { return r; }
+    Index cols() const { return c; }
+    S* data() { return d.data(); }
+    const S* data() const { return d.data(); }
+    void set(Index rr, Index cc) {
+        if ((R > 0 && rr != R) || (C > 0 && cc != C)) throw std::invalid_argument("svn eigen subset: resizing a fixed dimension");
+        r = rr;
+        c = cc;
+        d.assign(static_cast<size_t>(rr * cc), S(0));
+    }
+    void swap(DenseStorage& o) noexcept {
+        d.swap(o.d);
+        std::swap(r, o.r);
+        std::swap(c, o.c);
+    }
+};
 }  // namespace internal
 
 // ------------------------------------------------------------------------------------------
@@ -88,8 +127,15 @@ SVN_EI S redux(Index n, F&& coeff) {
         return res;
     }
 #endif
+    // Each term is rounded on its own, then added in index order: what g++ -O3 makes of
+    // Eigen's scalar redux when it vectorises the in-order reduction (the product is a
+    // vector multiply, the adds stay sequential, nothing is fused).  The volatile makes that
+    // explicit, so the result does not hinge on the vectoriser's cost model for a given type.
     S res = coeff(0);
-    for (Index i = 1; i < n; ++i) res = res + coeff(i);
+    for (Index i = 1; i < n; ++i) {
+        volatile S term = coeff(i);
+        res = res + term;
+    }
     return res;
 }
 }  // namespace internal
@@ -349,15 +395,15 @@ public:
     using Base::setZero;
     using Base::setOnes;
 
-    Matrix() : r_(R > 0 ? R : 0), c_(C > 0 ? C : 0), d_(static_cast<size_t>(r_ * c_)) {}
+    Matrix() = default;
     // dynamic: (rows, cols); vectors: (size)
     Matrix(Index rows, Index cols) requires(R == Dynamic || C == Dynamic) { resize(rows, cols); }
     explicit Matrix(Index n) requires((R == 1 || C == 1) && (R == Dynamic || C == Dynamic)) { resize(n); }
     // fixed 3-vectors
-    Matrix(S a, S b, S c) requires(R * C == 3) : Matrix() {
-        d_[0] = a;
-        d_[1] = b;
-        d_[2] = c;
+    Matrix(S a, S b, S c) requires(R * C == 3) {
+        st_.d[0] = a;
+        st_.d[1] = b;
+        st_.d[2] = c;
     }
     template <class T0, class T1, class T2>
     Matrix(T0 a, T1 b, T2 c) requires(R * C == 3 && std::is_arithmetic_v<T0> && !std::is_same_v<T0, S>)
@@ -369,63 +415,45 @@ public:
     template <class E> Matrix(const DenseBase<E>& e) { *this = e; }
     template <class E> Matrix& operator=(const DenseBase<E>& e) {
         const E& x = e.derived();
-        if constexpr (!std::is_same_v<E, Matrix>) {
-            Matrix tmp;
-            tmp.resize(x.rows(), x.cols());
-            tmp.assign_loop(x, [](auto& a, auto b) SVN_EIL { a = b; });
-            *this = std::move(tmp);
-        } else {
-            d_ = x.d_;
-            r_ = x.r_;
-            c_ = x.c_;
-        }
+        Matrix tmp;
+        tmp.resize(x.rows(), x.cols());
+        tmp.assign_loop(x, [](auto& a, auto b) SVN_EIL { a = b; });
+        st_.swap(tmp.st_);
         return *this;
     }
 
-    SVN_EI Index rows() const { return r_; }
-    SVN_EI Index cols() const { return c_; }
-    SVN_EI Index idx(Index i, Index j) const { return row_major ? i * c_ + j : j * r_ + i; }
-    SVN_EI S coeff(Index i, Index j) const { return d_[static_cast<size_t>(idx(i, j))]; }
-    SVN_EI S& coeffRef(Index i, Index j) { return d_[static_cast<size_t>(idx(i, j))]; }
-    SVN_EI S& operator[](Index k) { return d_[static_cast<size_t>(k)]; }
-    SVN_EI S operator[](Index k) const { return d_[static_cast<size_t>(k)]; }
-    SVN_EI S& operator()(Index k) { return d_[static_cast<size_t>(k)]; }
-    SVN_EI S operator()(Index k) const { return d_[static_cast<size_t>(k)]; }
-    S* data() { return d_.data(); }
-    const S* data() const { return d_.data(); }
+    SVN_EI Index rows() const { return st_.rows(); }
+    SVN_EI Index cols() const { return st_.cols(); }
+    SVN_EI Index idx(Index i, Index j) const { return row_major ? i * cols() + j : j * rows() + i; }
+    SVN_EI S coeff(Index i, Index j) const { return st_.data()[idx(i, j)]; }
+    SVN_EI S& coeffRef(Index i, Index j) { return st_.data()[idx(i, j)]; }
+    SVN_EI S& operator[](Index k) { return st_.data()[k]; }
+    SVN_EI S operator[](Index k) const { return st_.data()[k]; }
+    SVN_EI S& operator()(Index k) { return st_.data()[k]; }
+    SVN_EI S operator()(Index k) const { return st_.data()[k]; }
+    S* data() { return st_.data(); }
+    const S* data() const { return st_.data(); }
 
-    void resize(Index rows, Index cols) {
-        if ((R != Dynamic && rows != R) || (C != Dynamic && cols != C))
-            throw std::invalid_argument("svn eigen subset: resizing a fixed dimension");
-        r_ = rows;
-        c_ = cols;
-        d_.assign(static_cast<size_t>(rows * cols), S(0));
-    }
+    void resize(Index rows, Index cols) { st_.set(rows, cols); }
     void resize(Index n) {
         static_assert(R == 1 || C == 1, "resize(n) on a matrix");
         if constexpr (C == 1) resize(n, 1); else resize(1, n);
     }
-    void conservativeResize(Index rows, NoChange_t) { conservativeResize(rows, c_); }
+    void conservativeResize(Index rows, NoChange_t) { conservativeResize(rows, cols()); }
     void conservativeResize(Index n) {
         if constexpr (C == 1) conservativeResize(n, 1); else conservativeResize(1, n);
     }
     void conservativeResize(Index rows, Index cols) {
         Matrix m;
-        m.r_ = rows;
-        m.c_ = cols;
-        m.d_.assign(static_cast<size_t>(rows * cols), S(0));
-        for (Index i = 0; i < std::min(rows, r_); ++i)
-            for (Index j = 0; j < std::min(cols, c_); ++j) m.coeffRef(i, j) = coeff(i, j);
-        *this = std::move(m);
+        m.resize(rows, cols);
+        for (Index i = 0; i < std::min(rows, this->rows()); ++i)
+            for (Index j = 0; j < std::min(cols, this->cols()); ++j) m.coeffRef(i, j) = coeff(i, j);
+        st_.swap(m.st_);
     }
     void setZero(Index n) { resize(n), setZero(); }
     void setOnes(Index n) { resize(n), setOnes(); }
     void setZero(Index rows, Index cols) { resize(rows, cols), setZero(); }
-    void swap(Matrix& o) noexcept {
-        std::swap(r_, o.r_);
-        std::swap(c_, o.c_);
-        d_.swap(o.d_);
-    }
+    void swap(Matrix& o) noexcept { st_.swap(o.st_); }
     auto noalias() { return NoAlias{*this}; }
     struct NoAlias {
         Matrix& m;
@@ -439,14 +467,14 @@ public:
     auto array() const { return KindView<const Matrix&, true>(*this); }
     auto matrix() { return KindView<Matrix&, false>(*this); }
     auto matrix() const { return KindView<const Matrix&, false>(*this); }
-    auto row(Index i) { return Block<Matrix>(this, i, 0, 1, c_); }
-    auto row(Index i) const { return Block<const Matrix>(this, i, 0, 1, c_); }
-    auto col(Index j) { return Block<Matrix>(this, 0, j, r_, 1); }
-    auto col(Index j) const { return Block<const Matrix>(this, 0, j, r_, 1); }
-    auto leftCols(Index n) { return Block<Matrix>(this, 0, 0, r_, n); }
-    auto leftCols(Index n) const { return Block<const Matrix>(this, 0, 0, r_, n); }
-    auto rightCols(Index n) { return Block<Matrix>(this, 0, c_ - n, r_, n); }
-    auto rightCols(Index n) const { return Block<const Matrix>(this, 0, c_ - n, r_, n); }
+    auto row(Index i) { return Block<Matrix>(this, i, 0, 1, cols()); }
+    auto row(Index i) const { return Block<const Matrix>(this, i, 0, 1, cols()); }
+    auto col(Index j) { return Block<Matrix>(this, 0, j, rows(), 1); }
+    auto col(Index j) const { return Block<const Matrix>(this, 0, j, rows(), 1); }
+    auto leftCols(Index n) { return Block<Matrix>(this, 0, 0, rows(), n); }
+    auto leftCols(Index n) const { return Block<const Matrix>(this, 0, 0, rows(), n); }
+    auto rightCols(Index n) { return Block<Matrix>(this, 0, cols() - n, rows(), n); }
+    auto rightCols(Index n) const { return Block<const Matrix>(this, 0, cols() - n, rows(), n); }
     auto rowwise() { return RowwiseOp<Matrix&>(*this); }
     auto rowwise() const { return RowwiseOp<const Matrix&>(*this); }
 
@@ -457,14 +485,13 @@ public:
     static Matrix Identity() {
         Matrix m;
         m.setZero();
-        for (Index i = 0; i < std::min(m.r_, m.c_); ++i) m.coeffRef(i, i) = S(1);
+        for (Index i = 0; i < std::min(m.rows(), m.cols()); ++i) m.coeffRef(i, i) = S(1);
         return m;
     }
 
 private:
     template <class, int, int, int, int, int> friend class Matrix;
-    Index r_ = 0, c_ = 0;
-    std::vector<S> d_;
+    internal::DenseStorage<S, R, C> st_;
 };
 
 // array()/matrix() views: same coefficients, different operator* semantics
@@ -716,5 +743,6 @@ using Vector3f = Matrix<float, 3, 1>;
 using Vector3d = Matrix<double, 3, 1>;
 using Vector3i = Matrix<int, 3, 1>;
 using Matrix3d = Matrix<double, 3, 3>;
+static_assert(sizeof(Vector3d) == 3 * sizeof(double), "fixed-size storage must be inline (Eigen layout)");
 
 }  // namespace Eigen
