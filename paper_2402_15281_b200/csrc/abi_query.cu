@@ -109,13 +109,37 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
         ++g_launches;
         return SVN_OK;
     }
+    unsigned int* sched = nullptr;  // dynamic tile counter of the width-512 kernel, zeroed by K0
+    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&sched), sizeof(unsigned int)), "cudaMallocAsync(tile counter)");
+    a.sched = sched;
+    static const bool k0_ext = [] {  // A/B hook: the K0-built per-motion stream at width 512 too
+        const char* e = std::getenv("SVN_BF16_K0_EXT");
+        return e && e[0] == '1';
+    }();
+    if (m->N == 512 && !k0_ext) {
+        // width 512: the fused kernel's output warps build each tile's extension rows in a ring of
+        // two tile slots per CTA (grid x 2 x n_mb x 2 n-halves x N/4 rows x 32 B: 4.8 MB on c3,
+        // L2-resident) — no per-motion stream in HBM; K0 only resets keys, counters and the queue
+        const int64_t ctas = 2 * std::min<int64_t>(m->num_sms / 2, std::max<int64_t>(a.n_tiles, 1));
+        const size_t rows = static_cast<size_t>(ctas) * 2 * (m->n_mb ? m->n_mb : 1) * 2 * (m->N / 4);
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(ext ring)");
+        svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N / 4));
+        if (s != SVN_OK) return s;
+        a.ext_ring = ext;
+        a.xq_wq = m->d_wq_bf;
+        a.xq_base = m->d_mbbase_bf;
+        a.xq_wx = m->d_wxslots_bf;
+        SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, nullptr, keys, counters, n_keys,
+                                   sched, st),
+                 "motion_ext kernel (resets)");
+        ++g_launches;
+        return SVN_OK;
+    }
+    a.ext_ring = nullptr;
     const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * m->N;
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(motion ext)");
     svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N == 256 ? m->N / 2 : m->N / 4));
     if (s != SVN_OK) return s;
-    unsigned int* sched = nullptr;  // dynamic tile counter of the width-512 kernel, zeroed by K0
-    SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&sched), sizeof(unsigned int)), "cudaMallocAsync(tile counter)");
-    a.sched = sched;
     SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, ext, keys, counters, n_keys, sched, st),
              "motion_ext kernel");
     ++g_launches;

@@ -63,6 +63,13 @@ struct FusedArgs {
     int exact;                 // fp32 exact order (no q fold)
     int tile_rows;             // rows per work item the host cut the tiles with (SIMT: 128/64, or 32)
     unsigned int* sched;       // width-512 bf16 kernel: dynamic tile counter (zeroed by K0)
+    // width-512 bf16 kernel: the per-motion K=16 extension rows (folded bias + x-part splits)
+    // are built inside the fused kernel, by each CTA's output warp for the tile two ahead, into a
+    // per-CTA ring of two tile slots (L2-resident) that tmap_xq views; null = the K0-built stream
+    uint8_t* ext_ring;
+    const float* xq_wq;    // [n_mb][2dof][N] q-columns of the concat layers (bf16 path's folded params)
+    const float* xq_base;  // [n_mb][N] their bias
+    const float* xq_wx;    // [n_mb][3][N] their x-columns
     // outputs
     unsigned long long* keys;  // [M] packed (orderable(delta) << 32 | index), or null
     unsigned int* counters;    // [M] tiles done, for the fused finaliser, or null

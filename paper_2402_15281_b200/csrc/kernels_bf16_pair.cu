@@ -54,7 +54,7 @@ struct PairCfg {
     static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
     static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
     static constexpr int TQ = 8;                     // tile queue entries (dynamic schedule)
-    static constexpr uint32_t SMEM = OFF_BAR + 384;  // 20 + TQ barriers, TQ tile ids, TMEM slot
+    static constexpr uint32_t SMEM = OFF_BAR + 384;  // 22 + TQ barriers, TQ tile ids, TMEM slot
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(COLS % 32 == 0, "epilogue works in 32-column TMEM loads");
 };
@@ -216,7 +216,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     uint64_t* out_full = ax_full + 2;           // [tile parity] each CTA: dotbuf holds a finished tile (8 warps)
     uint64_t* out_empty = out_full + 2;         // [tile parity] each CTA: output warp has read dotbuf
     uint64_t* tq_full = out_empty + 2;          // [TQ] each CTA: tile queue entry published
-    long long* tq = reinterpret_cast<long long*>(tq_full + C::TQ);  // [TQ] each CTA: tile ids
+    uint64_t* xq_full = tq_full + C::TQ;        // [tile parity] each CTA: ext ring slot written (output warp)
+    long long* tq = reinterpret_cast<long long*>(xq_full + 2);  // [TQ] each CTA: tile ids
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + C::TQ);
 
     const int warp = threadIdx.x >> 5;
@@ -249,6 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             mbar_init(&out_empty[j], 1);
         }
         for (int q = 0; q < C::TQ; ++q) mbar_init(&tq_full[q], 1);
+        for (int j = 0; j < 2; ++j) mbar_init(&xq_full[j], 1);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < N; i += blockDim.x) wo_s[i] = a.wo[i];
@@ -281,12 +283,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             auto advance = [&]() {
                 if (++stage == C::STAGES) stage = 0, phase ^= 1u;
             };
+            uint32_t xq_ph[2] = {0u, 0u};
             for (int64_t k = 0;; ++k) {
                 const int64_t t = tile_at(k);
                 if (t >= a.n_tiles) break;
                 int32_t motion, nrows;
                 int64_t pbase, obase;
                 tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+                const int xb = static_cast<int>(k & 1);
+                if (a.ext_ring) {  // this tile's extension rows are in ring slot xb once the output warp says so
+                    mbar_wait(&xq_full[xb], xq_ph[xb]);
+                    xq_ph[xb] ^= 1u;
+                }
                 int64_t wrow = 0;  // 128-byte row of the weight stream
                 for (int l = 0; l < L; ++l) {
                     const LayerDev& ld = a.layer[l];
@@ -298,7 +306,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                             const uint32_t fb = full0 + stage * 8u;
                             uint8_t* dst = stages + stage * C::CHUNK;
                             if (ld.ext == 2) {
-                                const int64_t blob = ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
+                                const int64_t blob =
+                                    a.ext_ring ? ((static_cast<int64_t>(blockIdx.x) * 2 + xb) * a.n_mb + ld.mb_slot) * 2 + nh
+                                               : ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
                                 tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * C::BR), fb, pol);
                             } else {
                                 const int64_t r0 = ld.ext_row + (nh * 2 + rank) * C::BR;
@@ -498,6 +508,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
         };
+        // The per-motion extension rows of this CTA's 2 x BR columns per concat slot, for the tile
+        // two ahead, into ring slot b (free: every MMA of the tile that used it has completed).
+        // Same arithmetic as motion_ext_kernel (b_m = b + W_q . z_q in fp32, q0 then q1, then the
+        // bf16 hi/lo splits); skipped when slot b already holds the tile's motion.
+        int32_t ring_motion[2] = {-1, -1};
+        auto write_ext = [&](int64_t t, int b) {
+            if (!a.ext_ring) return;
+            int32_t motion, nrows;
+            int64_t pbase, obase;
+            tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
+            if (motion != ring_motion[b]) {
+                ring_motion[b] = motion;
+                const int nq = 2 * a.dof;
+                float zq[kMaxIn];
+#pragma unroll
+                for (int j = 0; j < kMaxIn - 3; ++j)
+                    zq[j] = j < nq ? __fmul_rn(__fsub_rn(a.q01[static_cast<int64_t>(motion) * nq + j], a.shift[3 + j]),
+                                               a.scale[3 + j])
+                                   : 0.f;
+                for (int sl = 0; sl < a.n_mb; ++sl) {
+                    const float* w = a.xq_wq + static_cast<int64_t>(sl) * nq * N;
+                    const float* bb = a.xq_base + static_cast<int64_t>(sl) * N;
+                    const float* wx = a.xq_wx + static_cast<int64_t>(sl) * 3 * N;
+#pragma unroll 2
+                    for (int i = 0; i < 8; ++i) {
+                        const int nh = i >> 2;
+                        const uint32_t rr = static_cast<uint32_t>((i & 3) * 32) + lane;
+                        const int n = nh * C::NH + static_cast<int>(rank) * C::BR + static_cast<int>(rr);
+                        float acc = bb[n];
+                        for (int kq = 0; kq < nq; ++kq) acc = __fmaf_rn(zq[kq], w[kq * N + n], acc);
+                        __nv_bfloat16 bh, bl, h0, l0, h1, l1, h2, l2;
+                        split_bf16(acc, bh, bl);
+                        split_bf16(wx[n], h0, l0);
+                        split_bf16(wx[N + n], h1, l1);
+                        split_bf16(wx[2 * N + n], h2, l2);
+                        const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
+                        __align__(16) __nv_bfloat16 v[16] = {bh, bl, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
+                        uint8_t* dst = a.ext_ring +
+                                       (((static_cast<int64_t>(blockIdx.x) * 2 + b) * a.n_mb + sl) * 2 + nh) * C::BR * 32;
+                        *reinterpret_cast<uint4*>(dst + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
+                        *reinterpret_cast<uint4*>(dst + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+                    }
+                }
+                fence_proxy_async_global();  // generic-proxy writes -> the producer's TMA reads
+                __threadfence();
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xq_full[b]);
+        };
         // the pair's scheduler: lane 0 of the leader's output warp
         const bool sched = rank == 0 && lane == 0;
         long long last_pub = 0;
@@ -518,6 +577,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             if (t < a.n_tiles) {
                 load_points(t);
                 store_ax(b);
+                write_ext(t, b);
             }
         }
         for (int64_t k = 0;; ++k) {
@@ -572,6 +632,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     }
                 }
             }
+            // tile t + 2's extension rows (needed when the producer reaches it, about a tile from now)
+            if (next) write_ext(t2, b);
             pe_x += prof_clock() - c0;
         }
         if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
@@ -625,7 +687,7 @@ __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N,
         keys[m] = ~0ull;
         counters[m] = 0u;
     }
-    if (slot >= n_mb) return;
+    if (slot >= n_mb || ext == nullptr) return;  // no ext: the fused kernel builds the rows itself
     __shared__ float zq[kMaxIn];
     const int nq = 2 * dof;
     if (threadIdx.x < nq) {
@@ -675,8 +737,8 @@ cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* 
         qn.shift[k] = a.shift[3 + k];
         qn.scale[k] = a.scale[3 + k];
     }
-    dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
-    motion_ext_kernel<<<grid, 256, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn,
+    dim3 grid(static_cast<unsigned>(a.M), (a.n_mb > 0 && ext) ? a.n_mb : 1);
+    motion_ext_kernel<<<grid, ext ? 256 : 32, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn,
                                              keys_init, counters_init, n_keys, a.N == 256 ? 1 : 0, sched_reset);
     return cudaGetLastError();
 }
