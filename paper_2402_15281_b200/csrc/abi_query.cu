@@ -112,23 +112,39 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
     unsigned int* sched = nullptr;  // dynamic tile counter of the width-512 kernel, zeroed by K0
     SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&sched), sizeof(unsigned int)), "cudaMallocAsync(tile counter)");
     a.sched = sched;
-    static const bool k0_ext = [] {  // A/B hook: the K0-built per-motion stream at width 512 too
-        const char* e = std::getenv("SVN_BF16_K0_EXT");
-        return e && e[0] == '1';
+    {
+        // chunks of 4 consecutive tiles per claim once every pair has >= 32 tiles: the ext ring is
+        // rebuilt about once per chunk; the end-of-kernel spread grows by at most 3 tiles (~0.1 ms)
+        static const int g_env = [] {
+            const char* e = std::getenv("SVN_TILE_GROUP");  // A/B hook
+            return e ? std::atoi(e) : 0;
+        }();
+        const int64_t pairs = std::max<int64_t>(1, m->num_sms / 2);
+        a.tile_group = g_env > 0 ? g_env : (a.n_tiles >= pairs * 32 ? 4 : 1);
+    }
+    static const int ext_mode = [] {  // test / A-B hook: SVN_BF16_EXT=k0 | ring (default: by size)
+        const char* e = std::getenv("SVN_BF16_EXT");
+        return !e ? 0 : std::strcmp(e, "k0") == 0 ? 1 : std::strcmp(e, "ring") == 0 ? 2 : 0;
     }();
-    if (m->N == 512 && !k0_ext) {
-        // width 512: the fused kernel's output warps build each tile's extension rows in a ring of
-        // two tile slots per CTA (grid x 2 x n_mb x 2 n-halves x N/4 rows x 32 B: 4.8 MB on c3,
-        // L2-resident) — no per-motion stream in HBM; K0 only resets keys, counters and the queue
+    const size_t stream_bytes = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * m->N * 32;
+    // width 512, a per-motion stream that would not stay in L2 (> 16 MB: c3, c4, c5): the fused
+    // kernel's output warps build each tile's extension rows in a ring of three tile slots per CTA
+    // (grid x 3 x n_mb x 2 n-halves x N/4 rows x 32 B: 7.3 MB on c3, L2-resident) — no per-motion
+    // stream in HBM; K0 only resets keys, counters and the queue.  Small batches (one motion per
+    // call, the reference's predict_min_distance) keep K0's parallel build: its rows stay in L2
+    // and the fused kernel's first tiles do not wait for an output warp to build them.
+    const bool ring = ext_mode == 2 || (ext_mode == 0 && stream_bytes > (size_t(16) << 20));
+    if (m->N == 512 && ring) {
         const int64_t ctas = 2 * std::min<int64_t>(m->num_sms / 2, std::max<int64_t>(a.n_tiles, 1));
-        const size_t rows = static_cast<size_t>(ctas) * 2 * (m->n_mb ? m->n_mb : 1) * 2 * (m->N / 4);
+        const size_t rows = static_cast<size_t>(ctas) * 3 * (m->n_mb ? m->n_mb : 1) * 2 * (m->N / 4);  // 3 slots
         SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(ext ring)");
         svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N / 4));
         if (s != SVN_OK) return s;
         a.ext_ring = ext;
         a.xq_wq = m->d_wq_bf;
         a.xq_base = m->d_mbbase_bf;
-        a.xq_wx = m->d_wxslots_bf;
+        SVN_CUDA(launch_ext_ring_init(ext, ctas, m->n_mb ? m->n_mb : 1, m->N, m->d_wxslots_bf, st), "ext ring init");
+        ++g_launches;
         SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, nullptr, keys, counters, n_keys,
                                    sched, st),
                  "motion_ext kernel (resets)");

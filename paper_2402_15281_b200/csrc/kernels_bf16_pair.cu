@@ -54,6 +54,7 @@ struct PairCfg {
     static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
     static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
     static constexpr int TQ = 8;                     // tile queue entries (dynamic schedule)
+    static constexpr int XR = 3;                     // ext ring slots per CTA (tiles in flight)
     static constexpr uint32_t SMEM = OFF_BAR + 384;  // 22 + TQ barriers, TQ tile ids, TMEM slot
     static_assert(SMEM <= 232448, "shared memory budget");
     static_assert(COLS % 32 == 0, "epilogue works in 32-column TMEM loads");
@@ -197,6 +198,57 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
     }
 }
 
+// The extension rows of one motion for this CTA's 2 x BR columns of every concat slot (four per
+// lane per n-half) into `ring` ([slot][n-half] blobs of BR rows): b_m = b + W_q . z_q in fp32 with
+// motion_ext_kernel's arithmetic (z_q = (q - shift) * scale; bias first, then q0, q1 in order),
+// then its bf16 hi/lo split into the row's first word.  NQ = 2 * dof at compile time
+// (0: runtime), so all 4 x NQ weight loads of an n-half are independent and issued together.
+template <int BR, int NH, int NQ>
+__device__ __noinline__ void build_ext(const FusedArgs& a, int32_t motion, uint8_t* ring, uint32_t rank, uint32_t lane) {
+    const int N = 2 * NH;
+    const int nq = NQ > 0 ? NQ : 2 * a.dof;
+    float zq[NQ > 0 ? NQ : kMaxIn];
+#pragma unroll
+    for (int j = 0; j < (NQ > 0 ? NQ : kMaxIn - 3); ++j)
+        zq[j] = j < nq ? __fmul_rn(__fsub_rn(a.q01[static_cast<int64_t>(motion) * nq + j], a.shift[3 + j]), a.scale[3 + j])
+                       : 0.f;
+    for (int sl = 0; sl < a.n_mb; ++sl) {
+        const float* __restrict__ w = a.xq_wq + static_cast<int64_t>(sl) * nq * N;
+        const float* __restrict__ bb = a.xq_base + static_cast<int64_t>(sl) * N;
+    #pragma unroll
+        for (int nh = 0; nh < 2; ++nh) {
+            int n[4];
+            float acc[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                n[j] = nh * NH + static_cast<int>(rank) * BR + j * 32 + static_cast<int>(lane);
+                acc[j] = __ldg(bb + n[j]);
+            }
+            if constexpr (NQ > 0) {
+#pragma unroll
+                for (int kq = 0; kq < NQ; ++kq)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] = __fmaf_rn(zq[kq], __ldg(w + kq * N + n[j]), acc[j]);
+            } else {
+                for (int kq = 0; kq < nq; ++kq)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[j] = __fmaf_rn(zq[kq], __ldg(w + kq * N + n[j]), acc[j]);
+            }
+            // only the b_m word of each row changes with the motion: the x-column splits of the
+            // row (model constants) were written once per call by ext_ring_init_kernel
+            uint8_t* blob = ring + (sl * 2 + nh) * BR * 32;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                __nv_bfloat16 bh, bl;
+                split_bf16(acc[j], bh, bl);
+                const __nv_bfloat162 w2 = __halves2bfloat162(bh, bl);
+                const uint32_t rr = static_cast<uint32_t>(j * 32) + lane;
+                *reinterpret_cast<uint32_t*>(blob + ext_offset(rr, 0)) = *reinterpret_cast<const uint32_t*>(&w2);
+            }
+        }
+    }
+}
+
 template <int N>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS, 1)
     fused_bf16_pair_kernel(const __grid_constant__ FusedArgs a) {
@@ -216,8 +268,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     uint64_t* out_full = ax_full + 2;           // [tile parity] each CTA: dotbuf holds a finished tile (8 warps)
     uint64_t* out_empty = out_full + 2;         // [tile parity] each CTA: output warp has read dotbuf
     uint64_t* tq_full = out_empty + 2;          // [TQ] each CTA: tile queue entry published
-    uint64_t* xq_full = tq_full + C::TQ;        // [tile parity] each CTA: ext ring slot written (output warp)
-    long long* tq = reinterpret_cast<long long*>(xq_full + 2);  // [TQ] each CTA: tile ids
+    uint64_t* xq_full = tq_full + C::TQ;        // [XR] each CTA: ext ring slot written (output warp)
+    long long* tq = reinterpret_cast<long long*>(xq_full + C::XR);  // [TQ] each CTA: tile ids
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq + C::TQ);
 
     const int warp = threadIdx.x >> 5;
@@ -250,7 +302,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             mbar_init(&out_empty[j], 1);
         }
         for (int q = 0; q < C::TQ; ++q) mbar_init(&tq_full[q], 1);
-        for (int j = 0; j < 2; ++j) mbar_init(&xq_full[j], 1);
+        for (int j = 0; j < C::XR; ++j) mbar_init(&xq_full[j], 1);
         fence_mbar_init();
     }
     for (int i = threadIdx.x; i < N; i += blockDim.x) wo_s[i] = a.wo[i];
@@ -283,17 +335,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             auto advance = [&]() {
                 if (++stage == C::STAGES) stage = 0, phase ^= 1u;
             };
-            uint32_t xq_ph[2] = {0u, 0u};
+            uint32_t xq_ph = 0u;  // phase bit per ring slot
             for (int64_t k = 0;; ++k) {
                 const int64_t t = tile_at(k);
                 if (t >= a.n_tiles) break;
                 int32_t motion, nrows;
                 int64_t pbase, obase;
                 tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
-                const int xb = static_cast<int>(k & 1);
+                const int xb = static_cast<int>(k % C::XR);
                 if (a.ext_ring) {  // this tile's extension rows are in ring slot xb once the output warp says so
-                    mbar_wait(&xq_full[xb], xq_ph[xb]);
-                    xq_ph[xb] ^= 1u;
+                    mbar_wait(&xq_full[xb], (xq_ph >> xb) & 1u);
+                    xq_ph ^= 1u << xb;
                 }
                 int64_t wrow = 0;  // 128-byte row of the weight stream
                 for (int l = 0; l < L; ++l) {
@@ -307,7 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                             uint8_t* dst = stages + stage * C::CHUNK;
                             if (ld.ext == 2) {
                                 const int64_t blob =
-                                    a.ext_ring ? ((static_cast<int64_t>(blockIdx.x) * 2 + xb) * a.n_mb + ld.mb_slot) * 2 + nh
+                                    a.ext_ring ? ((static_cast<int64_t>(blockIdx.x) * C::XR + xb) * a.n_mb + ld.mb_slot) * 2 + nh
                                                : ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
                                 tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * C::BR), fb, pol);
                             } else {
@@ -509,10 +561,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);
         };
         // The per-motion extension rows of this CTA's 2 x BR columns per concat slot, for the tile
-        // two ahead, into ring slot b (free: every MMA of the tile that used it has completed).
+        // three ahead, into ring slot b (free: every MMA of the tile that used it has completed).
         // Same arithmetic as motion_ext_kernel (b_m = b + W_q . z_q in fp32, q0 then q1, then the
         // bf16 hi/lo splits); skipped when slot b already holds the tile's motion.
-        int32_t ring_motion[2] = {-1, -1};
+        int32_t ring_motion[C::XR];
+#pragma unroll
+        for (int j = 0; j < C::XR; ++j) ring_motion[j] = -1;
         auto write_ext = [&](int64_t t, int b) {
             if (!a.ext_ring) return;
             int32_t motion, nrows;
@@ -520,36 +574,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
             if (motion != ring_motion[b]) {
                 ring_motion[b] = motion;
-                const int nq = 2 * a.dof;
-                float zq[kMaxIn];
-#pragma unroll
-                for (int j = 0; j < kMaxIn - 3; ++j)
-                    zq[j] = j < nq ? __fmul_rn(__fsub_rn(a.q01[static_cast<int64_t>(motion) * nq + j], a.shift[3 + j]),
-                                               a.scale[3 + j])
-                                   : 0.f;
-                for (int sl = 0; sl < a.n_mb; ++sl) {
-                    const float* w = a.xq_wq + static_cast<int64_t>(sl) * nq * N;
-                    const float* bb = a.xq_base + static_cast<int64_t>(sl) * N;
-                    const float* wx = a.xq_wx + static_cast<int64_t>(sl) * 3 * N;
-#pragma unroll 2
-                    for (int i = 0; i < 8; ++i) {
-                        const int nh = i >> 2;
-                        const uint32_t rr = static_cast<uint32_t>((i & 3) * 32) + lane;
-                        const int n = nh * C::NH + static_cast<int>(rank) * C::BR + static_cast<int>(rr);
-                        float acc = bb[n];
-                        for (int kq = 0; kq < nq; ++kq) acc = __fmaf_rn(zq[kq], w[kq * N + n], acc);
-                        __nv_bfloat16 bh, bl, h0, l0, h1, l1, h2, l2;
-                        split_bf16(acc, bh, bl);
-                        split_bf16(wx[n], h0, l0);
-                        split_bf16(wx[N + n], h1, l1);
-                        split_bf16(wx[2 * N + n], h2, l2);
-                        const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
-                        __align__(16) __nv_bfloat16 v[16] = {bh, bl, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
-                        uint8_t* dst = a.ext_ring +
-                                       (((static_cast<int64_t>(blockIdx.x) * 2 + b) * a.n_mb + sl) * 2 + nh) * C::BR * 32;
-                        *reinterpret_cast<uint4*>(dst + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
-                        *reinterpret_cast<uint4*>(dst + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
-                    }
+                uint8_t* ring = a.ext_ring + (static_cast<int64_t>(blockIdx.x) * C::XR + b) * a.n_mb * 2 * C::BR * 32;
+                switch (2 * a.dof) {  // compile-time q width: every load of a slot in flight at once
+                    case 12: build_ext<C::BR, C::NH, 12>(a, motion, ring, rank, lane); break;
+                    case 14: build_ext<C::BR, C::NH, 14>(a, motion, ring, rank, lane); break;
+                    case 4: build_ext<C::BR, C::NH, 4>(a, motion, ring, rank, lane); break;
+                    case 6: build_ext<C::BR, C::NH, 6>(a, motion, ring, rank, lane); break;
+                    case 8: build_ext<C::BR, C::NH, 8>(a, motion, ring, rank, lane); break;
+                    case 10: build_ext<C::BR, C::NH, 10>(a, motion, ring, rank, lane); break;
+                    default: build_ext<C::BR, C::NH, 0>(a, motion, ring, rank, lane); break;
                 }
                 fence_proxy_async_global();  // generic-proxy writes -> the producer's TMA reads
                 __threadfence();
@@ -568,25 +601,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             mbar_arrive_cluster(mapa_shared(smem_u32(&tq_full[q]), 1));
             last_pub = t;
         };
+        // Tiles are handed out in chunks of G consecutive ids (one motion, mostly), so the ext ring
+        // is rebuilt about once per chunk rather than per tile: the pair's first S = ceil(XR/G)
+        // chunks are static (pair, pair + npairs, ...), later ones come from the counter.
+        const int G = a.tile_group > 0 ? a.tile_group : 1;
+        const int S = (C::XR + G - 1) / G;
+        int s_used = 0, c_left = 0;
+        long long c_next = 0;
+        auto next_tile = [&]() -> long long {
+            if (last_pub >= a.n_tiles) return last_pub;  // end marker, repeated
+            if (c_left == 0) {
+                const long long c = s_used < S ? pair + static_cast<long long>(s_used++) * npairs
+                                               : static_cast<long long>(S) * npairs +
+                                                     static_cast<long long>(atomicAdd(a.sched, 1u));
+                c_next = c * G;
+                c_left = G;
+            }
+            --c_left;
+            const long long t = c_next++;
+            return t < a.n_tiles ? t : a.n_tiles;
+        };
         if (sched) {
-            publish(0, pair);
-            publish(1, pair + npairs);
+            for (int j = 0; j < C::XR; ++j) publish(j, next_tile());
         }
         for (int b = 0; b < 2; ++b) {
             const int64_t t = tile_at(b);
             if (t < a.n_tiles) {
                 load_points(t);
                 store_ax(b);
-                write_ext(t, b);
             }
+        }
+        for (int j = 0; j < C::XR; ++j) {
+            const int64_t t = tile_at(j);
+            if (t < a.n_tiles) write_ext(t, j);
         }
         for (int64_t k = 0;; ++k) {
             const int64_t t = tile_at(k);
             if (t >= a.n_tiles) break;
             const int b = static_cast<int>(k & 1);
-            if (sched)  // tile k+2: the next unclaimed one, or the end marker once the counter ran out
-                publish(k + 2, last_pub >= a.n_tiles ? last_pub
-                                                     : 2 * npairs + static_cast<long long>(atomicAdd(a.sched, 1u)));
+            if (sched)  // tile k+XR: the next unclaimed one, or the end marker once the counter ran out
+                publish(k + C::XR, next_tile());
             __syncwarp();
             const int64_t t2 = tile_at(k + 2);
             const bool next = t2 < a.n_tiles;
@@ -632,8 +686,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     }
                 }
             }
-            // tile t + 2's extension rows (needed when the producer reaches it, about a tile from now)
-            if (next) write_ext(t2, b);
+            // tile k+XR's extension rows into the slot tile k just released (needed when the producer
+            // reaches that tile, about two tiles from now)
+            {
+                const int64_t t3 = tile_at(k + C::XR);
+                if (t3 < a.n_tiles) write_ext(t3, static_cast<int>(k % C::XR));
+            }
             pe_x += prof_clock() - c0;
         }
         if (a.prof && lane == 0 && rank == 0) atomicAdd(a.prof + kProfEpiAx, pe_x);
@@ -665,6 +723,41 @@ cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t
         case 512: return launch_pair_n<512>(a, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// The motion-independent part of every ext ring row (K slots 2..15: the slot's x-column splits;
+// slots 0..1, the b_m word, are written by the fused kernel per motion).  One thread per row of
+// the ring [cta slot][mb slot][n-half] blobs of N/4 rows; column n of a row follows the pair
+// kernel's blob order (n-half, CTA rank within the pair).
+__global__ void ext_ring_init_kernel(uint8_t* __restrict__ ring, int64_t n_blobs, int n_mb, int N,
+                                     const float* __restrict__ wx_slots, int xr) {
+    const int BR = N / 4, NH = N / 2;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (row >= n_blobs * BR) return;
+    const int64_t blob = row / BR;
+    const uint32_t rr = static_cast<uint32_t>(row % BR);
+    const int nh = static_cast<int>(blob % 2);
+    const int sl = static_cast<int>((blob / 2) % n_mb);
+    const int64_t cta = blob / (2 * n_mb) / xr;
+    const int n = nh * NH + static_cast<int>(cta & 1) * BR + static_cast<int>(rr);
+    const float* wx = wx_slots + static_cast<int64_t>(sl) * 3 * N;
+    __nv_bfloat16 h0, l0, h1, l1, h2, l2;
+    split_bf16(wx[n], h0, l0);
+    split_bf16(wx[N + n], h1, l1);
+    split_bf16(wx[2 * N + n], h2, l2);
+    const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
+    __align__(16) __nv_bfloat16 v[16] = {z, z, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
+    uint8_t* base = ring + blob * BR * 32;
+    *reinterpret_cast<uint4*>(base + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
+    *reinterpret_cast<uint4*>(base + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+}
+
+cudaError_t launch_ext_ring_init(uint8_t* ring, int64_t ctas, int n_mb, int N, const float* wx_slots, cudaStream_t st) {
+    constexpr int xr = PairCfg<512>::XR;
+    const int64_t n_blobs = ctas * xr * n_mb * 2;
+    const int64_t rows = n_blobs * (N / 4);
+    ext_ring_init_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(ring, n_blobs, n_mb, N, wx_slots, xr);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------- K0 (bf16) -----

@@ -1,6 +1,7 @@
 """Width-512 bf16: the per-motion extension rows built inside the fused kernel (output warps,
 per-CTA ring of two tile slots) give exactly the bits of the K0-built per-motion stream
-(SVN_BF16_K0_EXT=1, the round-1 path) — same fp32 fold, same splits, only where they live.
+(SVN_BF16_EXT=k0, the round-1 path; the ring is forced with SVN_BF16_EXT=ring — by default it is
+used only when the per-motion stream would exceed L2, > 16 MB) — same fp32 fold, same splits, only where they live.
 Covers dense queries with many tiles per motion (the ring slot is reused across tiles of a
 motion), tiny clouds (every tile a new motion), forward_eval with mixed motions (tile table),
 a trained-like Fig. 2 net with BN and non-identity normaliser, and the DeepSDF second concat."""
@@ -29,7 +30,8 @@ for key, M, P in (("c3", 5, 3000), ("c3", 40, 100), ("c4", 3, 2500)):
     m = S.Model(w.program, S.init_params(w.program, 7, w.bound))
     r = m.query_min(pts, q, w.margin, precision="bf16", per_point=True)
     out[f"{key}_{M}_pp"] = r.per_point; out[f"{key}_{M}_min"] = r.min; out[f"{key}_{M}_arg"] = r.argmin
-    rows = np.concatenate([pts[:600], q[np.arange(600) % M]], axis=1).astype(np.float32)
+    nr = min(600, P)
+    rows = np.concatenate([pts[:nr], q[np.arange(nr) % M]], axis=1).astype(np.float32)
     out[f"{key}_{M}_fwd"] = m.forward_eval(rows, precision="bf16")
 Z, names = G.load()
 g, prog, _, p = G.params(Z, "fig2_5x512_mknorm")
@@ -40,9 +42,7 @@ np.savez(sys.argv[2], **out)
 
 def _run(tmp_path, k0):
     env = dict(os.environ)
-    env.pop("SVN_BF16_K0_EXT", None)
-    if k0:
-        env["SVN_BF16_K0_EXT"] = "1"
+    env["SVN_BF16_EXT"] = "k0" if k0 else "ring"
     out = tmp_path / ("k0.npz" if k0 else "ring.npz")
     r = subprocess.run([sys.executable, "-c", SCRIPT, str(ROOT), str(out)], env=env, capture_output=True, text=True,
                        timeout=600)
