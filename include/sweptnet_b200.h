@@ -70,7 +70,9 @@ typedef enum {
  *              per-motion q-fold.  As close to the exact value as fp32 arithmetic, but not
  *              in the reference's rounding order: per-point delta within the stated bound
  *              of tests/golden/fp32_split_bounds.json (UNSUPPORTED at other widths or when
- *              a weight exceeds 1e4). */
+ *              a weight exceeds 1e4).  A row whose hidden activation reaches the fp16
+ *              range (|h| >= 65520) is reported as delta = -inf: its motion's min is -inf
+ *              and its class "not free" (handed to the exact checker), never dropped. */
 typedef enum {
     SVN_PREC_BF16 = 0,
     SVN_PREC_FP32 = 1,
@@ -126,6 +128,12 @@ SVN_API svn_status svn_model_create(const svn_model_desc* desc, const float* par
 SVN_API svn_status svn_model_load_checkpoint(const char* path, int32_t device, svn_model** out);
 
 SVN_API svn_status svn_model_destroy(svn_model* model);
+
+/* The layer program a model runs (width, dof, layers) — e.g. of a model read from a
+ * checkpoint, whose header fixes it (nn.cpp:535-548: n_blocks, block_dim, input_dim).
+ * `layers` may be null (sizes only); else it must hold `capacity` >= n_layers entries. */
+SVN_API svn_status svn_model_get_program(const svn_model* model, int32_t* width, int32_t* dof,
+                                         int32_t* n_layers, svn_layer* layers, int32_t capacity);
 
 /* Batched proxy, device-resident inputs (pointers are device memory):
  *   points  float [P x 3]            (x, y, z)

@@ -110,10 +110,15 @@ public:
         check(svn_model_load_checkpoint(path.c_str(), device, &h));
         Model m;
         m.h_.reset(h, svn_model_destroy);
+        int32_t width = 0, dof = 0, n = 0;
+        check(svn_model_get_program(h, &width, &dof, &n, nullptr, 0));
+        m.prog_ = Program{width, dof, std::vector<svn_layer>(static_cast<size_t>(n))};
+        check(svn_model_get_program(h, &width, &dof, &n, m.prog_.layers.data(), n));
         return m;
     }
     const svn_model* handle() const { return h_.get(); }
     int dof() const { return prog_.dof; }
+    const Program& program() const { return prog_; }
 
 private:
     Model() = default;

@@ -102,6 +102,7 @@ def _finish(L):
         "svn_model_create": (C.c_int, [desc_p, P, I64, I32, C.POINTER(VP)]),
         "svn_model_load_checkpoint": (C.c_int, [C.c_char_p, I32, C.POINTER(VP)]),
         "svn_model_destroy": (C.c_int, [VP]),
+        "svn_model_get_program": (C.c_int, [VP, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), P, I32]),
         "svn_query_min_device": (C.c_int, [VP, C.c_int, P, I64, P, I64, D, P, P, P, P, VP]),
         "svn_query_min": (C.c_int, [VP, C.c_int, P, I64, P, I64, D, P, P, P, P]),
         "svn_keys_init_device": (C.c_int, [P, I64, VP]),
@@ -136,7 +137,7 @@ def _finish(L):
 
 
 EXPORTED = ("svn_param_count", "svn_trainable_param_count", "svn_init_params", "svn_model_create",
-            "svn_model_load_checkpoint", "svn_model_destroy", "svn_query_min_device", "svn_query_min",
+            "svn_model_load_checkpoint", "svn_model_destroy", "svn_model_get_program", "svn_query_min_device", "svn_query_min",
             "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
             "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_gcc_min_distance",
             "svn_gcc_min_distance_device", "svn_gcc_nn_search", "svn_multi_create", "svn_multi_destroy",

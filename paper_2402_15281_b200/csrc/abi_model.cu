@@ -547,6 +547,19 @@ SVN_API svn_status svn_model_destroy(svn_model* m) {
     }
 }
 
+SVN_API svn_status svn_model_get_program(const svn_model* m, int32_t* width, int32_t* dof, int32_t* n_layers,
+                                         svn_layer* layers, int32_t capacity) {
+    if (!m || !width || !dof || !n_layers) return fail(SVN_ERR_INVALID_ARGUMENT, "get_program: null argument");
+    *width = m->N;
+    *dof = m->dof;
+    *n_layers = m->L;
+    if (layers) {
+        if (capacity < m->L) return fail(SVN_ERR_INVALID_ARGUMENT, "get_program: layer buffer too small");
+        for (int i = 0; i < m->L; ++i) layers[i] = m->layers[i];
+    }
+    return SVN_OK;
+}
+
 }  // extern "C"
 
 extern "C" {

@@ -58,6 +58,12 @@ __host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
     return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
+// |x| >= 65520 rounds to an fp16 infinity: such an activation cannot be held in the
+// (hi, lo') planes.  The row is then reported as delta = -inf (OVERFLOW_DELTA): its
+// motion's min is -inf and its class "not free", i.e. it is handed to the exact checker
+// (the safe side of collision.cpp:68) instead of silently dropping out of the min as a NaN.
+constexpr float kF16Overflow = 65520.f;
+
 __device__ __forceinline__ void split(float x, __half& hi, __half& lo) {
     hi = __float2half_rn(x);
     lo = __float2half_rn((x - __half2float(hi)) * LO_SCALE);
@@ -82,7 +88,7 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 // 32 output columns of one row: v (fp32, already main + corr/2048) -> act / affine /
 // residual -> next layer's (hi, lo') planes, or the output dot on the last layer.
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot) {
+                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot, bool& ovf) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (act) {
@@ -134,6 +140,7 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         for (int p = 0; p < 4; ++p) {
             // paired split: hi = f16x2(x0, x1); lo' = f16x2((x - hi) * 2^11)
             const float x0 = v[8 * u + 2 * p], x1 = v[8 * u + 2 * p + 1];
+            ovf |= fmaxf(fabsf(x0), fabsf(x1)) >= kF16Overflow;  // fp16(x) would be +-inf
             const __half2 h = __floats2half2_rn(x0, x1);
             const float2 hf = __half22float2(h);
             const __half2 lo = __floats2half2_rn((x0 - hf.x) * LO_SCALE, (x1 - hf.y) * LO_SCALE);
@@ -344,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         int64_t k = 0;
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
             float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
+            bool ovf = false;
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
@@ -370,12 +378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     uint32_t rm2[32], rc2[32];
                     tmem_ld32_async(tb + 32, rm2);
                     tmem_ld32_async(tb + 128 + 32, rc2);
-                    epi32(ld, l, last, v, j * NHO + ch * COLS, row, Ahi, Alo, wo_s, dot);
+                    epi32(ld, l, last, v, j * NHO + ch * COLS, row, Ahi, Alo, wo_s, dot, ovf);
                     tmem_wait_tied(rm2);
                     tmem_wait_tied(rc2);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc2[i]), LO_INV, __uint_as_float(rm2[i]));
-                    epi32(ld, l, last, v, j * NHO + ch * COLS + 32, row, Ahi, Alo, wo_s, dot);
+                    epi32(ld, l, last, v, j * NHO + ch * COLS + 32, row, Ahi, Alo, wo_s, dot, ovf);
                     pe_w += prof_clock() - c1;
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
@@ -390,7 +398,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                 mbar_wait(&out_empty[b], oe_ph[b]);
                 oe_ph[b] ^= 1u;
             }
-            dotbuf[(b * 2 + ch) * TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
+            dotbuf[(b * 2 + ch) * TM + row] = ovf ? -INFINITY : (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
             pe_o += prof_clock() - c3;
@@ -453,7 +461,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int r = q * 32 + static_cast<int>(lane);
-                delta[q] = (dotbuf[(b * 2) * TM + r] + dotbuf[(b * 2 + 1) * TM + r]) + a.bo;
+                const float p0 = dotbuf[(b * 2) * TM + r], p1 = dotbuf[(b * 2 + 1) * TM + r];
+                // either half saw an fp16 overflow: -inf, whatever the other half's partial holds
+                delta[q] = (p0 == -INFINITY || p1 == -INFINITY) ? -INFINITY : (p0 + p1) + a.bo;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_empty[b]);

@@ -1,5 +1,6 @@
 // Compiles the C++ host API against the C-ABI library and runs the reference-shaped
 // calls.  Built and run by tests/test_cpp_host_api.py (GPU); compiled-only on CPU.
+#include <cstdint>
 #include <cstdio>
 #include <stdexcept>
 
@@ -45,8 +46,26 @@ int main() {
     MultiModel mg(prog, params, {0, 0});
     const MinResult r = mg.query_min(pts, q01, 0.02, Precision::FP32_EXACT, Shard::MOTIONS);
     const bool multi_ok = mg.devices() == 2 && r.min.size() == 3 && static_cast<double>(r.min[0]) == mn && r.argmin[0] == idx;
-    std::printf("min %.9g idx %d | forward argmin %d %.9g | proxy %.9g | empty-cloud error %d | multi %.9g %d\n", mn,
-                idx, best, static_cast<double>(d[best]), proxy(1), threw ? 1 : 0, static_cast<double>(r.min[0]),
-                multi_ok ? 1 : 0);
-    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw && multi_ok) ? 0 : 1;
+    // the same parameters as an SVCKPT01 checkpoint (nn.cpp:482-520): the loaded Model knows its
+    // program from the header (dof, width, Fig. 2 layers) and predicts the same bits
+    const char* ck = "host_api_demo.svckpt";
+    {
+        FILE* f = std::fopen(ck, "wb");
+        const uint32_t hdr[4] = {1u, 3u, 256u, 15u};
+        std::fwrite("SVCKPT01", 1, 8, f);
+        std::fwrite(hdr, sizeof(uint32_t), 4, f);
+        std::fwrite(params.data(), sizeof(float), params.size(), f);
+        std::fclose(f);
+    }
+    Model mc = Model::load_checkpoint(ck);
+    std::remove(ck);
+    auto [mn_c, idx_c] = predict_min_distance(mc, cloud, mo);
+    const bool ckpt_ok = mc.dof() == 6 && mc.program().width == 256 && mc.program().layers.size() == 4 &&
+                         mc.program().layers[0].act == 0 && mc.program().layers[3].residual == 1 && mn_c == mn &&
+                         idx_c == idx;
+    std::printf("min %.9g idx %d | forward argmin %d %.9g | proxy %.9g | empty-cloud error %d | multi %.9g %d | "
+                "checkpoint dof %d ok %d\n", mn, idx, best, static_cast<double>(d[best]), proxy(1), threw ? 1 : 0,
+                static_cast<double>(r.min[0]), multi_ok ? 1 : 0, mc.dof(), ckpt_ok ? 1 : 0);
+    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw && multi_ok && ckpt_ok) ? 0
+                                                                                                               : 1;
 }

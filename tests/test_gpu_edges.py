@@ -66,6 +66,27 @@ def test_many_motions_few_points(prec):
     assert np.array_equal(r.argmin, r.per_point.argmin(axis=1))
 
 
+def test_fp32_split_fp16_overflow_is_reported_not_dropped():
+    """fp32_split holds activations as fp16 (hi, lo') planes: a row whose activation reaches
+    the fp16 infinity (|h| >= 65520) cannot be represented.  It must not silently drop out of
+    the min as a NaN (that could turn a colliding motion "free"); it is reported as
+    delta = -inf, so its motion's min is -inf and the class is "not free" (handed to the exact
+    checker).  Rows that stay in range keep their bound."""
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 29, w.bound)
+    pts, q = w.make(seed=29, motions=3, points=600)
+    big = pts.copy()
+    big[5] = (3.0e6, -2.0e6, 1.0e6)  # layer-0 pre-activations ~1e5-1e6: beyond fp16
+    m = S.Model(w.program, params)
+    r = m.query_min(big, q, w.margin, precision="fp32_split", per_point=True)
+    assert np.all(r.per_point[:, 5] == -np.inf)
+    assert np.all(r.min == -np.inf) and np.all(r.argmin == 5) and not r.free.any()
+    o = O.query_min(w.program, params, big, q, w.margin, per_point=True, threads=8)[3]
+    assert np.all(np.isfinite(o[:, 5]))  # the reference's fp32 path stays finite there
+    ok = np.delete(np.arange(600), 5)
+    assert np.abs(r.per_point[:, ok].astype(np.float64) - o[:, ok]).max() <= _tol("fp32_split", w.program)
+
+
 @pytest.mark.parametrize("prec", ["bf16", "fp32", "fp32_exact"])
 def test_nan_point_at_index_zero_sticks(prec):
     """nn.cpp:476-478: a NaN prediction at row 0 is returned; NaN elsewhere is skipped.
