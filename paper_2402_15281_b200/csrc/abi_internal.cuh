@@ -125,13 +125,61 @@ struct NvtxRange {
     ~NvtxRange() { nvtxRangePop(); }
 };
 
-// Scratch buffers freed on the stream when the call's kernels are done.
+// Per-thread device scratch for the synchronous host-buffer entry points: a call's scratch
+// (keys, counters, tile counter, extension rows) is carved from one block that is reused by
+// the thread's next call (the call syncs its stream before returning), so a small call makes
+// no allocation API calls.  A call that needs more falls back to stream-ordered allocation and
+// the block grows to fit before the next one.
+struct Arena {
+    int device = -1;
+    uint8_t* base = nullptr;
+    size_t cap = 0, used = 0, need = 0;
+    void begin() { used = need = 0; }
+    static constexpr size_t kMaxBytes = size_t(64) << 20;  // larger calls keep stream-ordered scratch
+    cudaError_t grow_to_need() {  // after the call's stream sync
+        if (need <= cap || need > kMaxBytes) return cudaSuccess;
+        release();
+        size_t n = size_t(1) << 20;
+        while (n < need) n <<= 1;
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), n);
+        if (e == cudaSuccess) cap = n;
+        return e;
+    }
+    void release() {
+        if (base) cudaFree(base);
+        base = nullptr;
+        cap = 0;
+    }
+    ~Arena() { release(); }
+};
+extern thread_local Arena* g_arena;  // set for the duration of a synchronous call (ArenaScope)
+
+struct ArenaScope {
+    Arena* prev;
+    explicit ArenaScope(Arena* a) : prev(g_arena) {
+        a->begin();
+        g_arena = a;
+    }
+    ~ArenaScope() { g_arena = prev; }
+};
+
+// Scratch buffers freed on the stream when the call's kernels are done (or carved from the
+// thread's arena inside an ArenaScope).
 struct Scratch {
     cudaStream_t st;
     std::vector<void*> ptrs;
     explicit Scratch(cudaStream_t s) : st(s) {}
     cudaError_t alloc(void** p, size_t bytes) {
-        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+        const size_t b = (bytes ? bytes : 16) + 255 & ~static_cast<size_t>(255);
+        if (Arena* a = g_arena) {
+            a->need += b;
+            if (a->used + b <= a->cap) {
+                *p = a->base + a->used;
+                a->used += b;
+                return cudaSuccess;
+            }
+        }
+        cudaError_t e = cudaMallocAsync(p, b, st);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }
@@ -181,6 +229,7 @@ struct Staging {
 };
 
 Staging& thread_staging(int device);
+Arena& thread_arena(int device);
 inline size_t align256(size_t x) { return (x + 255) & ~static_cast<size_t>(255); }
 void ensure_pool(int device);
 cudaStream_t thread_stream(int device);

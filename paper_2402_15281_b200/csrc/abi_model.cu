@@ -527,6 +527,13 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
                 uint8_t* dxm = nullptr;
                 if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
                 if ((st = encode_blob_map(&sa.tmap_xm, dxm, 32, xm.size() / 32, 128)) != SVN_OK) return cleanup_fail(st);
+                // expected truncation loss per MMA instruction, in ulps of the final main
+                // accumulator (calibrated); SVN_SPLIT_RZ overrides it (A/B hook)
+                static const float rz = [] {
+                    const char* e = std::getenv("SVN_SPLIT_RZ");
+                    return e ? static_cast<float>(std::atof(e)) : kSplitRzComp;
+                }();
+                sa.rz_comp = rz;
                 m->base_split = sa;
                 m->has_split = true;
             }

@@ -43,6 +43,16 @@ int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
 
 
 
+thread_local Arena* g_arena = nullptr;
+
+Arena& thread_arena(int device) {
+    thread_local Arena ar[8];
+    thread_local Arena other;
+    Arena& a = (device >= 0 && device < 8) ? ar[device] : other;
+    a.device = device;
+    return a;
+}
+
 Staging& thread_staging(int device) {
     thread_local Staging st[8];
     thread_local Staging other;
@@ -376,6 +386,70 @@ svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw
     return SVN_OK;
 }
 
+
+// svn_query_min / svn_predict_min_distance: inputs from host memory, outputs to host memory.
+// fill(pts, q) writes the call's float inputs into the pinned staging block; points/q01 are
+// the caller's float arrays (null for predict_min_distance, whose double inputs are converted
+// by fill), sent to the device directly when they are already pinned.
+template <class Fill>
+svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int64_t M, double margin,
+                          const float* points, const float* q01, Fill fill, float* min_out, int32_t* argmin_out,
+                          uint8_t* free_out, float* per_point) {
+    if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+    if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+    if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+    if (!min_out || !argmin_out || !free_out) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+    DeviceGuard guard(m->device);
+    ensure_pool(m->device);
+    cudaStream_t st = thread_stream(m->device);
+    const int nq = 2 * m->dof;
+    // staged layout: [points | q01] in, [min | argmin | free] out
+    const size_t o_q = align256(sizeof(float) * 3 * P), o_min = align256(o_q + sizeof(float) * nq * M);
+    const size_t o_arg = align256(o_min + sizeof(float) * M), o_free = align256(o_arg + sizeof(int32_t) * M);
+    const size_t total = align256(o_free + M);
+    Staging& sg = thread_staging(m->device);
+    SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
+    // inputs already in pinned memory go to the device directly; pageable ones through the
+    // pinned staging block (one host copy, then one H2D).  (cudaPointerGetAttributes is only
+    // asked about caller arrays: on pageable memory it costs several microseconds.)
+    auto pinned = [](const void* p) {
+        cudaPointerAttributes at{};
+        return p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    };
+    const bool direct = pinned(points) && pinned(q01);
+    if (!direct) fill(reinterpret_cast<float*>(sg.host), reinterpret_cast<float*>(sg.host + o_q));
+    Arena& arena = thread_arena(m->device);
+    {
+        ArenaScope as(&arena);
+        Scratch sc(st);
+        float* dpp = nullptr;
+        if (per_point)
+            SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
+        if (direct) {
+            SVN_CUDA(cudaMemcpyAsync(sg.dev, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
+            SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),
+                     "H2D motions");
+        } else {
+            SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
+        }
+        const svn_status s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
+                                         reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
+                                         reinterpret_cast<float*>(sg.dev + o_min),
+                                         reinterpret_cast<int32_t*>(sg.dev + o_arg), sg.dev + o_free, dpp, nullptr, st);
+        if (s != SVN_OK) return s;
+        SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
+                 "D2H min/argmin/free");
+        if (per_point)
+            SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
+    }
+    SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+    SVN_CUDA(arena.grow_to_need(), "scratch arena");
+    std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
+    std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
+    std::memcpy(free_out, sg.host + o_free, M);
+    return SVN_OK;
+}
+
 }  // namespace abi
 }  // namespace svn
 
@@ -433,60 +507,14 @@ SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const f
                                  const float* q01, int64_t M, double margin, float* min_out, int32_t* argmin_out,
                                  uint8_t* free_out, float* per_point) {
     try {
-        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
-        if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
-        if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
-        if (!points || !q01 || !min_out || !argmin_out || !free_out)
-            return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
-        DeviceGuard guard(m->device);
-        ensure_pool(m->device);
-        cudaStream_t st = thread_stream(m->device);
-        const int nq = 2 * m->dof;
-        // staged layout: [points | q01] in, [min | argmin | free] out
-        const size_t o_q = align256(sizeof(float) * 3 * P), o_min = align256(o_q + sizeof(float) * nq * M);
-        const size_t o_arg = align256(o_min + sizeof(float) * M), o_free = align256(o_arg + sizeof(int32_t) * M);
-        const size_t total = align256(o_free + M);
-        Staging& sg = thread_staging(m->device);
-        SVN_CUDA(sg.reserve(m->device, total), "staging buffers");
-        // inputs already in pinned memory go to the device directly; pageable ones through the
-        // pinned staging block (one host copy, then one H2D)
-        auto pinned = [](const void* p) {
-            cudaPointerAttributes at{};
-            return cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
-        };
-        const bool direct = pinned(points) && pinned(q01);
-        if (!direct) {
-            std::memcpy(sg.host, points, sizeof(float) * 3 * P);
-            std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
-        }
-        svn_status s;
-        {
-            Scratch sc(st);
-            float* dpp = nullptr;
-            if (per_point)
-                SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
-            if (direct) {
-                SVN_CUDA(cudaMemcpyAsync(sg.dev, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
-                SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),
-                         "H2D motions");
-            } else {
-                SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
-            }
-            s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
-                            reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
-                            reinterpret_cast<float*>(sg.dev + o_min), reinterpret_cast<int32_t*>(sg.dev + o_arg),
-                            sg.dev + o_free, dpp, nullptr, st);
-            if (s != SVN_OK) return s;
-            SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
-                     "D2H min/argmin/free");
-            if (per_point)
-                SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
-        }
-        SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
-        std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
-        std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
-        std::memcpy(free_out, sg.host + o_free, M);
-        return SVN_OK;
+        if (!points || !q01) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+        const int nq = m ? 2 * m->dof : 0;
+        return query_min_host(m, prec, P, M, margin, points, q01,
+                              [&](float* hp, float* hq) {
+                                  std::memcpy(hp, points, sizeof(float) * 3 * P);
+                                  std::memcpy(hq, q01, sizeof(float) * nq * M);
+                              },
+                              min_out, argmin_out, free_out, per_point);
     } catch (...) {
         return host_exception();
     }
@@ -547,15 +575,18 @@ SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision pr
         if (3 + 2 * dof != m->in) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: motion dof does not match model");
         if (!cloud || !q0 || !q1 || !min_out || !argmin_out)
             return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: null buffer");
-        // nn.cpp:469-473: every coordinate and joint value is cast to float
-        std::vector<float> pts(static_cast<size_t>(3 * P)), q(static_cast<size_t>(2 * dof));
-        for (int64_t i = 0; i < 3 * P; ++i) pts[i] = static_cast<float>(cloud[i]);
-        for (int i = 0; i < dof; ++i) q[i] = static_cast<float>(q0[i]);
-        for (int i = 0; i < dof; ++i) q[dof + i] = static_cast<float>(q1[i]);
+        // nn.cpp:469-473: every coordinate and joint value is cast to float (straight into the
+        // pinned staging block)
         float mn = 0.f;
         int32_t idx = 0;
         uint8_t fr = 0;
-        svn_status s = svn_query_min(m, prec, pts.data(), P, q.data(), 1, 0.0, &mn, &idx, &fr, nullptr);
+        svn_status s = query_min_host(m, prec, P, 1, 0.0, nullptr, nullptr,
+                                      [&](float* hp, float* hq) {
+                                          for (int64_t i = 0; i < 3 * P; ++i) hp[i] = static_cast<float>(cloud[i]);
+                                          for (int i = 0; i < dof; ++i) hq[i] = static_cast<float>(q0[i]);
+                                          for (int i = 0; i < dof; ++i) hq[dof + i] = static_cast<float>(q1[i]);
+                                      },
+                                      &mn, &idx, &fr, nullptr);
         if (s != SVN_OK) return s;
         *min_out = static_cast<double>(mn);
         *argmin_out = idx;

@@ -9,6 +9,7 @@ namespace svn {
 
 constexpr int kMaxLayers = 32;
 constexpr int kMaxIn = 32;  // input_dim = 3 + 2*dof <= 32
+constexpr float kSplitRzComp = 0.25f;  // fp32_split truncation compensation (FusedArgs::rz_comp)
 constexpr int kFp32SmallTile = 32;  // SIMT tile rows when a query has fewer big tiles than SMs
 
 enum : int { kConcat = 1, kAct = 2, kAffine = 4, kResidual = 8 };
@@ -80,6 +81,10 @@ struct FusedArgs {
     double margin;
     float* per_point;          // [.. out_base + row], or null
     unsigned long long* prof;  // optional wait-time counters (clock64 cycles), see kProf*
+    // fp32_split: the tensor core's fp32 accumulation truncates (rounds toward zero) once per
+    // MMA instruction; the epilogue adds rz_comp x (instructions in the chain) x ulp(main) x
+    // sign(main) back to the main accumulator (scripts/emulate_split.py)
+    float rz_comp;
 };
 
 // Wait/work accounting of the tensor-core kernels (scripts/profsum.py) costs ~1.3 % on c3, so
@@ -192,6 +197,33 @@ struct SmemOptIn {
         return e;
     }
 };
+
+// The fused kernels are launched with programmatic stream serialization: their prologue
+// (barrier init, TMEM allocation, tensor-map prefetch, w_o staging) overlaps the tail of K0,
+// and they pdl_wait() before reading anything K0 wrote.  SVN_PDL=0 turns it off (A/B hook).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVN_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename Kernel>
+cudaError_t launch_fused_pdl(Kernel kernel, unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                             const FusedArgs& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
 
 // Launchers (kernels_*.cu).
 cudaError_t launch_motion_bias(const FusedArgs& a, const float* wq /*[n_mb][2dof][N]*/,

@@ -317,6 +317,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // K0 (keys, counters, tile queue, extension rows) has completed
 
     if (warp == 0) {
         // ---------------------------------------------------------------- producer --
@@ -713,8 +714,9 @@ static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t s
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;
-    fused_bf16_pair_kernel<N><<<static_cast<unsigned>(2 * pairs), C::THREADS, C::SMEM, st>>>(a);
-    return cudaGetLastError();
+    const cudaError_t le = launch_fused_pdl(fused_bf16_pair_kernel<N>, static_cast<unsigned>(2 * pairs), C::THREADS,
+                                            C::SMEM, st, a);
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st) {
@@ -773,6 +775,7 @@ __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N,
                                   const float* __restrict__ wx_slots, uint8_t* __restrict__ ext, const QNormX qn,
                                   unsigned long long* keys, unsigned int* counters, int64_t n_keys, int pp_layout,
                                   unsigned int* sched) {
+    pdl_launch_dependents();  // the fused kernel may start its prologue now (it pdl_wait()s for our writes)
     const int64_t m = blockIdx.x;
     const int slot = blockIdx.y;
     if (sched && m == 0 && slot == 0 && threadIdx.x == 0) *sched = 0u;  // the fused kernel's tile counter

@@ -254,6 +254,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // K0 (keys, counters, tile queue, extension rows) has completed
 
     if (warp == 0) {
         // ------------------------------------------------------------------ producer --
@@ -560,8 +561,9 @@ cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t s
     const int64_t need = a.n_tiles <= pairs ? a.n_tiles : (a.n_tiles + 1) / 2;
     if (need < pairs) pairs = need;
     if (pairs < 1) return cudaSuccess;
-    fused_bf16_pp_kernel<<<static_cast<unsigned>(2 * pairs), pp::THREADS, pp::SMEM, st>>>(a);
-    return cudaGetLastError();
+    const cudaError_t le = launch_fused_pdl(fused_bf16_pp_kernel, static_cast<unsigned>(2 * pairs), pp::THREADS,
+                                            pp::SMEM, st, a);
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 }  // namespace svn

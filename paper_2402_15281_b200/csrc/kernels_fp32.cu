@@ -31,6 +31,7 @@ __global__ void motion_bias_kernel(const float* __restrict__ q01, int64_t M, int
                                    const float* __restrict__ wq, const float* __restrict__ base_bias,
                                    float* __restrict__ motion_bias, const QNorm qn, unsigned long long* keys,
                                    unsigned int* counters, int64_t n_keys) {
+    pdl_launch_dependents();  // the fused kernel may start its prologue now (it pdl_wait()s for our writes)
     const int64_t m = blockIdx.x;
     const int slot = blockIdx.y;
     if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
         fence_mbar_init();
     }
     __syncthreads();
+    pdl_wait();  // K0 (per-motion biases, keys, counters) has completed
 
     // producer state (thread 0): issues chunk g_prod into stage g_prod % STAGES
     ChunkIter prod{0, 0};
@@ -379,8 +381,9 @@ static cudaError_t launch_fp32_n(const FusedArgs& a, int num_sms, cudaStream_t s
     if (e != cudaSuccess) return e;
     int64_t grid = a.n_tiles < num_sms ? a.n_tiles : num_sms;
     if (grid < 1) return cudaSuccess;
-    fused_fp32_kernel<N, CG, TMO><<<static_cast<unsigned>(grid), C::THREADS, C::SMEM, st>>>(a);
-    return cudaGetLastError();
+    const cudaError_t le = launch_fused_pdl(fused_fp32_kernel<N, CG, TMO>, static_cast<unsigned>(grid), C::THREADS,
+                                            C::SMEM, st, a);
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 static int fp32_cg() {

@@ -85,12 +85,31 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
 }
 
+// main + corr / 2048, with main's expected truncation loss added back: the tensor core's
+// fp32 accumulator drops the bits below its 24-bit significand at every MMA instruction
+// (toward zero), so after n instructions main sits on average ~n x c x ulp below |exact|.
+// sign|exponent bits of main as a float = +-2^e; times kf = c x n x 2^-23 = the signed loss.
+__device__ __forceinline__ float combine(uint32_t m, uint32_t c, float kf) {
+    const float mf = __uint_as_float(m);
+    const float se = __uint_as_float(m & 0xff800000u);
+    return fmaf(__uint_as_float(c), LO_INV, fmaf(se, kf, mf));
+}
+
 // 32 output columns of one row: v (fp32, already main + corr/2048) -> act / affine /
 // residual -> next layer's (hi, lo') planes, or the output dot on the last layer.
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
                                       uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot, bool& ovf) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+    if (l == 0 || (fl & kConcat)) {
+        // the layer's K=16 extension carries z_x (and b_m) as fp16 splits: an input beyond the
+        // fp16 range arrives as inf / NaN, which the ReLU below would turn into 0.  v * 0 is
+        // NaN exactly for a non-finite v.
+        float nf = 0.f;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) nf = fmaf(v[i], 0.f, nf);
+        ovf |= nf != nf;
+    }
     if (act) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = v[i] > 0.f ? v[i] : 0.f;
@@ -140,7 +159,7 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         for (int p = 0; p < 4; ++p) {
             // paired split: hi = f16x2(x0, x1); lo' = f16x2((x - hi) * 2^11)
             const float x0 = v[8 * u + 2 * p], x1 = v[8 * u + 2 * p + 1];
-            ovf |= fmaxf(fabsf(x0), fabsf(x1)) >= kF16Overflow;  // fp16(x) would be +-inf
+            ovf |= !(fabsf(x0) < kF16Overflow && fabsf(x1) < kF16Overflow);  // fp16(x) would be +-inf
             const __half2 h = __floats2half2_rn(x0, x1);
             const float2 hf = __half22float2(h);
             const __half2 lo = __floats2half2_rn((x0 - hf.x) * LO_SCALE, (x1 - hf.y) * LO_SCALE);
@@ -209,6 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // K0 (keys, counters, tile queue, extension rows) has completed
 
     if (warp == 0) {
         // ---------------------------------------------------------------- producer --
@@ -364,6 +384,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     tc_fence_after();
                     const uint32_t tb = tmem + t_lane + static_cast<uint32_t>(j * 256 + ch * COLS);
                     static_assert(COLS == 64, "two 32-column chunks per thread per half");
+                    // truncation compensation: rz_comp x (MMAs into main) x 2^-23, times
+                    // sign(main) x 2^exponent(main) = the main accumulator's ulp, signed
+                    const float kf = a.rz_comp * static_cast<float>(l == 0 ? 1 : N / 16 + (ld.ext ? 1 : 0)) *
+                                     (1.0f / 8388608.0f);
                     float v[32];
                     {
                         uint32_t rm[32], rc[32];
@@ -372,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                         tmem_wait_tied(rm);
                         tmem_wait_tied(rc);
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc[i]), LO_INV, __uint_as_float(rm[i]));
+                        for (int i = 0; i < 32; ++i) v[i] = combine(rm[i], rc[i], kf);
                     }
                     // second chunk's loads fly while the first chunk is split and stored
                     uint32_t rm2[32], rc2[32];
@@ -382,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     tmem_wait_tied(rm2);
                     tmem_wait_tied(rc2);
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = fmaf(__uint_as_float(rc2[i]), LO_INV, __uint_as_float(rm2[i]));
+                    for (int i = 0; i < 32; ++i) v[i] = combine(rm2[i], rc2[i], kf);
                     epi32(ld, l, last, v, j * NHO + ch * COLS + 32, row, Ahi, Alo, wo_s, dot, ovf);
                     pe_w += prof_clock() - c1;
                     tc_fence_before();
@@ -509,8 +533,9 @@ cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st)
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;
-    fused_split_kernel<<<static_cast<unsigned>(2 * pairs), sp::THREADS, sp::SMEM, st>>>(a);
-    return cudaGetLastError();
+    const cudaError_t le = launch_fused_pdl(fused_split_kernel, static_cast<unsigned>(2 * pairs), sp::THREADS,
+                                            sp::SMEM, st, a);
+    return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- K0 (split) --
@@ -524,6 +549,7 @@ __global__ void split_ext_kernel(const float* __restrict__ q01, int dof, int n_m
                                  const float* __restrict__ base_bias, const float* __restrict__ wx_slots,
                                  uint8_t* __restrict__ ext, const QNormS qn, unsigned long long* keys,
                                  unsigned int* counters, int64_t n_keys) {
+    pdl_launch_dependents();  // the fused kernel may start its prologue now (it pdl_wait()s for our writes)
     using namespace sp;
     const int64_t m = blockIdx.x;
     const int slot = blockIdx.y;

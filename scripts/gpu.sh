@@ -10,6 +10,8 @@
 #   ab VAR "v1 v2" [args]      A/B of env-selected variants, alternated twice
 #   multirank                  bench.py's multi-rank path on one GPU (gloo ranks on device 0)
 #   sweep [motions...]         c2 network in bf16 over motion counts
+#   latency                    per-call predict_min_distance latency from C++ (scripts/latency_cpp.cpp)
+#   rzsweep [c...]             fp32_split error per calibration seed for truncation compensations c
 set -u
 mkdir -p gpurun_out
 task=${1:-test}; shift || true
@@ -63,5 +65,11 @@ case "$task" in
       timeout 600 python bench.py --config c2 --precision bf16 --motions $m --steps 4 --warmup 3 --no-cpu-baseline \
         --no-e2e --no-parity > gpurun_out/sw_$m.log 2>&1; line gpurun_out/sw_$m.log "c2 bf16 M=$m"
     done ;;
+  latency)
+    g++ -std=c++17 -O2 -Iinclude scripts/latency_cpp.cpp -Lpaper_2402_15281_b200/_lib -lsweptnet_b200 \
+      -Wl,-rpath,$PWD/paper_2402_15281_b200/_lib -o gpurun_out/latency_cpp && \
+    timeout 300 gpurun_out/latency_cpp 2>&1 | tee gpurun_out/latency.log ;;
+  rzsweep)
+    for c in ${@:-0 0.25}; do SVN_SPLIT_RZ=$c timeout 900 python scripts/split_rz_sweep.py; done 2>&1 | tee gpurun_out/rzsweep.log ;;
   *) echo "unknown task $task"; exit 2 ;;
 esac

@@ -16,6 +16,8 @@ __host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
 
 // mode 0: N=256 chain; 1: N=128 chain; 2: split pattern 3 x N=128 (hi.hi, hi.lo, lo.hi)
 // mode 3: merged pattern N=256 (hi.[hi;lo]) + N=128 (lo.hi)
+// mode 4: M=128 pair (64 rows per CTA, TMEM "2x2" layout) N=256 chain; 5: M=128 split pattern
+// 3 x N=256; 6: M=128 N=128 chain
 __global__ void __cluster_dims__(2, 1, 1) mma_bw(int mode, int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t done;
@@ -36,6 +38,7 @@ __global__ void __cluster_dims__(2, 1, 1) mma_bw(int mode, int iters, unsigned l
     if (cluster_ctarank() == 0 && threadIdx.x == 0) {
         const uint32_t a_hi = smem_u32(sm), a_lo = a_hi + 16384, b = a_hi + 32768;  // 16 KiB A slabs, 32 KiB B
         constexpr uint32_t i256 = idesc_f16(256, 256), i128 = idesc_f16(256, 128);
+        constexpr uint32_t m128n256 = idesc_f16(128, 256), m128n128 = idesc_f16(128, 128);
         const unsigned long long t0 = clock64();
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
@@ -50,9 +53,17 @@ __global__ void __cluster_dims__(2, 1, 1) mma_bw(int mode, int iters, unsigned l
                     mma_bf16_pair(tmem, ah, bh, i128, 1u);
                     mma_bf16_pair(tmem + 128, ah, bl, i128, 1u);
                     mma_bf16_pair(tmem + 128, al, bh, i128, 1u);
-                } else {
+                } else if (mode == 3) {
                     mma_bf16_pair(tmem, ah, bh, i256, 1u);
                     mma_bf16_pair(tmem + 128, al, bh, i128, 1u);
+                } else if (mode == 4) {
+                    mma_bf16_pair(tmem, ah, bh, m128n256, 1u);
+                } else if (mode == 5) {
+                    mma_bf16_pair(tmem, ah, bh, m128n256, 1u);
+                    mma_bf16_pair(tmem + 128, ah, bl, m128n256, 1u);
+                    mma_bf16_pair(tmem + 128, al, bh, m128n256, 1u);
+                } else {
+                    mma_bf16_pair(tmem, ah, bh, m128n128, 1u);
                 }
             }
         }
@@ -74,10 +85,12 @@ int main() {
     cudaFuncSetAttribute(mma_bw, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const char* names[4] = {"N=256 chain", "N=128 chain", "split 3xN128", "merged N256+N128"};
-    const double flop_per_it[4] = {4 * 256.0 * 256 * 16 * 2, 4 * 256.0 * 128 * 16 * 2, 3 * 4 * 256.0 * 128 * 16 * 2,
-                                   (4 * 256.0 * 256 * 16 * 2 + 4 * 256.0 * 128 * 16 * 2)};
-    for (int mode = 0; mode < 4; ++mode) {
+    const char* names[7] = {"N=256 chain", "N=128 chain", "split 3xN128", "merged N256+N128",
+                            "M128 N=256 chain", "M128 split 3xN256", "M128 N=128 chain"};
+    const double flop_per_it[7] = {4 * 256.0 * 256 * 16 * 2, 4 * 256.0 * 128 * 16 * 2, 3 * 4 * 256.0 * 128 * 16 * 2,
+                                   (4 * 256.0 * 256 * 16 * 2 + 4 * 256.0 * 128 * 16 * 2),
+                                   4 * 128.0 * 256 * 16 * 2, 3 * 4 * 128.0 * 256 * 16 * 2, 4 * 128.0 * 128 * 16 * 2};
+    for (int mode = 0; mode < 7; ++mode) {
         const int iters = 4000;
         mma_bw<<<sms, 128, 96 * 1024>>>(mode, 10, d);
         cudaEvent_t e0, e1;

@@ -307,3 +307,32 @@ def test_width_128_fp32_bit_identical(prog, M, P):
     assert np.array_equal(r.min, omin) and np.array_equal(r.argmin, oarg) and np.array_equal(r.free, ofree)
     with pytest.raises(S.SvnError):
         S.Model(prog, params).query_min(pts, q, 0.02, precision="bf16")
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32_exact", "fp32_split"])
+def test_small_calls_read_each_calls_inputs(prec):
+    """Host-buffer calls stage through a per-thread pinned block (abi_query.cu, query_min_host):
+    every call must use its own points and motions, also with a second model (possibly at a
+    freed model's address)."""
+    w = WORKLOADS["c2"]
+    for mseed in (41, 42):
+        params = S.init_params(w.program, mseed, w.bound)
+        m = S.Model(w.program, params)
+        for seed in (1, 2, 3, 1):
+            pts, q = w.make(seed=seed, motions=3, points=2999)
+            r = m.query_min(pts, q, w.margin, precision=prec)  # no per-point output
+            omin, oarg, ofree, opp = O.query_min(w.program, params, pts, q, w.margin, per_point=True, threads=8)
+            tol = _tol(prec, w.program)
+            assert np.abs(r.min.astype(np.float64) - omin).max() <= tol
+            if prec == "fp32_exact":
+                assert np.array_equal(r.min, omin) and np.array_equal(r.argmin, oarg)
+                assert np.array_equal(r.free, ofree)
+            cloud = pts[:1000].astype(np.float64)
+            got = m.predict_min_distance(cloud, q[0, :6], q[0, 6:], precision=prec)
+            ref = O.predict_min_distance(w.program, params, cloud, q[0, :6].astype(np.float64),
+                                         q[0, 6:].astype(np.float64))
+            if prec == "fp32_exact":
+                assert got == ref
+            else:
+                assert abs(got[0] - ref[0]) <= tol
+        del m
