@@ -65,14 +65,17 @@ typedef enum {
  *  FP32_EXACT  (bias, h part, x, q0, q1 — nn.cpp:118-124), bit-identical to the reference
  *              float path up to the documented dot-product order, so the 1e-5 bar holds
  *              with zero error.  The two names are the same path.
- *  FP32_SPLIT  fp32-grade on tcgen05 (width 256): every operand split into fp16 hi +
- *              2^11-scaled lo, three f16 MMAs per product into two fp32 TMEM accumulators,
- *              per-motion q-fold.  As close to the exact value as fp32 arithmetic, but not
- *              in the reference's rounding order: per-point delta within the stated bound
- *              of tests/golden/fp32_split_bounds.json (UNSUPPORTED at other widths or when
- *              a weight exceeds 1e4).  A row whose hidden activation reaches the fp16
- *              range (|h| >= 65520) is reported as delta = -inf: its motion's min is -inf
- *              and its class "not free" (handed to the exact checker), never dropped. */
+ *  FP32_SPLIT  fp32-grade on tcgen05 (width 256 and 512): every operand split into fp16
+ *              hi + 2^11-scaled lo, three f16 MMAs per product into two fp32 TMEM
+ *              accumulators (the tensor core's per-instruction truncation compensated in the
+ *              epilogue), per-motion q-fold.  Not in the reference's rounding order:
+ *              per-point delta within the bound of tests/golden/fp32_split_bounds.json —
+ *              the 1e-5 FP32 bar at width 256, a stated bound of 2.3e-5 to 2.6e-5 for the
+ *              width-512 plain/DeepSDF networks (UNSUPPORTED at other widths or when a
+ *              weight exceeds 1e4).  A row whose hidden activation reaches the fp16 range
+ *              (|h| >= 65520) or whose input is not finite is reported as delta = -inf: its
+ *              motion's min is -inf and its class "not free" (handed to the exact checker),
+ *              never dropped. */
 typedef enum {
     SVN_PREC_BF16 = 0,
     SVN_PREC_FP32 = 1,

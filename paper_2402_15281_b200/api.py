@@ -91,7 +91,8 @@ class Model:
         points float [P, 3]; q01 float [M, 2*dof] = (q0 | q1).
         precision: "bf16" (tcgen05, per-network stated bound), "fp32" / "fp32_exact" (the FP32
         path: FFMA in the reference's order, bit-identical to the oracle), "fp32_split"
-        (width 256: fp32-grade split-fp16 on tcgen05, its own stated bound)."""
+        (width 256/512: fp32-grade split-fp16 on tcgen05; 1e-5 at width 256, a stated bound at
+        width 512)."""
         pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
         q = np.ascontiguousarray(q01, dtype=np.float32).reshape(-1, 2 * self.program.dof)
         P, M = pts.shape[0], q.shape[0]

@@ -461,11 +461,12 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
             m->has_bf16 = true;
         }
 
-        // fp32-accurate tensor-core path (width 256): every weight split into fp16 hi and
-        // 2^11-scaled lo' planes, per (layer, quarter step, 64-wide K slab, CTA half r) a
-        // [hi: 64 rows][lo': 64 rows] SW128 image; extension rows [main 64][corr 64] per
-        // (n-half, r).  Needs |W|, |b| well inside the fp16 range.
-        if (N == 256) {
+        // fp32-accurate tensor-core path (width 256 and 512): every weight split into fp16 hi
+        // and 2^11-scaled lo' planes, per (layer, quarter step, 64-wide K slab, CTA half r) a
+        // [hi: BRH rows][lo': BRH rows] SW128 image (BRH = width / 4 B rows per CTA and
+        // n-half); extension rows [main BRH][corr BRH] per (n-half, r).  Needs |W|, |b| well
+        // inside the fp16 range.
+        if (N == 256 || N == 512) {
             float wmax = 0.f;
             for (int64_t i = 2 * in; i < n_params; ++i) wmax = std::max(wmax, std::fabs(params[i]));
             if (wmax < 1.0e4f) {
@@ -474,7 +475,9 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
                     hi = __float2half_rn(x);
                     lo = __float2half_rn((x - __half2float(hi)) * 2048.0f);
                 };
-                std::vector<uint8_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * 4 * 2 * 2 * 2 * 64 * 128);
+                const int NHO = N / 2, BRH = N / 4, KSL = N / 128;
+                const size_t plane = static_cast<size_t>(BRH) * 128;
+                std::vector<uint8_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * 4 * KSL * 2 * 2 * plane);
                 uint8_t* out = ws.data();
                 const float* Wl = params + 2 * in;
                 for (int l = 0; l < L; ++l) {
@@ -482,17 +485,17 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
                     if (l > 0) {
                         for (int step = 0; step < 4; ++step) {
                             const int nh = step & 1, kh = step >> 1;
-                            for (int ks = 0; ks < 2; ++ks)
+                            for (int ks = 0; ks < KSL; ++ks)
                                 for (int r = 0; r < 2; ++r) {
-                                    for (int nr = 0; nr < 64; ++nr)
+                                    for (int nr = 0; nr < BRH; ++nr)
                                         for (int kc = 0; kc < 64; ++kc) {
-                                            const int n = nh * 128 + r * 64 + nr, k = (kh * 2 + ks) * 64 + kc;
+                                            const int n = nh * NHO + r * BRH + nr, k = (kh * KSL + ks) * 64 + kc;
                                             __half hi, lo;
                                             split_h(Wl[static_cast<int64_t>(k) * N + n], hi, lo);
-                                            *reinterpret_cast<__half*>(out + sw128_offset(nr, kc, 64)) = hi;
-                                            *reinterpret_cast<__half*>(out + 8192 + sw128_offset(nr, kc, 64)) = lo;
+                                            *reinterpret_cast<__half*>(out + sw128_offset(nr, kc, BRH)) = hi;
+                                            *reinterpret_cast<__half*>(out + plane + sw128_offset(nr, kc, BRH)) = lo;
                                         }
-                                    out += 16384;
+                                    out += 2 * plane;
                                 }
                         }
                     }
@@ -513,27 +516,29 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
                         const size_t base = xm.size();
                         xm.resize(base + static_cast<size_t>(N) * 2 * 32, 0);
                         for (int n = 0; n < N; ++n) {
-                            const int nh = n / 128, wi = n % 128, r = wi / 64, rr = wi % 64;
-                            uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * 128) * 32;
+                            const int nh = n / NHO, wi = n % NHO, r = wi / BRH, rr = wi % BRH;
+                            uint8_t* blob = xm.data() + base + static_cast<size_t>((nh * 2 + r) * 2 * BRH) * 32;
                             __half hi, lo;
                             split_h(b[n], hi, lo);
-                            *reinterpret_cast<__half*>(blob + ext_offset(rr, 0)) = hi;         // main: b_h
-                            *reinterpret_cast<__half*>(blob + 2048 + ext_offset(rr, 0)) = lo;  // corr: b_l'
+                            *reinterpret_cast<__half*>(blob + ext_offset(rr, 0)) = hi;             // main: b_h
+                            *reinterpret_cast<__half*>(blob + BRH * 32 + ext_offset(rr, 0)) = lo;  // corr: b_l'
                         }
                     }
                     Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
                 }
-                if (xm.empty()) xm.resize(128 * 32, 0);
+                if (xm.empty()) xm.resize(static_cast<size_t>(2 * BRH) * 32, 0);
                 uint8_t* dxm = nullptr;
                 if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
-                if ((st = encode_blob_map(&sa.tmap_xm, dxm, 32, xm.size() / 32, 128)) != SVN_OK) return cleanup_fail(st);
+                if ((st = encode_blob_map(&sa.tmap_xm, dxm, 32, xm.size() / 32, static_cast<uint32_t>(2 * BRH))) !=
+                    SVN_OK)
+                    return cleanup_fail(st);
                 // expected truncation loss per MMA instruction, in ulps of the final main
                 // accumulator (calibrated); SVN_SPLIT_RZ overrides it (A/B hook)
                 static const float rz = [] {
                     const char* e = std::getenv("SVN_SPLIT_RZ");
-                    return e ? static_cast<float>(std::atof(e)) : kSplitRzComp;
+                    return e ? static_cast<float>(std::atof(e)) : -1.0f;
                 }();
-                sa.rz_comp = rz;
+                sa.rz_comp = rz >= 0.f ? rz : (N == 256 ? kSplitRzComp256 : kSplitRzComp512);
                 m->base_split = sa;
                 m->has_split = true;
             }

@@ -17,7 +17,7 @@ svn_status check_prec(const svn_model* m, svn_precision prec) {
             return fail(SVN_ERR_UNSUPPORTED, "fp32 path needs width 128, 256 or 512");
     } else if (prec == SVN_PREC_FP32_SPLIT) {
         if (!m->has_split)
-            return fail(SVN_ERR_UNSUPPORTED, "fp32_split path needs width 256, >= 2 layers and |W| < 1e4");
+            return fail(SVN_ERR_UNSUPPORTED, "fp32_split path needs width 256 or 512, >= 2 layers and |W| < 1e4");
     } else {
         return fail(SVN_ERR_INVALID_ARGUMENT, "unknown precision");
     }
@@ -32,7 +32,12 @@ Kind kernel_kind(const svn_model*, svn_precision prec) {
     return Kind::SIMT;
 }
 
-int tile_rows(Kind k, int N) { return k == Kind::SIMT ? (N >= 512 ? 64 : 128) : 256; }
+// rows per tile (a CTA pair's tile for the tensor-core kernels; fp32_split at width 512 holds
+// 64 rows per CTA)
+int tile_rows(Kind k, int N) {
+    if (k == Kind::SIMT) return N >= 512 ? 64 : 128;
+    return (k == Kind::SPLIT && N == 512) ? 128 : 256;
+}
 // SIMT: a query with fewer big tiles than SMs is cut into 32-row tiles (4 warps per CTA,
 // more SMs busy; each output's k-ordered FMA chain is unchanged)
 int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
@@ -109,10 +114,10 @@ cudaError_t launch_k1(const FusedArgs& a, Kind kind, int num_sms, cudaStream_t s
 svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long long* keys, unsigned int* counters,
                       int64_t n_keys, Scratch& sc, cudaStream_t st, bool split) {
     uint8_t* ext = nullptr;
-    if (split) {  // [motion][slot][n-half][CTA half][main 64 rows | corr 64 rows] x 32 B
+    if (split) {  // [motion][slot][n-half][CTA half][main N/4 rows | corr N/4 rows] x 32 B
         const size_t rows = static_cast<size_t>(M) * (m->n_mb ? m->n_mb : 1) * 2 * m->N;
         SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&ext), rows * 32), "cudaMallocAsync(split ext)");
-        svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, 128);
+        svn_status s = encode_blob_map(&a.tmap_xq, ext, 32, rows, static_cast<uint32_t>(m->N / 2));
         if (s != SVN_OK) return s;
         SVN_CUDA(launch_split_ext(a, m->d_wq, m->d_mbbase, m->d_wxslots, ext, keys, counters, n_keys, st),
                  "split_ext kernel");

@@ -9,7 +9,9 @@ namespace svn {
 
 constexpr int kMaxLayers = 32;
 constexpr int kMaxIn = 32;  // input_dim = 3 + 2*dof <= 32
-constexpr float kSplitRzComp = 0.25f;  // fp32_split truncation compensation (FusedArgs::rz_comp)
+// fp32_split truncation compensation per width (FusedArgs::rz_comp), calibrated on the B200
+constexpr float kSplitRzComp256 = 0.25f;
+constexpr float kSplitRzComp512 = 0.2f;
 constexpr int kFp32SmallTile = 32;  // SIMT tile rows when a query has fewer big tiles than SMs
 
 enum : int { kConcat = 1, kAct = 2, kAffine = 4, kResidual = 8 };

@@ -1,4 +1,4 @@
-// kernels_split.cu — K1 (fp32-accurate) on tcgen05 for width 256: split-fp16 products.
+// kernels_split.cu — K1 (fp32-accurate) on tcgen05 for width 256 and 512: split-fp16 products.
 //
 // The fp32 path's 1e-5 per-point bar (BASELINE.json north_star) without SIMT FFMA: every
 // operand x is split into fp16 hi = fp16(x) and scaled lo' = fp16((x - hi) * 2^11) (22
@@ -8,13 +8,22 @@
 //     D = main + corr * 2^-11      (the lo' . lo' term, ~2^-22 relative, is dropped)
 // Measured (scripts/microbench_split.cu): 2.7e-6 max error vs fp64 on a 128x256x256 product
 // with |D| ~ 5, against 2.3e-6 for a sequential fp32 FMA chain.  Bias, the per-motion q-fold
-// and the x-part ride in a K=16 extension slab split the same way.
+// and the x-part ride in a K=16 extension slab split the same way.  The tensor core truncates
+// its fp32 accumulator once per instruction; the epilogue adds the expected loss back
+// (combine() below).
 //
-// Structure = the CTA-pair kernel (kernels_bf16_pair.cu) with the width-256 layer output
-// treated as two output halves of 128 columns, each owning a main and a corr accumulator:
-// 2 x (128 + 128) = all 512 TMEM columns.  A layer runs as quarter steps (n-half, k-half)
-// (0,0) (1,0) (0,1) (1,1); the epilogue of output half 0 overlaps step (1,1).  The
-// activation tile is held as two fp16 planes (hi, lo'), 2 x 64 KiB per CTA.
+// Structure = the CTA-pair kernel (kernels_bf16_pair.cu) with the layer output treated as two
+// n-halves, each owning a main and a corr accumulator: 2 x (128 + 128) = all 512 TMEM columns.
+// A layer runs as quarter steps (n-half, k-half) (0,0) (1,0) (0,1) (1,1); the epilogue of
+// output half 0 overlaps step (1,1).  The activation tile is held as two fp16 planes (hi, lo'),
+// 2 x 64 KiB per CTA at either width:
+//   width 256: 128 rows per CTA, M=256 pair MMAs with N=128 (one n-half), each accumulator
+//              128 lanes x 128 columns;
+//   width 512: 64 rows per CTA, M=128 pair MMAs with N=256 — the accumulator of a CTA's 64
+//              rows x 256 columns sits in TMEM's "2x2" layout (rows in lanes 0-63 for
+//              columns 0-127 of the n-half, in lanes 64-127 for columns 128-255), again 128
+//              TMEM columns, so the TMEM plan is the same; a weight slab (one plane of 128
+//              B rows x 64 K per CTA) is one 16 KiB stage, its hi and lo' planes two stages.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -25,31 +34,41 @@ namespace svn {
 
 namespace sp {
 
-constexpr int N = 256;                      // layer width
-constexpr int TM = 128;                     // rows per CTA (pair tile = 256 rows)
-constexpr int NHO = 128;                    // output columns per n-half (MMA N)
-constexpr int BRH = NHO / 2;                // B rows per CTA per n-half (cta_group::2 split of N)
-constexpr int KSL = (N / 2) / 64;           // 64-wide K slabs per k-half
-constexpr uint32_t A_SLAB = TM * 128;       // 16 KiB
-constexpr uint32_t A_PLANE = TM * N * 2;    // 64 KiB per fp16 plane
-constexpr uint32_t AX_BYTES = TM * 32;      // 4 KiB
-constexpr uint32_t B_HALF = BRH * 128;      // 8 KiB: one plane of one slab for this CTA
-constexpr uint32_t CHUNK = 2 * B_HALF;      // 16 KiB: [hi][lo'] of one slab
-constexpr uint32_t XHALF = BRH * 32;        // 2 KiB: extension rows (main or corr) for this CTA
-constexpr int STAGES = 5;
-constexpr int EPI_WARPS = 8;
-constexpr int OUT_WARP = 2 + EPI_WARPS;     // keys / per-point outputs / A extensions of later tiles
-constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
-constexpr int COLS = NHO / 2;               // columns per epilogue thread per half (64)
-constexpr uint32_t OFF_AHI = 0;
-constexpr uint32_t OFF_ALO = A_PLANE;
-constexpr uint32_t OFF_AX = 2 * A_PLANE;
-constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
-constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * CHUNK;
-constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
-constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
-constexpr uint32_t SMEM = OFF_BAR + 256;
-static_assert(SMEM <= 232448, "shared memory budget");
+template <int N_>
+struct Cfg {
+    static constexpr int N = N_;                        // layer width
+    static constexpr int TM = N == 256 ? 128 : 64;      // rows per CTA (pair tile = 2 TM rows)
+    static constexpr int NHO = N / 2;                   // output columns per n-half (MMA N)
+    static constexpr int BRH = NHO / 2;                 // B rows per CTA per n-half (cta_group::2 split of N)
+    static constexpr int KSL = (N / 2) / 64;            // 64-wide K slabs per k-half
+    static constexpr uint32_t A_SLAB = TM * 128;        // one 64-K slab of an A plane
+    static constexpr uint32_t A_PLANE = TM * N * 2;     // 64 KiB per fp16 plane
+    static constexpr uint32_t AX_BYTES = TM * 32;
+    static constexpr uint32_t STAGE = 16384;            // one TMA stage
+    static constexpr uint32_t PLANE_B = BRH * 128;      // one plane of one weight slab for this CTA
+    static constexpr int SPS = 2 * PLANE_B / STAGE;     // stages per weight slab: 1 ([hi|lo']) or 2 (hi, lo')
+    static constexpr uint32_t XHALF = BRH * 32;         // extension rows (main or corr) for this CTA
+    static constexpr int STAGES = 5;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int OUT_WARP = 2 + EPI_WARPS;      // keys / per-point outputs / A extensions of later tiles
+    static constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
+    static constexpr int COLS = 64;                     // columns per epilogue thread per n-half
+    static constexpr int PARTS = N / 128;               // partial output dots per row (epilogue threads)
+    static constexpr int RQ = TM / 32;                  // 32-row groups per CTA (output warp)
+    static constexpr uint32_t OFF_AHI = 0;
+    static constexpr uint32_t OFF_ALO = A_PLANE;
+    static constexpr uint32_t OFF_AX = 2 * A_PLANE;
+    static constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
+    static constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * STAGE;
+    static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
+    static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * PARTS * TM * 4;
+    static constexpr uint32_t SMEM = OFF_BAR + 256;
+    static_assert(SMEM <= 232448, "shared memory budget");
+    static_assert(SPS == 1 || SPS == 2, "a weight slab is one or two stages");
+    static_assert(2 * XHALF <= STAGE, "extension slab fits one stage");
+    static_assert(OFF_STAGE % 1024 == 0, "SW128 stages need 1 KiB alignment");
+};
+
 constexpr float LO_SCALE = 2048.0f;
 constexpr float LO_INV = 1.0f / 2048.0f;
 
@@ -97,6 +116,7 @@ __device__ __forceinline__ float combine(uint32_t m, uint32_t c, float kf) {
 
 // 32 output columns of one row: v (fp32, already main + corr/2048) -> act / affine /
 // residual -> next layer's (hi, lo') planes, or the output dot on the last layer.
+template <int TM>
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
                                       uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot, bool& ovf) {
     const int fl = ld.flags;
@@ -174,17 +194,22 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
 
 }  // namespace sp
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
+template <int N>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS, 1)
     fused_split_kernel(const __grid_constant__ FusedArgs a) {
     using namespace sp;
+    using C = Cfg<N>;
+    constexpr int TM = C::TM, NHO = C::NHO, BRH = C::BRH, KSL = C::KSL, STAGES = C::STAGES, SPS = C::SPS;
+    constexpr int EPI_WARPS = C::EPI_WARPS, OUT_WARP = C::OUT_WARP, COLS = C::COLS, PARTS = C::PARTS, RQ = C::RQ;
+    constexpr uint32_t A_SLAB = C::A_SLAB, AX_BYTES = C::AX_BYTES, STAGE = C::STAGE, XHALF = C::XHALF;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* Ahi = smem + OFF_AHI;
-    uint8_t* Alo = smem + OFF_ALO;
-    uint8_t* AX = smem + OFF_AX;  // [2][AX_BYTES]
-    uint8_t* stages = smem + OFF_STAGE;
-    float* wo_s = reinterpret_cast<float*>(smem + OFF_WO);
-    float* dotbuf = reinterpret_cast<float*>(smem + OFF_DOT);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+    uint8_t* Ahi = smem + C::OFF_AHI;
+    uint8_t* Alo = smem + C::OFF_ALO;
+    uint8_t* AX = smem + C::OFF_AX;  // [2][AX_BYTES]
+    uint8_t* stages = smem + C::OFF_STAGE;
+    float* wo_s = reinterpret_cast<float*>(smem + C::OFF_WO);
+    float* dotbuf = reinterpret_cast<float*>(smem + C::OFF_DOT);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint64_t* full = bars;
     uint64_t* empty = full + STAGES;
     uint64_t* d_full = empty + STAGES;
@@ -257,7 +282,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                         if (kh == 0 && ld.ext) {
                             slot(2 * XHALF);
                             const uint32_t fb = full0 + stage * 8u;
-                            uint8_t* dst = stages + stage * CHUNK;
+                            uint8_t* dst = stages + stage * STAGE;
                             if (ld.ext == 2) {
                                 const int64_t blob = ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
                                 tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * 2 * BRH), fb, pol);
@@ -269,11 +294,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                         }
                         if (l > 0) {
                             for (int ks = 0; ks < KSL; ++ks) {
-                                slot(CHUNK);
-                                tma_load_2d_pair(stages + stage * CHUNK, &a.tmap_w, 0,
-                                                 static_cast<int32_t>(wrow + rank * 2 * BRH), full0 + stage * 8u, pol);
+                                // this CTA's [hi | lo'] rows of the slab: one 128-row box per stage
+                                for (int sub = 0; sub < SPS; ++sub) {
+                                    slot(STAGE);
+                                    tma_load_2d_pair(stages + stage * STAGE, &a.tmap_w, 0,
+                                                     static_cast<int32_t>(wrow + rank * 2 * BRH + sub * 128),
+                                                     full0 + stage * 8u, pol);
+                                    advance();
+                                }
                                 wrow += 4 * BRH;
-                                advance();
                             }
                         }
                     }
@@ -317,7 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                             mbar_wait(&full[stage], phase);
                             pw_f += prof_clock() - c0;
                             tc_fence_after();
-                            const uint32_t xs = s_base + stage * CHUNK;
+                            const uint32_t xs = s_base + stage * STAGE;
                             const uint64_t adesc = noswz_desc(ax_base + b * AX_BYTES, 128, 256);
                             mma_bf16_pair(d_main, adesc, noswz_desc(xs, 128, 256), idesc, 0u);
                             mma_bf16_pair(d_corr, adesc, noswz_desc(xs + XHALF, 128, 256), idesc, 0u);
@@ -327,12 +356,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                         }
                         if (l > 0) {
                             for (int ks = 0; ks < KSL; ++ks) {
+                                // the slab's stages: [hi | lo'] in one, or hi then lo' in the next
+                                const int st2 = (SPS == 2 && stage + 1 == STAGES) ? 0 : stage + SPS - 1;
+                                const uint32_t ph2 = (SPS == 2 && stage + 1 == STAGES) ? phase ^ 1u : phase;
                                 const unsigned long long c0 = prof_clock();
                                 mbar_wait(&full[stage], phase);
+                                if (SPS == 2) mbar_wait(&full[st2], ph2);
                                 pw_f += prof_clock() - c0;
                                 tc_fence_after();
                                 const uint32_t aoff = static_cast<uint32_t>(kh * KSL + ks) * A_SLAB;
-                                const uint32_t bhi = s_base + static_cast<uint32_t>(stage) * CHUNK, blo = bhi + B_HALF;
+                                const uint32_t bhi = s_base + static_cast<uint32_t>(stage) * STAGE;
+                                const uint32_t blo = SPS == 2 ? s_base + static_cast<uint32_t>(st2) * STAGE : bhi + C::PLANE_B;
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk) {
                                     const uint32_t first = (acc || kh || ks || kk) ? 1u : 0u;
@@ -343,7 +377,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                                     mma_bf16_pair(d_corr, sw128_desc(alo + aoff + kk * 32), b_hi, idesc, 1u);
                                 }
                                 mma_commit_pair(&empty[stage], 3);
-                                if (++stage == STAGES) stage = 0, phase ^= 1u;
+                                if (SPS == 2) mma_commit_pair(&empty[st2], 3);
+                                for (int sub = 0; sub < SPS; ++sub)
+                                    if (++stage == STAGES) stage = 0, phase ^= 1u;
                             }
                         }
                         if (l == 0) mma_commit_pair(&d_full[nh], 3);
@@ -363,7 +399,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         const int e = warp - 2;
         const uint32_t quad = static_cast<uint32_t>(warp & 3);
         const int ch = e >> 2;
-        const uint32_t row = quad * 32 + lane;
+        // width 256: lane quadrant = 32 rows, all of the n-half's columns; width 512 ("2x2"
+        // accumulator): quadrants 0/1 = rows 0-31/32-63 of n-half columns 0-127, 2/3 = the same
+        // rows of columns 128-255
+        const uint32_t row = (N == 256 ? quad : (quad & 1u)) * 32 + lane;
+        const int cq = N == 256 ? 0 : static_cast<int>(quad >> 1) * 128;
+        const int part = (N == 256 ? 0 : static_cast<int>(quad >> 1) * 2) + ch;
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
         uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
@@ -384,6 +425,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     tc_fence_after();
                     const uint32_t tb = tmem + t_lane + static_cast<uint32_t>(j * 256 + ch * COLS);
                     static_assert(COLS == 64, "two 32-column chunks per thread per half");
+                    const int col0 = j * NHO + cq + ch * COLS;
                     // truncation compensation: rz_comp x (MMAs into main) x 2^-23, times
                     // sign(main) x 2^exponent(main) = the main accumulator's ulp, signed
                     const float kf = a.rz_comp * static_cast<float>(l == 0 ? 1 : N / 16 + (ld.ext ? 1 : 0)) *
@@ -402,12 +444,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                     uint32_t rm2[32], rc2[32];
                     tmem_ld32_async(tb + 32, rm2);
                     tmem_ld32_async(tb + 128 + 32, rc2);
-                    epi32(ld, l, last, v, j * NHO + ch * COLS, row, Ahi, Alo, wo_s, dot, ovf);
+                    epi32<TM>(ld, l, last, v, col0, row, Ahi, Alo, wo_s, dot, ovf);
                     tmem_wait_tied(rm2);
                     tmem_wait_tied(rc2);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = combine(rm2[i], rc2[i], kf);
-                    epi32(ld, l, last, v, j * NHO + ch * COLS + 32, row, Ahi, Alo, wo_s, dot, ovf);
+                    epi32<TM>(ld, l, last, v, col0 + 32, row, Ahi, Alo, wo_s, dot, ovf);
                     pe_w += prof_clock() - c1;
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
@@ -422,7 +464,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
                 mbar_wait(&out_empty[b], oe_ph[b]);
                 oe_ph[b] ^= 1u;
             }
-            dotbuf[(b * 2 + ch) * TM + row] = ovf ? -INFINITY : (dot.x + dot.y) + (dot.z + dot.w);
+            dotbuf[(b * PARTS + part) * TM + row] = ovf ? -INFINITY : (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
             pe_o += prof_clock() - c3;
@@ -439,13 +481,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         // the tile two ahead (same parity), whose point loads are issued before the wait.
         const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
         uint32_t of_ph[2] = {0u, 0u};
-        float px[4][3];
+        float px[RQ][3];
         auto load_points = [&](int64_t t) {
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < RQ; ++q) {
                 const int32_t r = static_cast<int32_t>(rank * TM + q * 32 + lane);
                 const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
                 px[q][0] = xp[0];
@@ -455,7 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
         };
         auto store_ax = [&](int b) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < RQ; ++q)
                 write_ax(AX + b * AX_BYTES, static_cast<uint32_t>(q * 32) + lane, (px[q][0] - a.shift[0]) * a.scale[0],
                          (px[q][1] - a.shift[1]) * a.scale[1], (px[q][2] - a.shift[2]) * a.scale[2]);
             fence_proxy_async_smem();
@@ -481,19 +523,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
             of_ph[b] ^= 1u;
             // every MMA of tile t has completed, so AX[b] is free for tile t + 2 npairs
             if (next) store_ax(b);
-            float delta[4];
+            float delta[RQ];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < RQ; ++q) {
                 const int r = q * 32 + static_cast<int>(lane);
-                const float p0 = dotbuf[(b * 2) * TM + r], p1 = dotbuf[(b * 2 + 1) * TM + r];
-                // either half saw an fp16 overflow: -inf, whatever the other half's partial holds
-                delta[q] = (p0 == -INFINITY || p1 == -INFINITY) ? -INFINITY : (p0 + p1) + a.bo;
+                float p[PARTS];
+                bool inf = false;
+#pragma unroll
+                for (int i = 0; i < PARTS; ++i) {
+                    p[i] = dotbuf[(b * PARTS + i) * TM + r];
+                    inf |= p[i] == -INFINITY;
+                }
+                const float sum = PARTS == 2 ? p[0] + p[1] : (p[0] + p[1]) + (p[PARTS - 2] + p[PARTS - 1]);
+                // a part saw an fp16 overflow: -inf, whatever the other parts hold
+                delta[q] = inf ? -INFINITY : sum + a.bo;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_empty[b]);
             unsigned long long key = ~0ull;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < RQ; ++q) {
                 const int32_t rr = static_cast<int32_t>(rank * TM + q * 32 + lane);
                 if (rr < nrows) {
                     if (a.per_point) a.per_point[obase + rr] = delta[q];
@@ -526,16 +575,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::THREADS, 1)
     if (warp == 1) tmem_dealloc_pair(tmem, 512);
 }
 
-cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st) {
+template <int N>
+static cudaError_t launch_split_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    using C = sp::Cfg<N>;
     static SmemOptIn opt;
-    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_split_kernel), (int)sp::SMEM);
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_split_kernel<N>), (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;
-    const cudaError_t le = launch_fused_pdl(fused_split_kernel, static_cast<unsigned>(2 * pairs), sp::THREADS,
-                                            sp::SMEM, st, a);
+    const cudaError_t le = launch_fused_pdl(fused_split_kernel<N>, static_cast<unsigned>(2 * pairs), C::THREADS,
+                                            C::SMEM, st, a);
     return le != cudaSuccess ? le : cudaGetLastError();
+}
+
+cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    switch (a.N) {
+        case 256: return launch_split_n<256>(a, num_sms, st);
+        case 512: return launch_split_n<512>(a, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
 }
 
 // ---------------------------------------------------------------- K0 (split) --
@@ -545,12 +604,15 @@ struct QNormS {
     float shift[kMaxIn], scale[kMaxIn];
 };
 
+template <int N>
 __global__ void split_ext_kernel(const float* __restrict__ q01, int dof, int n_mb, const float* __restrict__ wq,
                                  const float* __restrict__ base_bias, const float* __restrict__ wx_slots,
                                  uint8_t* __restrict__ ext, const QNormS qn, unsigned long long* keys,
                                  unsigned int* counters, int64_t n_keys) {
     pdl_launch_dependents();  // the fused kernel may start its prologue now (it pdl_wait()s for our writes)
     using namespace sp;
+    constexpr int NHO = Cfg<N>::NHO, BRH = Cfg<N>::BRH;
+    constexpr uint32_t XHALF = Cfg<N>::XHALF;
     const int64_t m = blockIdx.x;
     const int slot = blockIdx.y;
     if (keys && slot == 0 && threadIdx.x == 0 && m < n_keys) {
@@ -597,8 +659,12 @@ cudaError_t launch_split_ext(const FusedArgs& a, const float* wq, const float* m
         qn.scale[k] = a.scale[3 + k];
     }
     dim3 grid(static_cast<unsigned>(a.M), a.n_mb > 0 ? a.n_mb : 1);
-    split_ext_kernel<<<grid, 256, 0, st>>>(a.q01, a.dof, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn, keys_init,
-                                           counters_init, n_keys);
+    if (a.N == 512)
+        split_ext_kernel<512><<<grid, 256, 0, st>>>(a.q01, a.dof, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn, keys_init,
+                                                    counters_init, n_keys);
+    else
+        split_ext_kernel<256><<<grid, 256, 0, st>>>(a.q01, a.dof, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn, keys_init,
+                                                    counters_init, n_keys);
     return cudaGetLastError();
 }
 

@@ -221,10 +221,12 @@ def test_classification_with_calibrated_output_bias(key):
         print(f"{key} {prec}: free {r.free.mean():.2f}, ambiguous {int(amb.sum())}/48")
 
 
-@pytest.mark.parametrize("key,M,P,seed", [("c1", 1, 4096, 3), ("c2", 8, 3000, 3), ("c2", 16, 4096, 2024)])
+@pytest.mark.parametrize("key,M,P,seed", [("c1", 1, 4096, 3), ("c2", 8, 3000, 3), ("c2", 16, 4096, 2024),
+                                          ("c3", 4, 3000, 8), ("c4", 3, 2500, 8), ("c3", 1, 129, 9)])
 def test_fp32_split_within_stated_bound(key, M, P, seed):
-    """fp32_split (width 256 on tcgen05, split-fp16): within the frozen bound of the network,
-    and the fused min/argmin equal those of its own per-point output."""
+    """fp32_split (split-fp16 on tcgen05; width 256: 128 rows per CTA, width 512: 64 rows per
+    CTA on M=128 pair MMAs): within the frozen bound of the network (1e-5 at width 256), and
+    the fused min/argmin equal those of its own per-point output."""
     w, pts, q, params = _case(key, M, P, seed)
     r = S.Model(w.program, params).query_min(pts, q, w.margin, precision="fp32_split", per_point=True)
     omin, oarg, ofree, opp = _oracle(w.program, params, pts, q, w.margin)
@@ -238,12 +240,20 @@ def test_fp32_split_within_stated_bound(key, M, P, seed):
     assert np.array_equal(r.free[~amb], ofree[~amb])
 
 
-def test_fp32_split_unsupported_at_width_512():
+def test_fp32_split_width_512_forward_eval_mixed_motions():
+    """forward_eval rows of mixed motions (the a-8 path, tile table of 128-row tiles) on the
+    width-512 split kernel: within the bound, and batch-invariant (rows evaluated alone give
+    the same bits)."""
     w = WORKLOADS["c3"]
-    model = S.Model(w.program, S.init_params(w.program, 1, w.bound))
-    pts, q = w.make(seed=1, motions=1, points=10)
-    with pytest.raises(S.SvnError, match="fp32_split"):
-        model.query_min(pts, q, w.margin, precision="fp32_split")
+    params = S.init_params(w.program, 4, w.bound)
+    pts, q = w.make(seed=4, motions=5, points=300)
+    idx = np.arange(300)
+    rows = np.concatenate([pts, q[idx % 5]], axis=1).astype(np.float32)
+    m = S.Model(w.program, params)
+    out = m.forward_eval(rows, precision="fp32_split")
+    ref = O.forward_eval(w.program, params, rows)
+    assert np.abs(out.astype(np.float64) - ref).max() <= FP32_SPLIT_BOUND[w.program.name]
+    assert np.array_equal(m.forward_eval(rows[7:8], precision="fp32_split"), out[7:8])
 
 
 @pytest.mark.parametrize("width,blocks", [(256, 3), (512, 5)])
