@@ -1,8 +1,8 @@
 """Parity report: every BASELINE config's network through the CUDA path (C-ABI) against the
-CPU oracle, on bounded seeded samples, written as JSON (profiles/r1_parity_report.json).
+CPU oracle, on bounded seeded samples, written as JSON (profiles/r2_parity_report.json).
 
 Test infrastructure (it imports oracle/), run on a GPU box:
-    python tests/parity_report.py [--out profiles/r1_parity_report.json]
+    python tests/parity_report.py [--out profiles/r2_parity_report.json]
 
 Per (config, precision) it records the per-point max |delta_gpu - delta_oracle| against the
 stated tolerance (fp32: 1e-5 — met bit-identically, fp32_split and bf16: the frozen bounds of
@@ -39,8 +39,8 @@ FP32_SPLIT_BOUND = {k: v["bound"] for k, v in _F.items() if isinstance(v, dict)}
 CASES = [
     ("c1", 1, 4096, ["fp32", "fp32_split", "bf16"]),
     ("c2", 64, 2048, ["fp32", "fp32_split", "bf16"]),
-    ("c3", 16, 2048, ["bf16", "fp32"]),
-    ("c4", 16, 2048, ["bf16", "fp32"]),
+    ("c3", 16, 2048, ["bf16", "fp32", "fp32_split"]),
+    ("c4", 16, 2048, ["bf16", "fp32", "fp32_split"]),
 ]
 
 
@@ -90,7 +90,7 @@ def one(w, params, pts, q, prec, threads, oracle_out, truth=None):
 
 def main() -> int:
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=str(ROOT / "profiles" / "r1_parity_report.json"))
+    ap.add_argument("--out", default=str(ROOT / "profiles" / "r2_parity_report.json"))
     ap.add_argument("--seed", type=int, default=2024)
     args = ap.parse_args()
     threads = os.cpu_count() or 1
