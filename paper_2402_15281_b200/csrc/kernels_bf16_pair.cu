@@ -32,9 +32,14 @@
 
 namespace svn {
 
-template <int N>
+// TM_ = rows per CTA: 128 (M=256 pair MMAs, the throughput kernel) or 64 (M=128 pair MMAs,
+// for launches with fewer 256-row tiles than CTA pairs: half the rows per tile halves the
+// latency of a tile's pass through the network).  At TM=64 a CTA's 64 x NH accumulator sits in
+// TMEM's "2x2" layout (lanes 0-63: columns 0..NH/2-1, lanes 64-127: columns NH/2..NH-1, NH/2
+// TMEM columns); the B side (weights, extension rows) is the same at both sizes.
+template <int N, int TM_ = 128>
 struct PairCfg {
-    static constexpr int TM = 128;                   // rows per CTA (pair tile = 256)
+    static constexpr int TM = TM_;                   // rows per CTA (pair tile = 2 TM)
     static constexpr int NH = N / 2;                 // MMA N = one output half
     static constexpr int BR = NH / 2;                // B rows per CTA per chunk
     static constexpr int KSL = NH / 64;              // 64-wide K slabs per k-half
@@ -43,16 +48,18 @@ struct PairCfg {
     static constexpr uint32_t AX_BYTES = TM * 32;    // K=16 extension of A (4 KiB)
     static constexpr uint32_t CHUNK = BR * 128;      // per-CTA main weight chunk
     static constexpr uint32_t XCHUNK = BR * 32;      // per-CTA extension chunk
-    static constexpr int STAGES = N >= 512 ? 5 : 8;
+    static constexpr int STAGES = N >= 512 ? (TM == 128 ? 5 : 8) : 8;
     static constexpr int EPI_WARPS = 8;
     static constexpr int OUT_WARP = 2 + EPI_WARPS;   // keys / per-point outputs / A extensions
     static constexpr int THREADS = 64 + EPI_WARPS * 32 + 32;
-    static constexpr int COLS = NH / 2;              // columns per epilogue thread per half
+    static constexpr int COLS = TM == 128 ? NH / 2 : NH / 4;  // columns per epilogue thread per half
+    static constexpr int PARTS = TM == 128 ? 2 : 4;  // partial output dots per row (epilogue threads)
+    static constexpr int RQ = TM / 32;               // 32-row groups per CTA (output warp)
     static constexpr uint32_t OFF_AX = A_BYTES;
     static constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
     static constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * CHUNK;
     static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
-    static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
+    static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * PARTS * TM * 4;
     static constexpr int TQ = 8;                     // tile queue entries (dynamic schedule)
     static constexpr int XR = 3;                     // ext ring slots per CTA (tiles in flight)
     static constexpr uint32_t SMEM = OFF_BAR + 384;  // 22 + TQ barriers, TQ tile ids, TMEM slot
@@ -87,7 +94,7 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 }
 
 // Epilogue of 32 columns of one row (the MMA already added bias and x-part).
-template <int N>
+template <int N, int TM>
 __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
                                            uint8_t* A, const float* wo_s, float4& dot) {
     const int fl = ld.flags;
@@ -129,14 +136,14 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
                 p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
                 p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
             }
-            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, 128)) = p;
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
         }
         return;
     }
     if (act && res && !aff && !last) {  // folded Fig. 2 block: h~ += ReLU(a), as bf16x2
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            uint4* slot = reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, 128));
+            uint4* slot = reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
             const uint4 o = *slot;
             uint4 p;
             p.x = add_bf16x2(pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
@@ -165,7 +172,7 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
     if (res) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const uint4 o = *reinterpret_cast<const uint4*>(A + sw128_offset(row, c0 + 8 * u, 128));
+            const uint4 o = *reinterpret_cast<const uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
             v[8 * u + 0] += bflo(o.x);
             v[8 * u + 1] += bfhi(o.x);
             v[8 * u + 2] += bflo(o.y);
@@ -193,7 +200,7 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
             p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
             p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
             p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
-            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, 128)) = p;
+            *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
         }
     }
 }
@@ -249,10 +256,10 @@ __device__ __noinline__ void build_ext(const FusedArgs& a, int32_t motion, uint8
     }
 }
 
-template <int N>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS, 1)
+template <int N, int TMR>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THREADS, 1)
     fused_bf16_pair_kernel(const __grid_constant__ FusedArgs a) {
-    using C = PairCfg<N>;
+    using C = PairCfg<N, TMR>;
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* A = smem;
     uint8_t* AX = smem + C::OFF_AX;  // [2][AX_BYTES]
@@ -465,7 +472,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
         const int e = warp - 2;
         const uint32_t quad = static_cast<uint32_t>(warp & 3);
         const int ch = e >> 2;
-        const uint32_t row = quad * 32 + lane;  // row within this CTA's 128
+        // TM=128: lane quadrant = 32 rows, all of the n-half's columns.  TM=64 ("2x2"
+        // accumulator): quadrants 0/1 = rows 0-31/32-63 of the n-half's columns 0..NH/2-1,
+        // 2/3 = the same rows of columns NH/2..NH-1.
+        const uint32_t row = (C::TM == 128 ? quad : (quad & 1u)) * 32 + lane;  // row within this CTA
+        const int cq = C::TM == 128 ? 0 : static_cast<int>(quad >> 1) * (C::NH / 2);
+        const int part = (C::TM == 128 ? 0 : static_cast<int>(quad >> 1) * 2) + ch;
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
         uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
@@ -486,19 +498,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                     {
                         // rolling pipeline over 32-column chunks: the next TMEM load is in
                         // flight while the current chunk is packed and stored
-                        const int c0 = j * C::NH + ch * C::COLS;
+                        const int tc0 = j * C::NH + ch * C::COLS;  // TMEM column of the chunk
+                        const int c0 = tc0 + cq;                   // its output column
                         constexpr int NCH = C::COLS / 32;
                         uint32_t ra[32], rb[32];
                         const uint32_t tb = tmem + t_lane;
-                        tmem_ld32_async(tb + static_cast<uint32_t>(c0), ra);
-                        tmem_ld32_async(tb + static_cast<uint32_t>(c0 + 32), rb);
+                        tmem_ld32_async(tb + static_cast<uint32_t>(tc0), ra);
+                        tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32), rb);
                         tmem_wait_tied2(ra, rb);
 #pragma unroll
                         for (int q = 0; q < NCH; q += 2) {
-                            pair_epi32<N>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot);
-                            if (q + 2 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(c0 + 32 * (q + 2)), ra);
-                            pair_epi32<N>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot);
-                            if (q + 3 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(c0 + 32 * (q + 3)), rb);
+                            pair_epi32<N, C::TM>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot);
+                            if (q + 2 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32 * (q + 2)), ra);
+                            pair_epi32<N, C::TM>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot);
+                            if (q + 3 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32 * (q + 3)), rb);
                             if (q + 2 < NCH) tmem_wait_tied2(ra, rb);
                         }
                     }
@@ -518,7 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
                 mbar_wait(&out_empty[b], oe_ph[b]);
                 oe_ph[b] ^= 1u;
             }
-            dotbuf[(b * 2 + ch) * C::TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
+            dotbuf[(b * C::PARTS + part) * C::TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
             pe_o += prof_clock() - c3;
@@ -536,14 +549,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
         // the tile two ahead (same parity), whose point loads are issued before the wait.
         const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
         uint32_t of_ph[2] = {0u, 0u};
-        float px[4][3];
+        float px[C::RQ][3];
         unsigned long long pe_x = 0;
         auto load_points = [&](int64_t t) {
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * C::TM, motion, pbase, obase, nrows);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < C::RQ; ++q) {
                 const int32_t r = static_cast<int32_t>(rank * C::TM + q * 32 + lane);
                 const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
                 px[q][0] = xp[0];
@@ -553,7 +566,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
         };
         auto store_ax = [&](int b) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
+            for (int q = 0; q < C::RQ; ++q)
                 write_ax(AX + b * C::AX_BYTES, static_cast<uint32_t>(q * 32) + lane,
                          (px[q][0] - a.shift[0]) * a.scale[0], (px[q][1] - a.shift[1]) * a.scale[1],
                          (px[q][2] - a.shift[2]) * a.scale[2]);
@@ -654,17 +667,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
             const unsigned long long c0 = prof_clock();
             // every MMA of tile t has completed, so AX[b] is free for tile t + 2 npairs
             if (next) store_ax(b);
-            float delta[4];
+            float delta[C::RQ];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < C::RQ; ++q) {
                 const int r = q * 32 + static_cast<int>(lane);
-                delta[q] = (dotbuf[(b * 2) * C::TM + r] + dotbuf[(b * 2 + 1) * C::TM + r]) + a.bo;
+                const float* d = dotbuf + (b * C::PARTS) * C::TM + r;
+                delta[q] = (C::PARTS == 2 ? d[0] + d[C::TM] : (d[0] + d[C::TM]) + (d[2 * C::TM] + d[3 * C::TM])) + a.bo;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_empty[b]);
             unsigned long long key = ~0ull;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < C::RQ; ++q) {
                 const int32_t rr = static_cast<int32_t>(rank * C::TM + q * 32 + lane);
                 if (rr < nrows) {
                     if (a.per_point) a.per_point[obase + rr] = delta[q];
@@ -705,16 +719,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N>::THREADS,
     if (warp == 1) tmem_dealloc_pair(tmem, N);
 }
 
-template <int N>
+template <int N, int TM>
 static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
-    using C = PairCfg<N>;
+    using C = PairCfg<N, TM>;
     static SmemOptIn opt;
-    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pair_kernel<N>), (int)C::SMEM);
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pair_kernel<N, TM>), (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;
-    const cudaError_t le = launch_fused_pdl(fused_bf16_pair_kernel<N>, static_cast<unsigned>(2 * pairs), C::THREADS,
+    const cudaError_t le = launch_fused_pdl(fused_bf16_pair_kernel<N, TM>, static_cast<unsigned>(2 * pairs), C::THREADS,
                                             C::SMEM, st, a);
     return le != cudaSuccess ? le : cudaGetLastError();
 }
@@ -722,7 +736,8 @@ static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t s
 cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t st) {
     switch (a.N) {
         case 256: return launch_fused_bf16_pp(a, num_sms, st);  // two tiles in flight (kernels_bf16_pp.cu)
-        case 512: return launch_pair_n<512>(a, num_sms, st);
+        case 512:  // 128-row pair tiles for launches with fewer 256-row tiles than pairs (abi tile_rows_for)
+            return a.tile_rows == 128 ? launch_pair_n<512, 64>(a, num_sms, st) : launch_pair_n<512, 128>(a, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
