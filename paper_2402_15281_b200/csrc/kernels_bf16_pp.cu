@@ -192,8 +192,8 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
 
 #ifdef SVN_CTA_TIMES
 // Per-CTA globaltimer stamps of the last launch (entry, after the prologue and pdl_wait,
-// exit), read back by svn_debug_cta_times (scripts/cta_times.py); instrumented builds only.
-__device__ unsigned long long g_cta_times[3 * 1024];
+// exit) and the SM it ran on, read back by svn_debug_cta_times (scripts/cta_times.py); instrumented builds only.
+__device__ unsigned long long g_cta_times[4 * 1024];
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -205,7 +205,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     fused_bf16_pp_kernel(const __grid_constant__ FusedArgs a) {
     using namespace pp;
 #ifdef SVN_CTA_TIMES
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[3 * blockIdx.x] = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[4 * blockIdx.x] = gtimer();
 #endif
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* Abuf = smem;                      // [2][A_BYTES]
@@ -270,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     const uint32_t tmem = *tmem_slot;
     pdl_wait();  // K0 (keys, counters, tile queue, extension rows) has completed
 #ifdef SVN_CTA_TIMES
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[3 * blockIdx.x + 1] = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[4 * blockIdx.x + 1] = gtimer();
 #endif
 
     if (warp == 0) {
@@ -567,13 +567,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     tc_fence_after();
     if (warp == 1) tmem_dealloc_pair(tmem, 512);
 #ifdef SVN_CTA_TIMES
-    if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[3 * blockIdx.x + 2] = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_cta_times[4 * blockIdx.x + 2] = gtimer();
+        g_cta_times[4 * blockIdx.x + 3] = smid;
+    }
 #endif
 }
 
 #ifdef SVN_CTA_TIMES
 extern "C" __attribute__((visibility("default"))) int svn_debug_cta_times(unsigned long long* out, int n) {
-    return static_cast<int>(cudaMemcpyFromSymbol(out, g_cta_times, sizeof(unsigned long long) * 3 * n));
+    return static_cast<int>(cudaMemcpyFromSymbol(out, g_cta_times, sizeof(unsigned long long) * 4 * n));
 }
 #endif
 
