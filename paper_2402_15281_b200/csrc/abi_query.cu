@@ -405,6 +405,16 @@ svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw
 }
 
 
+constexpr int64_t kSmallStagingPoints = 8192;  // above it the DMA copy is faster (20000 points: +9 us)
+
+bool small_staging_enabled() {  // SVN_SMALL_STAGING=0: DMA copies for every call (A/B hook)
+    static const bool on = [] {
+        const char* e = std::getenv("SVN_SMALL_STAGING");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // svn_query_min / svn_predict_min_distance: inputs from host memory, outputs to host memory.
 // fill(pts, q) writes the call's float inputs into the pinned staging block; points/q01 are
 // the caller's float arrays (null for predict_min_distance, whose double inputs are converted
@@ -443,20 +453,29 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         float* dpp = nullptr;
         if (per_point)
             SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dpp), sizeof(float) * P * M), "cudaMallocAsync");
+        // small staged calls (the reference's per-motion predict_min_distance): a kernel pulls the
+        // inputs out of the pinned block and the fused finaliser writes (min, argmin, free)
+        // straight into it — no DMA copy on the critical path (each costs ~5-10 us of setup)
+        const bool small = !direct && !per_point && P <= kSmallStagingPoints && M <= 64 && small_staging_enabled();
         if (direct) {
             SVN_CUDA(cudaMemcpyAsync(sg.dev, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
             SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),
                      "H2D motions");
+        } else if (small) {
+            SVN_CUDA(launch_stage_in(sg.host, sg.dev, o_min, st), "stage_in kernel");
+            ++g_launches;
         } else {
             SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
         }
+        uint8_t* const out = small ? sg.host : sg.dev;
         const svn_status s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
                                          reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
-                                         reinterpret_cast<float*>(sg.dev + o_min),
-                                         reinterpret_cast<int32_t*>(sg.dev + o_arg), sg.dev + o_free, dpp, nullptr, st);
+                                         reinterpret_cast<float*>(out + o_min), reinterpret_cast<int32_t*>(out + o_arg),
+                                         out + o_free, dpp, nullptr, st);
         if (s != SVN_OK) return s;
-        SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
-                 "D2H min/argmin/free");
+        if (!small)
+            SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
+                     "D2H min/argmin/free");
         if (per_point)
             SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
     }

@@ -233,6 +233,7 @@ cudaError_t launch_motion_bias(const FusedArgs& a, const float* wq /*[n_mb][2dof
                                unsigned long long* keys_init, unsigned int* counters_init, int64_t n_keys,
                                cudaStream_t st);
 cudaError_t launch_keys_init(unsigned long long* keys, int64_t M, cudaStream_t st);
+cudaError_t launch_stage_in(const void* host_src, void* dev_dst, size_t bytes, cudaStream_t st);
 cudaError_t launch_grid_points(const double* origin, double voxel, const int32_t* dims, float* pts, cudaStream_t st);
 cudaError_t launch_keys_finalize(const unsigned long long* keys, int64_t M, double margin, float* min_out,
                                  int32_t* argmin_out, uint8_t* free_out, cudaStream_t st);

@@ -12,6 +12,8 @@
 // delta matches the reference's own nn.cpp (oracle/ref) and the C restatement bit for bit.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <cstdlib>
 
 #include "fused.cuh"
@@ -73,6 +75,24 @@ cudaError_t launch_motion_bias(const FusedArgs& a, const float* wq, const float*
 __global__ void keys_init_kernel(unsigned long long* keys, int64_t M) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i < M) keys[i] = ~0ull;
+}
+
+// Small host-buffer calls: the pinned staging block's inputs copied to the device by a kernel
+// reading host memory directly (unified addressing) — for a few tens of KiB this lands sooner
+// than a DMA copy, whose setup latency dominates at that size.  16-byte words, grid-stride.
+__global__ void stage_in_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t n16) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n16;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
+cudaError_t launch_stage_in(const void* host_src, void* dev_dst, size_t bytes, cudaStream_t st) {
+    const int64_t n16 = static_cast<int64_t>((bytes + 15) / 16);
+    if (n16 <= 0) return cudaSuccess;
+    const int64_t blocks = std::min<int64_t>((n16 + 255) / 256, 256);
+    stage_in_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(static_cast<const uint4*>(host_src),
+                                                                   static_cast<uint4*>(dev_dst), n16);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_keys_init(unsigned long long* keys, int64_t M, cudaStream_t st) {
