@@ -109,6 +109,9 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 // (toward zero), so after n instructions main sits on average ~n x c x ulp below |exact|.
 // sign|exponent bits of main as a float = +-2^e; times kf = c x n x 2^-23 = the signed loss.
 __device__ __forceinline__ float combine(uint32_t m, uint32_t c, float kf) {
+#ifdef SVN_SPLIT_NO_RZ  // A/B build: the uncompensated combine
+    return fmaf(__uint_as_float(c), LO_INV, __uint_as_float(m));
+#endif
     const float mf = __uint_as_float(m);
     const float se = __uint_as_float(m & 0xff800000u);
     return fmaf(__uint_as_float(c), LO_INV, fmaf(se, kf, mf));
@@ -121,7 +124,11 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
                                       uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot, bool& ovf) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
+#ifndef SVN_SPLIT_NO_NANCHECK  // A/B build without the non-finite input check
     if (l == 0 || (fl & kConcat)) {
+#else
+    if (false) {
+#endif
         // the layer's K=16 extension carries z_x (and b_m) as fp16 splits: an input beyond the
         // fp16 range arrives as inf / NaN, which the ReLU below would turn into 0.  v * 0 is
         // NaN exactly for a non-finite v.
