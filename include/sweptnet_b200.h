@@ -70,9 +70,10 @@ typedef enum {
  *              accumulators (the tensor core's per-instruction truncation compensated in the
  *              epilogue), per-motion q-fold.  Not in the reference's rounding order:
  *              per-point delta within the bound of tests/golden/fp32_split_bounds.json —
- *              the 1e-5 FP32 bar at width 256, a stated bound of 2.3e-5 to 2.6e-5 for the
- *              width-512 plain/DeepSDF networks (UNSUPPORTED at other widths or when a
- *              weight exceeds 1e4).  A row whose hidden activation reaches the fp16 range
+ *              the 1e-5 FP32 bar at width 256 and for the reference's Fig. 2 networks, a
+ *              stated bound of 2.2e-5 to 2.5e-5 for the width-512 plain/DeepSDF networks
+ *              (UNSUPPORTED at other widths or when a weight exceeds 1e4).  A row whose
+ *              hidden activation reaches the fp16 range
  *              (|h| >= 65520) or whose input is not finite is reported as delta = -inf: its
  *              motion's min is -inf and its class "not free" (handed to the exact checker),
  *              never dropped. */

@@ -106,15 +106,24 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 
 // main + corr / 2048, with main's expected truncation loss added back: the tensor core's
 // fp32 accumulator drops the bits below its 24-bit significand at every MMA instruction
-// (toward zero), so after n instructions main sits on average ~n x c x ulp below |exact|.
-// sign|exponent bits of main as a float = +-2^e; times kf = c x n x 2^-23 = the signed loss.
-__device__ __forceinline__ float combine(uint32_t m, uint32_t c, float kf) {
-#ifdef SVN_SPLIT_NO_RZ  // A/B build: the uncompensated combine
-    return fmaf(__uint_as_float(c), LO_INV, __uint_as_float(m));
-#endif
-    const float mf = __uint_as_float(m);
-    const float se = __uint_as_float(m & 0xff800000u);
-    return fmaf(__uint_as_float(c), LO_INV, fmaf(se, kf, mf));
+// (toward zero), so after n instructions main sits on average ~c x n ulps below |exact|.  The
+// loss is taken proportional to |main| (one ulp is between 2^-24 and 2^-23 of |main|; c
+// absorbs the mean): v = main x (1 + c n 2^-23) + corr x 2^-11, for two columns at once with
+// the packed fp32 pair ops (two independent round-to-nearest results each) — one instruction
+// per column, as many as the uncompensated fma(corr, 2^-11, main).
+__device__ __forceinline__ void combine32(const uint32_t* m, const uint32_t* c, float kmul, float* v) {
+    unsigned long long k2, s2;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(k2) : "f"(kmul));
+    asm("mov.b64 %0, {%1, %1};" : "=l"(s2) : "f"(LO_INV));
+#pragma unroll
+    for (int i = 0; i < 32; i += 2) {
+        unsigned long long mm, cc, t;
+        asm("mov.b64 %0, {%1, %2};" : "=l"(mm) : "r"(m[i]), "r"(m[i + 1]));
+        asm("mov.b64 %0, {%1, %2};" : "=l"(cc) : "r"(c[i]), "r"(c[i + 1]));
+        asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(t) : "l"(cc), "l"(s2));
+        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(t) : "l"(mm), "l"(k2));
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(v[i]), "=f"(v[i + 1]) : "l"(t));
+    }
 }
 
 // 32 output columns of one row: v (fp32, already main + corr/2048) -> act / affine /
@@ -433,10 +442,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS,
                     const uint32_t tb = tmem + t_lane + static_cast<uint32_t>(j * 256 + ch * COLS);
                     static_assert(COLS == 64, "two 32-column chunks per thread per half");
                     const int col0 = j * NHO + cq + ch * COLS;
-                    // truncation compensation: rz_comp x (MMAs into main) x 2^-23, times
-                    // sign(main) x 2^exponent(main) = the main accumulator's ulp, signed
-                    const float kf = a.rz_comp * static_cast<float>(l == 0 ? 1 : N / 16 + (ld.ext ? 1 : 0)) *
-                                     (1.0f / 8388608.0f);
+                    // truncation compensation: main x (1 + rz_comp x (MMAs into main) x 2^-23)
+                    const float kmul =
+                        1.0f + a.rz_comp * static_cast<float>(l == 0 ? 1 : N / 16 + (ld.ext ? 1 : 0)) * (1.0f / 8388608.0f);
                     float v[32];
                     {
                         uint32_t rm[32], rc[32];
@@ -444,8 +452,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS,
                         tmem_ld32_async(tb + 128, rc);
                         tmem_wait_tied(rm);
                         tmem_wait_tied(rc);
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = combine(rm[i], rc[i], kf);
+                        combine32(rm, rc, kmul, v);
                     }
                     // second chunk's loads fly while the first chunk is split and stored
                     uint32_t rm2[32], rc2[32];
@@ -454,8 +461,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS,
                     epi32<TM>(ld, l, last, v, col0, row, Ahi, Alo, wo_s, dot, ovf);
                     tmem_wait_tied(rm2);
                     tmem_wait_tied(rc2);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = combine(rm2[i], rc2[i], kf);
+                    combine32(rm2, rc2, kmul, v);
                     epi32<TM>(ld, l, last, v, col0 + 32, row, Ahi, Alo, wo_s, dot, ovf);
                     pe_w += prof_clock() - c1;
                     tc_fence_before();
