@@ -5,6 +5,7 @@
 // in nn.cpp keep their CPU bodies.  Errors come back as the reference's own exception types and
 // texts (std::invalid_argument, nn.cpp:98-99,462,465).
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -83,6 +84,19 @@ uint64_t fingerprint(const Mlp& m) {
     return h;
 }
 
+// The arithmetic of the drop-in, read once from SWEPTNET_B200_PRECISION: "fp32_exact" (default:
+// the reference's float results bit for bit), "fp32_split" (fp32-grade on the tensor cores,
+// within 1e-5 on the reference's Fig. 2 networks) or "bf16" (the fastest; its stated bound).
+svn_precision precision() {
+    static const svn_precision p = [] {
+        const char* e = std::getenv("SWEPTNET_B200_PRECISION");
+        if (e && std::strcmp(e, "bf16") == 0) return SVN_PREC_BF16;
+        if (e && std::strcmp(e, "fp32_split") == 0) return SVN_PREC_FP32_SPLIT;
+        return SVN_PREC_FP32_EXACT;
+    }();
+    return p;
+}
+
 const svn_model* device_model(const Mlp& m) {
     static std::mutex mu;  // callers are parallel_for workers (bench.cpp:156,193)
     static std::unordered_map<const Mlp*, std::pair<uint64_t, svn_model*>> cache;
@@ -108,7 +122,7 @@ MlpT<float>::Vec forward_eval<float>(const MlpT<float>& model, const MlpT<float>
     if (raw.cols() != model.input_dim) throw std::invalid_argument("forward: input width mismatch");
     if (raw.rows() < 1) throw std::invalid_argument("forward: batch must be non-empty");
     MlpT<float>::Vec out(raw.rows());
-    check(svn_forward_eval(device_model(model), SVN_PREC_FP32_EXACT, raw.data(), raw.rows(), raw.cols(),
+    check(svn_forward_eval(device_model(model), precision(), raw.data(), raw.rows(), raw.cols(),
                            out.data()));  // raw is RowMajor (nn.hpp:18)
     return out;
 }
@@ -118,7 +132,7 @@ std::pair<double, int> predict_min_distance(const Mlp& model, const std::vector<
     double mn = 0;
     int32_t idx = 0;
     // std::vector<Vec3> is a contiguous double [P x 3] (Vec3 = Eigen::Vector3d, geometry.hpp:11)
-    check(svn_predict_min_distance(device_model(model), SVN_PREC_FP32_EXACT, cloud.front().data(),
+    check(svn_predict_min_distance(device_model(model), precision(), cloud.front().data(),
                                    static_cast<int64_t>(cloud.size()), m.q0.data(), m.q1.data(),
                                    static_cast<int32_t>(m.q0.size()), &mn, &idx));
     return {mn, idx};
