@@ -414,12 +414,22 @@ static int fp32_cg() {
     return v;
 }
 
+static int fp32_small_cg() {
+    static const int v = [] {
+        const char* e = std::getenv("SVN_FP32_SMALL_CG");
+        return e ? std::atoi(e) : 64;  // width 512: 8 warps per 32-row tile, -3 % per call at 3000 points
+    }();
+    return v;
+}
+
 cudaError_t launch_fused_fp32(const FusedArgs& a, int num_sms, cudaStream_t st) {
     if (a.tile_rows == kFp32SmallTile) {  // few tiles: 32-row tiles, 4 warps each (64 columns gave 8 warps
         switch (a.N) {                     // but measured 8 % slower on c1)
             case 128: return launch_fp32_n<128, 32, kFp32SmallTile>(a, num_sms, st);
             case 256: return launch_fp32_n<256, 32, kFp32SmallTile>(a, num_sms, st);
-            case 512: return launch_fp32_n<512, 32, kFp32SmallTile>(a, num_sms, st);
+            case 512:  // 8 warps per 32-row tile (8 x 8 register tiles); SVN_FP32_SMALL_CG=32: 4 warps
+                return fp32_small_cg() == 64 ? launch_fp32_n<512, 64, kFp32SmallTile>(a, num_sms, st)
+                                             : launch_fp32_n<512, 32, kFp32SmallTile>(a, num_sms, st);
             default: return cudaErrorInvalidValue;
         }
     }
