@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""CPU emulation of the fp32_split arithmetic on a plain network (c2's 4x256), to find
+"""CPU emulation of the fp32_split arithmetic on a plain or DeepSDF network (c2/c3/c4), to find
 which part of the tensor-core path carries its error against the oracle: operand storage
 (fp16 hi + lo'*2^-11 planes), the dropped lo'*lo' term, or the accumulation inside the
 tensor core (one rounding per K=16 MMA instruction, round-to-nearest or toward zero).
@@ -168,7 +168,7 @@ def main():
     prog = w.program
     pts, q = w.make(seed=a.seed, motions=16, points=a.points)
     q = q[:a.motions]
-    params = S.init_params(prog, a.seed, w.bound) if False else O.init_params(prog, a.seed, w.bound)
+    params = O.init_params(prog, a.seed, w.bound)
     _, _, _, opp = O.query_min(prog, params, pts, q, w.margin, per_point=True, threads=8)
     M = q.shape[0]
     raw = np.concatenate([np.repeat(pts[None].astype(np.float64), M, 0).reshape(-1, 3),
