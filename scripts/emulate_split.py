@@ -16,7 +16,6 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-import paper_2402_15281_b200 as S  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 from paper_2402_15281_b200.workloads import WORKLOADS  # noqa: E402
 
