@@ -86,6 +86,7 @@ struct svn_model {
     float* d_mbbase = nullptr; // [n_mb][N]
     float* d_wxslots = nullptr; // [n_mb][3][N] x-part columns of the concat layers
     bool has_bf16 = false;
+    bool has_mixed = false;   // width-512 bf16: rows of mixed motions without per-motion folding
     svn::FusedArgs base_bf16{};       // bf16 kernels: base with the BN affine folded (see fold_affine_bf16)
     float* d_wq_bf = nullptr;     // K0 inputs of the bf16 kernels, from the folded parameters
     float* d_mbbase_bf = nullptr;

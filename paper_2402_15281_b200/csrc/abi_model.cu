@@ -451,6 +451,44 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
             uint8_t* dxm = nullptr;
             if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return cleanup_fail(st);
             if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return cleanup_fail(st);
+            if (N == 512 && !wq_bf.empty()) {
+                // rows of mixed motions (forward_eval batches whose rows all differ in q): per
+                // (concat slot, n-half, CTA half r) four K=16 slabs of BR rows — [b hi, b lo, W_x
+                // splits] as in motion_ext_kernel but with the model bias, then W_q in (hi, lo, hi)
+                // triples matching the per-row A slabs (z_q hi, z_q hi, z_q lo) of the kernel
+                const int NH = N / 2, n_slots = static_cast<int>(mbbase_bf.size() / N);
+                std::vector<uint8_t> mix(static_cast<size_t>(n_slots) * 2 * 2 * 4 * BR * 32, 0);
+                for (int sl = 0; sl < n_slots; ++sl)
+                    for (int n = 0; n < N; ++n) {
+                        const int nh = n / NH, wi = n % NH, r = wi / BR, rr = wi % BR;
+                        uint8_t* blob = mix.data() + static_cast<size_t>(((sl * 2 + nh) * 2 + r) * 4) * BR * 32;
+                        auto put = [&](int sub, int k, __nv_bfloat16 v) {
+                            *reinterpret_cast<__nv_bfloat16*>(blob + sub * BR * 32 + ext_offset(rr, k)) = v;
+                        };
+                        __nv_bfloat16 hi, lo;
+                        split_bf16_host(mbbase_bf[static_cast<size_t>(sl) * N + n], hi, lo);
+                        put(0, 0, hi);
+                        put(0, 1, lo);
+                        for (int c = 0; c < 3; ++c) {
+                            split_bf16_host(wx_bf[(static_cast<size_t>(sl) * 3 + c) * N + n], hi, lo);
+                            put(0, 2 + 3 * c, hi);
+                            put(0, 3 + 3 * c, lo);
+                            put(0, 4 + 3 * c, hi);
+                        }
+                        for (int k = 0; k < nq; ++k) {
+                            split_bf16_host(wq_bf[(static_cast<size_t>(sl) * nq + k) * N + n], hi, lo);
+                            const int q0 = 3 * k;
+                            put(1 + q0 / 16, q0 % 16, hi);
+                            put(1 + (q0 + 1) / 16, (q0 + 1) % 16, lo);
+                            put(1 + (q0 + 2) / 16, (q0 + 2) % 16, hi);
+                        }
+                    }
+                uint8_t* dmix = nullptr;
+                if ((st = m->upload(mix.data(), mix.size(), &dmix)) != SVN_OK) return cleanup_fail(st);
+                if ((st = encode_blob_map(&a.tmap_xmix, dmix, 128, mix.size() / 128, 128)) != SVN_OK)
+                    return cleanup_fail(st);
+                m->has_mixed = 3 * nq <= 48;
+            }
             if ((st = m->upload(wq_bf.data(), wq_bf.size(), &m->d_wq_bf)) != SVN_OK) return cleanup_fail(st);
             if ((st = m->upload(mbbase_bf.data(), mbbase_bf.size(), &m->d_mbbase_bf)) != SVN_OK) return cleanup_fail(st);
             if ((st = m->upload(wx_bf.data(), wx_bf.size(), &m->d_wxslots_bf)) != SVN_OK) return cleanup_fail(st);

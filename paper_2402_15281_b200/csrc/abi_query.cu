@@ -346,9 +346,53 @@ svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw
             return SVN_OK;
         }
     }
-    const Kind kind = kernel_kind(m, prec);
+    Kind kind = kernel_kind(m, prec);
+    const int nq = 2 * m->dof;
+    if (kind != Kind::SIMT && !(kind == Kind::BF16 && m->N == 512 && m->has_mixed)) {
+        // rows of mostly distinct motions (segments shorter than 32 rows on average) would cost
+        // the folded tensor-core kernels one tile per segment; without a per-row q-part variant
+        // (width-512 bf16 has one, below) they run on the FP32 path, which reads each row's q and
+        // is exact — inside every stated bound, and faster than one tile per row
+        int64_t segs = 1;
+        for (int64_t r = 1; r < B && segs * 32 <= B; ++r)
+            segs += std::memcmp(raw_host + r * cols + 3, raw_host + (r - 1) * cols + 3, sizeof(float) * nq) != 0;
+        if (segs * 32 > B) kind = Kind::SIMT;
+    }
     const int TM0 = tile_rows(kind, m->N);
-    const int nq = 2 * m->dof, TM = tile_rows_for(kind, m->N, (B + TM0 - 1) / TM0, m->num_sms);
+    const int TM = tile_rows_for(kind, m->N, (B + TM0 - 1) / TM0, m->num_sms);
+    if (kind == Kind::SIMT) {
+        // the FP32 path does not fold q (exact order): every row reads its own q0|q1 from the raw
+        // batch, so tiles are cut over the rows regardless of motion — a batch whose rows all
+        // differ in motion (eval_mae, bench.cpp:80-88; training validation, nn.cpp:370) runs
+        // full tiles instead of one tile per row
+        std::vector<TileDesc> tiles;
+        for (int64_t t0 = 0; t0 < B; t0 += TM)
+            tiles.push_back(TileDesc{t0, t0, 0, static_cast<int32_t>(std::min<int64_t>(TM, B - t0))});
+        FusedArgs a = m->base;
+        a.exact = 1;
+        a.row_q = 1;
+        a.points = raw_dev;
+        a.point_stride = cols;
+        a.P = B;
+        a.M = 1;
+        a.q01 = raw_dev + 3;  // unused with row_q
+        a.n_tiles = static_cast<int64_t>(tiles.size());
+        a.tile_rows = TM;
+        a.tiles_per_motion = 1;
+        a.per_point = out_dev;
+        a.keys = nullptr;
+        a.counters = nullptr;
+        a.motion_bias = nullptr;
+        Scratch sc(st);
+        TileDesc* dt = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dt), sizeof(TileDesc) * tiles.size()), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(dt, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice, st),
+                 "H2D tiles");
+        a.tiles = dt;
+        SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
+        SVN_CUDA(cudaStreamSynchronize(st), "forward kernels");  // the host tile vector feeds an async copy
+        return SVN_OK;
+    }
     std::vector<float> qseg;
     std::vector<TileDesc> tiles;
     int64_t seg_start = 0;
@@ -364,6 +408,45 @@ svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw
         }
         ++nseg;
         seg_start = r;
+    }
+    if (kind == Kind::BF16 && m->N == 512 && m->has_mixed && static_cast<int64_t>(nseg) * 32 > B) {
+        // rows of mostly distinct motions (segments shorter than 32 rows on average): instead of
+        // one tile per segment, 128-row tiles over the rows with every concat layer's q-part
+        // computed per row by the tensor core (FusedArgs::mixed, kernels_bf16_pair.cu)
+        tiles.clear();
+        for (int64_t t0 = 0; t0 < B; t0 += 128)
+            tiles.push_back(TileDesc{t0, t0, 0, static_cast<int32_t>(std::min<int64_t>(128, B - t0))});
+        FusedArgs a = m->base_bf16;
+        a.mixed = 1;
+        a.points = raw_dev;
+        a.point_stride = cols;
+        a.q01 = raw_dev + 3;  // K0 reads no motion in this mode
+        a.P = B;
+        a.M = 1;
+        a.n_tiles = static_cast<int64_t>(tiles.size());
+        a.tile_rows = 128;
+        a.tiles_per_motion = 1;
+        a.per_point = out_dev;
+        a.keys = nullptr;
+        a.counters = nullptr;
+        a.ext_ring = nullptr;
+        a.tile_group = 1;
+        Scratch sc(st);
+        TileDesc* dt = nullptr;
+        unsigned int* sched = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&dt), sizeof(TileDesc) * tiles.size()), "cudaMallocAsync");
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&sched), sizeof(unsigned int)), "cudaMallocAsync");
+        SVN_CUDA(cudaMemcpyAsync(dt, tiles.data(), sizeof(TileDesc) * tiles.size(), cudaMemcpyHostToDevice, st),
+                 "H2D tiles");
+        a.tiles = dt;
+        a.sched = sched;
+        SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, nullptr, nullptr, nullptr, 0, sched,
+                                   st),
+                 "motion_ext kernel (tile counter reset)");
+        ++g_launches;
+        SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
+        SVN_CUDA(cudaStreamSynchronize(st), "forward kernels");
+        return SVN_OK;
     }
     FusedArgs a = kind == Kind::SPLIT ? m->base_split : kind == Kind::BF16 ? m->base_bf16 : m->base;
     a.exact = kind == Kind::SIMT ? 1 : 0;

@@ -41,6 +41,8 @@ struct FusedArgs {
     alignas(64) CUtensorMap tmap_w;   // weight stream viewed as [rows][128 B]
     alignas(64) CUtensorMap tmap_xm;  // model extension stream [rows][32 B]
     alignas(64) CUtensorMap tmap_xq;  // per-motion extension stream [rows][32 B]
+    alignas(64) CUtensorMap tmap_xmix;  // width-512 bf16, rows of mixed motions: per (concat slot,
+                                        // n-half, CTA half) 16 KiB = [b + x-part slab | 3 q slabs]
     // model
     int L, N, dof, in;
     LayerDev layer[kMaxLayers];
@@ -64,6 +66,10 @@ struct FusedArgs {
     int64_t n_tiles;
     const TileDesc* tiles;     // non-null: explicit tile table (forward_eval segments)
     int exact;                 // fp32 exact order (no q fold)
+    int row_q;                 // exact mode: each row's q0|q1 follows its x in `points` (forward_eval
+                               // rows of mixed motions; tiles then span motions)
+    int mixed;                 // width-512 bf16 kernel (64 rows per CTA): rows of mixed motions, the
+                               // q-part of every concat layer by the tensor core from per-row A slabs
     int tile_rows;             // rows per work item the host cut the tiles with (SIMT: 128/64, or 32)
     unsigned int* sched;       // width-512 bf16 kernel: dynamic tile counter (zeroed by K0)
     int tile_group;            // width-512 bf16 kernel: tiles per claimed chunk (1: per tile)

@@ -45,7 +45,10 @@ struct PairCfg {
     static constexpr int KSL = NH / 64;              // 64-wide K slabs per k-half
     static constexpr uint32_t A_SLAB = TM * 128;     // 16 KiB
     static constexpr uint32_t A_BYTES = TM * N * 2;
-    static constexpr uint32_t AX_BYTES = TM * 32;    // K=16 extension of A (4 KiB)
+    static constexpr uint32_t AX_BYTES = TM * 32;    // K=16 extension of A (one slab)
+    // per tile parity: the x slab, and at TM=64 three more for the per-row q-part of rows of
+    // mixed motions (FusedArgs::mixed)
+    static constexpr uint32_t AXP = TM == 64 ? 4 * AX_BYTES : AX_BYTES;
     static constexpr uint32_t CHUNK = BR * 128;      // per-CTA main weight chunk
     static constexpr uint32_t XCHUNK = BR * 32;      // per-CTA extension chunk
     static constexpr int STAGES = N >= 512 ? (TM == 128 ? 5 : 8) : 8;
@@ -56,7 +59,7 @@ struct PairCfg {
     static constexpr int PARTS = TM == 128 ? 2 : 4;  // partial output dots per row (epilogue threads)
     static constexpr int RQ = TM / 32;               // 32-row groups per CTA (output warp)
     static constexpr uint32_t OFF_AX = A_BYTES;
-    static constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AX_BYTES;
+    static constexpr uint32_t OFF_STAGE = OFF_AX + 2 * AXP;
     static constexpr uint32_t OFF_WO = OFF_STAGE + STAGES * CHUNK;
     static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
     static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * PARTS * TM * 4;
@@ -91,6 +94,33 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
     __align__(16) __nv_bfloat16 v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
+}
+
+// Rows of mixed motions: the row's q-part as three more K=16 A slabs, z_k = (q_k - shift) * scale
+// (motion_ext_kernel's arithmetic) in (hi, hi, lo) triples against the model's (hi, lo, hi) W_q
+// triples — the same three-product bf16 split as the x-part.
+__device__ __forceinline__ void write_axq(uint8_t* axq, uint32_t slab_bytes, uint32_t row, const float* q,
+                                          const FusedArgs& a) {
+    __align__(16) __nv_bfloat16 v[48];
+    const __nv_bfloat16 zero = __float2bfloat16_rn(0.0f);
+#pragma unroll
+    for (int i = 0; i < 48; ++i) v[i] = zero;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        if (k < 2 * a.dof) {
+            __nv_bfloat16 h, l;
+            split_bf16(__fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]), h, l);
+            v[3 * k] = h;
+            v[3 * k + 1] = h;
+            v[3 * k + 2] = l;
+        }
+    }
+#pragma unroll
+    for (int sl = 0; sl < 3; ++sl)
+#pragma unroll
+        for (int h8 = 0; h8 < 2; ++h8)
+            *reinterpret_cast<uint4*>(axq + sl * slab_bytes + ext_offset(row, 8 * h8)) =
+                *reinterpret_cast<const uint4*>(&v[16 * sl + 8 * h8]);
 }
 
 // Epilogue of 32 columns of one row (the MMA already added bias and x-part).
@@ -317,6 +347,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
         prefetch_tmap(&a.tmap_w);
         prefetch_tmap(&a.tmap_xm);
         prefetch_tmap(&a.tmap_xq);
+        if (C::TM == 64 && a.mixed) prefetch_tmap(&a.tmap_xmix);
     }
     if (warp == 1) tmem_alloc_pair(tmem_slot, N);
     tc_fence_before();
@@ -362,15 +393,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                     for (int step = 0; step < steps; ++step) {
                         const int nh = step & 1, kh = step >> 1;
                         if (kh == 0 && ld.ext) {
-                            slot(C::XCHUNK);
                             const uint32_t fb = full0 + stage * 8u;
                             uint8_t* dst = stages + stage * C::CHUNK;
-                            if (ld.ext == 2) {
+                            if (C::TM == 64 && a.mixed && ld.ext == 2) {
+                                // rows of mixed motions: the model's [b + x-part | q-part] slabs
+                                slot(C::CHUNK);
+                                tma_load_2d_pair(dst, &a.tmap_xmix, 0,
+                                                 static_cast<int32_t>(((ld.mb_slot * 2 + nh) * 2 + rank) * 128), fb, pol);
+                            } else if (ld.ext == 2) {
+                                slot(C::XCHUNK);
                                 const int64_t blob =
                                     a.ext_ring ? ((static_cast<int64_t>(blockIdx.x) * C::XR + xb) * a.n_mb + ld.mb_slot) * 2 + nh
                                                : ((static_cast<int64_t>(motion) * a.n_mb + ld.mb_slot) * 2 + nh) * 2 + rank;
                                 tma_load_2d_pair(dst, &a.tmap_xq, 0, static_cast<int32_t>(blob * C::BR), fb, pol);
                             } else {
+                                slot(C::XCHUNK);
                                 const int64_t r0 = ld.ext_row + (nh * 2 + rank) * C::BR;
                                 tma_load_2d_pair(dst, &a.tmap_xm, 0, static_cast<int32_t>(r0), fb, pol);
                             }
@@ -430,8 +467,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                                 pw_f += prof_clock() - c0;
                             }
                             tc_fence_after();
-                            mma_bf16_pair(d_addr, noswz_desc(ax_base + b * C::AX_BYTES, 128, 256),
-                                          noswz_desc(s_base + stage * C::CHUNK, 128, 256), idesc, 0u);
+                            const uint32_t axb = ax_base + b * C::AXP, xs = s_base + stage * C::CHUNK;
+                            mma_bf16_pair(d_addr, noswz_desc(axb, 128, 256), noswz_desc(xs, 128, 256), idesc, 0u);
+                            if (C::TM == 64 && a.mixed && ld.ext == 2) {  // + the rows' q-part
+#pragma unroll
+                                for (int i = 1; i < 4; ++i)
+                                    mma_bf16_pair(d_addr, noswz_desc(axb + i * C::AX_BYTES, 128, 256),
+                                                  noswz_desc(xs + i * C::XCHUNK, 128, 256), idesc, 1u);
+                            }
                             mma_commit_pair(&empty[stage], 3);
                             if (++stage == C::STAGES) stage = 0, phase ^= 1u;
                             acc = true;
@@ -550,6 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
         const uint32_t ax_full0 = mapa_shared(smem_u32(ax_full), 0);
         uint32_t of_ph[2] = {0u, 0u};
         float px[C::RQ][3];
+        float pq[C::TM == 64 ? C::RQ : 1][16];  // rows of mixed motions: each row's q0|q1
         unsigned long long pe_x = 0;
         auto load_points = [&](int64_t t) {
             int32_t motion, nrows;
@@ -562,14 +606,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                 px[q][0] = xp[0];
                 px[q][1] = xp[1];
                 px[q][2] = xp[2];
+                if constexpr (C::TM == 64) {
+                    if (a.mixed) {
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) pq[q][k] = k < 2 * a.dof ? xp[3 + k] : 0.f;
+                    }
+                }
             }
         };
         auto store_ax = [&](int b) {
 #pragma unroll
-            for (int q = 0; q < C::RQ; ++q)
-                write_ax(AX + b * C::AX_BYTES, static_cast<uint32_t>(q * 32) + lane,
+            for (int q = 0; q < C::RQ; ++q) {
+                write_ax(AX + b * C::AXP, static_cast<uint32_t>(q * 32) + lane,
                          (px[q][0] - a.shift[0]) * a.scale[0], (px[q][1] - a.shift[1]) * a.scale[1],
                          (px[q][2] - a.shift[2]) * a.scale[2]);
+                if constexpr (C::TM == 64) {
+                    if (a.mixed)
+                        write_axq(AX + b * C::AXP + C::AX_BYTES, C::AX_BYTES, static_cast<uint32_t>(q * 32) + lane, pq[q], a);
+                }
+            }
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(ax_full0 + b * 8u);

@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(Fp32Cfg<N, CG, TMO>::THREADS, 1) fused_fp32_ke
             for (int k = 0; k < 3; ++k)
                 *act_at(N + k, tid) = __fmul_rn(__fsub_rn(xp[k], a.shift[k]), a.scale[k]);
             if (a.exact) {
-                const float* q = a.q01 + static_cast<int64_t>(motion) * 2 * a.dof;
+                const float* q = a.row_q ? xp + 3 : a.q01 + static_cast<int64_t>(motion) * 2 * a.dof;
                 for (int k = 0; k < 2 * a.dof; ++k)
                     *act_at(N + 3 + k, tid) = __fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]);
             }

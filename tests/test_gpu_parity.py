@@ -114,6 +114,36 @@ def test_forward_eval_mixed_motions_matches_oracle():
     assert np.abs(out16 - ref).max() <= BF16_BOUND[w.program.name]
 
 
+@pytest.mark.parametrize("key,prog_name", [("c3", None), ("c4", None), ("c3", "fig2_5x512")])
+@pytest.mark.parametrize("B", [1, 1000, 3001])
+def test_forward_eval_rows_of_distinct_motions(key, prog_name, B):
+    """forward_eval batches whose rows all differ in motion (eval_mae, bench.cpp:80-90; training
+    validation, nn.cpp:370).  The FP32 path runs them as full tiles (each row reads its own q) and
+    stays bit-identical; bf16 at width 512 runs 128-row tiles with the q-part per row on the
+    tensor core (FusedArgs::mixed) within the network's bound, and agrees with the folded path
+    on the same rows grouped by motion."""
+    w = WORKLOADS[key]
+    prog = S.fig2(5, 512, 6) if prog_name else w.program
+    params = S.init_params(prog, 6, "ref" if prog_name else w.bound)
+    pts, q = w.make(seed=6, motions=64, points=4096)
+    rng = np.random.default_rng(B)
+    qi = rng.integers(0, 64, B)
+    raw = np.concatenate([pts[rng.integers(0, pts.shape[0], B)],
+                          q[qi] + rng.uniform(-0.05, 0.05, (B, q.shape[1])).astype(np.float32)], axis=1).astype(np.float32)
+    model = S.Model(prog, params)
+    ref = O.forward_eval(prog, params, raw)
+    assert np.array_equal(model.forward_eval(raw, precision="fp32_exact"), ref)
+    out = model.forward_eval(raw, precision="bf16")
+    bound = BF16_BOUND[prog.name]
+    assert np.abs(out.astype(np.float64) - ref).max() <= bound
+    if B > 1:  # the same rows sorted by motion with a shared q per group: the folded segment path
+        g = np.argsort(qi, kind="stable")
+        grouped = raw[g].copy()
+        grouped[:, 3:] = q[qi[g]]
+        ref_g = O.forward_eval(prog, params, grouped)
+        assert np.abs(model.forward_eval(grouped, precision="bf16").astype(np.float64) - ref_g).max() <= bound
+
+
 def test_predict_min_distance_reference_signature():
     w = WORKLOADS["c1"]
     params = S.init_params(w.program, 4, "he")
@@ -243,17 +273,19 @@ def test_fp32_split_within_stated_bound(key, M, P, seed):
 def test_fp32_split_width_512_forward_eval_mixed_motions():
     """forward_eval rows of mixed motions (the a-8 path, tile table of 128-row tiles) on the
     width-512 split kernel: within the bound, and batch-invariant (rows evaluated alone give
-    the same bits)."""
+    the same bits); a batch of mostly distinct motions runs on the FP32 path (exact)."""
     w = WORKLOADS["c3"]
     params = S.init_params(w.program, 4, w.bound)
     pts, q = w.make(seed=4, motions=5, points=300)
-    idx = np.arange(300)
-    rows = np.concatenate([pts, q[idx % 5]], axis=1).astype(np.float32)
+    idx = np.sort(np.arange(300) % 5)  # five runs of 60 rows: the folded tile-table path
+    rows = np.concatenate([pts, q[idx]], axis=1).astype(np.float32)
     m = S.Model(w.program, params)
     out = m.forward_eval(rows, precision="fp32_split")
     ref = O.forward_eval(w.program, params, rows)
     assert np.abs(out.astype(np.float64) - ref).max() <= FP32_SPLIT_BOUND[w.program.name]
-    assert np.array_equal(m.forward_eval(rows[7:8], precision="fp32_split"), out[7:8])
+    assert np.array_equal(m.forward_eval(rows[60:120], precision="fp32_split"), out[60:120])  # one run alone
+    mixed = np.concatenate([pts, q[np.arange(300) % 5]], axis=1).astype(np.float32)
+    assert np.array_equal(m.forward_eval(mixed, precision="fp32_split"), O.forward_eval(w.program, params, mixed))
 
 
 @pytest.mark.parametrize("width,blocks", [(256, 3), (512, 5)])
