@@ -1,7 +1,7 @@
 """Build an A/B variant of the native library: python scripts/build_variant.py OUT.so [file.cu=/path/alt.cu ...]
 
 Copies csrc/ to a scratch directory, swaps in the given alternative sources, and builds
-with the package's own flags (the result is used via SVN_LIB=... in scripts/gpu_ab.sh)."""
+with the package's own flags (the result is used via SVN_LIB=scripts/ab/... with `scripts/gpu.sh ab`)."""
 import shutil
 import sys
 import tempfile
