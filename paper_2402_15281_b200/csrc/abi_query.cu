@@ -63,6 +63,40 @@ int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
 
 thread_local Arena* g_arena = nullptr;
 
+// SVN_HOST_TRACE=1: host-side time of the phases of a small host-buffer query, averaged and
+// printed to stderr every 300 calls (where a per-motion call's fixed cost goes).
+struct HostTrace {
+    static bool on() {
+        static const bool v = [] {
+            const char* e = std::getenv("SVN_HOST_TRACE");
+            return e && e[0] == '1';
+        }();
+        return v;
+    }
+    double acc[9] = {};
+    int n = 0;
+    std::chrono::steady_clock::time_point t;
+    void start() { t = std::chrono::steady_clock::now(); }
+    void lap(int i) {
+        const auto now = std::chrono::steady_clock::now();
+        acc[i] += std::chrono::duration<double, std::micro>(now - t).count();
+        t = now;
+    }
+    void done() {
+        if (++n < 300) return;
+        std::fprintf(stderr, "[svn host] us/call: fill %.1f | stage %.1f | scratch %.1f | K0 %.1f | K1 %.1f | D2H %.1f | sync %.1f | out %.1f | pin %.1f\n",
+                     acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n, acc[8] / n);
+        n = 0;
+        for (double& x : acc) x = 0;
+    }
+};
+thread_local HostTrace g_trace;
+thread_local bool g_trace_on = false;
+#define SVN_TRACE(i) \
+    do {             \
+        if (g_trace_on) g_trace.lap(i); \
+    } while (0)
+
 Arena& thread_arena(int device) {
     thread_local Arena ar[8];
     thread_local Arena other;
@@ -271,6 +305,7 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.min_out = min_out;
     a.argmin_out = argmin_out;
     a.free_out = free_out;
+    SVN_TRACE(2);
     if (kind != Kind::SIMT) {
         s = motion_ext(m, a, M, keys_partial ? nullptr : keys, counters, keys_partial ? 0 : M, sc, st,
                        kind == Kind::SPLIT);
@@ -283,7 +318,9 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
                  "motion_bias kernel");
         ++g_launches;
     }
+    SVN_TRACE(3);
     SVN_CUDA(launch_k1(a, kind, m->num_sms, st), "fused MLP kernel");
+    SVN_TRACE(4);
     return SVN_OK;
 }
 
@@ -502,6 +539,11 @@ bool small_staging_enabled() {  // SVN_SMALL_STAGING=0: DMA copies for every cal
 // fill(pts, q) writes the call's float inputs into the pinned staging block; points/q01 are
 // the caller's float arrays (null for predict_min_distance, whose double inputs are converted
 // by fill), sent to the device directly when they are already pinned.
+// nn.cpp:469-471's double -> float cast of the cloud, vectorisable (no aliasing)
+static void cvt_f64_f32(float* __restrict__ d, const double* __restrict__ src, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) d[i] = static_cast<float>(src[i]);
+}
+
 template <class Fill>
 svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int64_t M, double margin,
                           const float* points, const float* q01, Fill fill, float* min_out, int32_t* argmin_out,
@@ -527,8 +569,12 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         cudaPointerAttributes at{};
         return p && cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
     };
+    g_trace_on = HostTrace::on();
+    if (g_trace_on) g_trace.start();
     const bool direct = pinned(points) && pinned(q01);
+    SVN_TRACE(8);
     if (!direct) fill(reinterpret_cast<float*>(sg.host), reinterpret_cast<float*>(sg.host + o_q));
+    SVN_TRACE(0);
     Arena& arena = thread_arena(m->device);
     {
         ArenaScope as(&arena);
@@ -550,6 +596,7 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         } else {
             SVN_CUDA(cudaMemcpyAsync(sg.dev, sg.host, o_min, cudaMemcpyHostToDevice, st), "H2D points + motions");
         }
+        SVN_TRACE(1);
         uint8_t* const out = small ? sg.host : sg.dev;
         const svn_status s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
                                          reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
@@ -561,12 +608,19 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
                      "D2H min/argmin/free");
         if (per_point)
             SVN_CUDA(cudaMemcpyAsync(per_point, dpp, sizeof(float) * P * M, cudaMemcpyDeviceToHost, st), "D2H delta");
+        SVN_TRACE(5);
     }
     SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+    SVN_TRACE(6);
     SVN_CUDA(arena.grow_to_need(), "scratch arena");
     std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
     std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
     std::memcpy(free_out, sg.host + o_free, M);
+    if (g_trace_on) {
+        g_trace.lap(7);
+        g_trace.done();
+        g_trace_on = false;
+    }
     return SVN_OK;
 }
 
@@ -702,7 +756,7 @@ SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision pr
         uint8_t fr = 0;
         svn_status s = query_min_host(m, prec, P, 1, 0.0, nullptr, nullptr,
                                       [&](float* hp, float* hq) {
-                                          for (int64_t i = 0; i < 3 * P; ++i) hp[i] = static_cast<float>(cloud[i]);
+                                          cvt_f64_f32(hp, cloud, 3 * P);
                                           for (int i = 0; i < dof; ++i) hq[i] = static_cast<float>(q0[i]);
                                           for (int i = 0; i < dof; ++i) hq[dof + i] = static_cast<float>(q1[i]);
                                       },
