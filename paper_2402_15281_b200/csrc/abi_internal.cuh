@@ -74,6 +74,7 @@ void split_bf16_host(float x, __nv_bfloat16& hi, __nv_bfloat16& lo);
 
 struct svn_model {
     int device = 0;
+    uint64_t serial = 0;  // unique per created model: keys the per-thread graph cache (abi_query.cu)
     int L = 0, N = 0, dof = 0, in = 0;
     int num_sms = 148;
     int n_mb = 0;

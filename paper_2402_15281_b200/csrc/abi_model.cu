@@ -267,6 +267,8 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
         DeviceGuard guard(device);
 
         auto m = new svn_model();
+        static std::atomic<uint64_t> next_serial{1};
+        m->serial = next_serial.fetch_add(1);
         m->device = device;
         m->L = d->n_layers;
         m->N = d->width;

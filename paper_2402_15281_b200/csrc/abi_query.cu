@@ -539,6 +539,98 @@ bool small_staging_enabled() {  // SVN_SMALL_STAGING=0: DMA copies for every cal
 // fill(pts, q) writes the call's float inputs into the pinned staging block; points/q01 are
 // the caller's float arrays (null for predict_min_distance, whose double inputs are converted
 // by fill), sent to the device directly when they are already pinned.
+// Small staged calls as one CUDA graph (SVN_GRAPH=0 turns it off): the stage-in kernel, K0
+// and the fused kernel (behind its programmatic edge), with scratch from the thread's arena and
+// inputs / outputs in the pinned staging block, are captured once per (thread, model,
+// precision, P, M, margin, staging block, arena block) and replayed with one graph launch
+// instead of three kernel launches.
+struct GraphEntry {
+    const svn_model* m;
+    uint64_t serial;
+    int prec;
+    int64_t P, M;
+    double margin;
+    const uint8_t *host, *dev, *arena;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    uint64_t used;
+};
+
+struct GraphCache {
+    std::vector<GraphEntry> e;
+    uint64_t tick = 0;
+    ~GraphCache() {
+        for (GraphEntry& x : e)
+            if (x.exec) cudaGraphExecDestroy(x.exec);
+    }
+};
+
+bool graphs_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVN_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// true: the call ran (launched) as a graph; false: use the stream path (a failed capture only
+// loses the fast path — the stream path reports any real error)
+bool small_graph(const svn_model* m, svn_precision prec, int64_t P, int64_t M, double margin, Staging& sg,
+                 Arena& arena, size_t o_q, size_t o_min, size_t o_arg, size_t o_free, cudaStream_t st) {
+    thread_local GraphCache gc;
+    GraphEntry* hit = nullptr;
+    for (GraphEntry& x : gc.e)
+        if (x.m == m && x.serial == m->serial && x.prec == static_cast<int>(prec) && x.P == P && x.M == M &&
+            x.margin == margin && x.host == sg.host && x.dev == sg.dev && x.arena == arena.base) {
+            hit = &x;
+            break;
+        }
+    if (!hit) {
+        if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        const int64_t l0 = g_launches;
+        bool ok = launch_stage_in(sg.host, sg.dev, o_min, st) == cudaSuccess;
+        bool fallback_alloc = false;
+        if (ok) {
+            ArenaScope as(&arena);
+            Scratch sc(st);
+            ok = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev), P, 0,
+                             reinterpret_cast<const float*>(sg.dev + o_q), M, margin,
+                             reinterpret_cast<float*>(sg.host + o_min), reinterpret_cast<int32_t*>(sg.host + o_arg),
+                             sg.host + o_free, nullptr, nullptr, st) == SVN_OK;
+            fallback_alloc = !sc.ptrs.empty();
+        }
+        cudaGraph_t g = nullptr;
+        const cudaError_t ee = cudaStreamEndCapture(st, &g);
+        const int64_t launches = g_launches - l0 + 1;
+        g_launches = l0;
+        cudaGraphExec_t ex = nullptr;
+        if (!ok || fallback_alloc || ee != cudaSuccess || !g || cudaGraphInstantiate(&ex, g, 0) != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            return false;
+        }
+        cudaGraphDestroy(g);
+        if (gc.e.size() >= 8) {
+            auto lru = std::min_element(gc.e.begin(), gc.e.end(),
+                                        [](const GraphEntry& x, const GraphEntry& y) { return x.used < y.used; });
+            cudaGraphExecDestroy(lru->exec);
+            gc.e.erase(lru);
+        }
+        gc.e.push_back({m, m->serial, static_cast<int>(prec), P, M, margin, sg.host, sg.dev, arena.base, ex, launches, 0});
+        hit = &gc.e.back();
+    }
+    hit->used = ++gc.tick;
+    if (cudaGraphLaunch(hit->exec, st) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    g_launches += hit->launches;
+    return true;
+}
+
 // nn.cpp:469-471's double -> float cast of the cloud, vectorisable (no aliasing)
 static void cvt_f64_f32(float* __restrict__ d, const double* __restrict__ src, int64_t n) {
     for (int64_t i = 0; i < n; ++i) d[i] = static_cast<float>(src[i]);
@@ -576,7 +668,11 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
     if (!direct) fill(reinterpret_cast<float*>(sg.host), reinterpret_cast<float*>(sg.host + o_q));
     SVN_TRACE(0);
     Arena& arena = thread_arena(m->device);
-    {
+    const bool small = !direct && !per_point && P <= kSmallStagingPoints && M <= 64 && small_staging_enabled();
+    if (small && arena.cap > 0 && graphs_enabled() && !g_timing && !prof_enabled() &&
+        small_graph(m, prec, P, M, margin, sg, arena, o_q, o_min, o_arg, o_free, st)) {
+        SVN_TRACE(4);
+    } else {
         ArenaScope as(&arena);
         Scratch sc(st);
         float* dpp = nullptr;
@@ -585,7 +681,6 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         // small staged calls (the reference's per-motion predict_min_distance): a kernel pulls the
         // inputs out of the pinned block and the fused finaliser writes (min, argmin, free)
         // straight into it — no DMA copy on the critical path (each costs ~5-10 us of setup)
-        const bool small = !direct && !per_point && P <= kSmallStagingPoints && M <= 64 && small_staging_enabled();
         if (direct) {
             SVN_CUDA(cudaMemcpyAsync(sg.dev, points, sizeof(float) * 3 * P, cudaMemcpyHostToDevice, st), "H2D points");
             SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),

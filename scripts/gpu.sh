@@ -69,7 +69,7 @@ case "$task" in
   latency)
     g++ -std=c++17 -O2 -Iinclude scripts/latency_cpp.cpp -Lpaper_2402_15281_b200/_lib -lsweptnet_b200 \
       -Wl,-rpath,$PWD/paper_2402_15281_b200/_lib -o gpurun_out/latency_cpp && \
-    timeout 300 gpurun_out/latency_cpp 2>&1 | tee gpurun_out/latency.log ;;
+    for v in ${LAT_GRAPH:-1}; do echo "SVN_GRAPH=$v"; SVN_GRAPH=$v timeout 300 gpurun_out/latency_cpp; done 2>&1 | tee gpurun_out/latency.log ;;
   rzsweep)
     for c in ${@:-0 0.25}; do SVN_SPLIT_RZ=$c timeout 900 python scripts/split_rz_sweep.py; done 2>&1 | tee gpurun_out/rzsweep.log ;;
   *) echo "unknown task $task"; exit 2 ;;
