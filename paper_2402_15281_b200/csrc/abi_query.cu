@@ -40,14 +40,14 @@ int tile_rows(Kind k, int N) {
 }
 // SIMT: a query with fewer big tiles than SMs is cut into 32-row tiles (4 warps per CTA,
 // more SMs busy; each output's k-ordered FMA chain is unchanged)
-// bf16 at width 512: a launch with fewer 256-row tiles than CTA pairs (one motion x a few
+// bf16 (width 512 and 256): a launch with fewer 256-row tiles than CTA pairs (one motion x a few
 // thousand points — the reference's per-motion predict_min_distance) is latency-bound, so it
 // runs 128-row pair tiles (64 rows per CTA, M=128 MMAs): twice the tiles, each through the
 // network in about half the time.  SVN_PAIR_TILE=128|256 forces one (A/B hook).
 int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
     const int t = tile_rows(k, N);
     if (k == Kind::SIMT && big_tiles < num_sms) return kFp32SmallTile;
-    if (k == Kind::BF16 && N == 512) {
+    if (k == Kind::BF16 && (N == 512 || N == 256)) {
         static const int forced = [] {
             const char* e = std::getenv("SVN_PAIR_TILE");
             return e ? std::atoi(e) : 0;

@@ -21,12 +21,8 @@ namespace svn {
 namespace pp {
 
 constexpr int N = 256;
-constexpr int TM = 128;                    // rows per CTA (tile = 256 rows per pair)
 constexpr int BR = N / 2;                  // B rows per CTA (M=256 x N=256 MMA: CTA r holds rows r*128..)
 constexpr int KSL = N / 64;                // K slabs per layer
-constexpr uint32_t A_SLAB = TM * 128;      // 16 KiB
-constexpr uint32_t A_BYTES = TM * N * 2;   // 64 KiB
-constexpr uint32_t AX_BYTES = TM * 32;     // 4 KiB
 constexpr uint32_t SLAB_B = BR * 128;      // 16 KiB
 constexpr uint32_t XCHUNK = BR * 32;       // 4 KiB
 constexpr int WSTAGES = 4;
@@ -42,15 +38,28 @@ constexpr int EPI_WARPS = 8;
 constexpr int OUT_WARP = 2 + EPI_WARPS;    // first output warp: keys / per-point outputs / next tile's A extension
 constexpr int OUT_WARPS = 2;              // one per slot
 constexpr int THREADS = 64 + EPI_WARPS * 32 + OUT_WARPS * 32;
-constexpr int COLS = N / 2;                // columns per epilogue thread
-constexpr uint32_t OFF_AX = 2 * A_BYTES;
-constexpr uint32_t OFF_W = OFF_AX + 2 * AX_BYTES;
-constexpr uint32_t OFF_X = OFF_W + WSTAGES * SLAB_B;
-constexpr uint32_t OFF_WO = OFF_X + XSTAGES * XCHUNK;
-constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
-constexpr uint32_t OFF_BAR = OFF_DOT + 2 * 2 * TM * 4;
-constexpr uint32_t SMEM = OFF_BAR + 256;
-static_assert(SMEM <= 232448, "shared memory budget");
+// Rows per CTA: 128 (M=256 MMAs, the throughput form) or 64 for launches with fewer 256-row
+// tiles than CTA pairs (M=128 MMAs: each CTA's 64 x 256 accumulator in TMEM's "2x2" layout —
+// lanes 0-63 hold columns 0-127, lanes 64-127 columns 128-255 — so twice the tiles, each
+// through the network in ~0.6x the time).  The B side (weights, extension rows) is the same.
+template <int TM_>
+struct Cfg {
+    static constexpr int TM = TM_;
+    static constexpr uint32_t A_SLAB = TM * 128;
+    static constexpr uint32_t A_BYTES = TM * N * 2;
+    static constexpr uint32_t AX_BYTES = TM * 32;
+    static constexpr int COLS = TM == 128 ? N / 2 : N / 4;  // columns per epilogue thread
+    static constexpr int PARTS = TM == 128 ? 2 : 4;         // partial output dots per row
+    static constexpr int RQ = TM / 32;                      // 32-row groups per CTA (output warps)
+    static constexpr uint32_t OFF_AX = 2 * A_BYTES;
+    static constexpr uint32_t OFF_W = OFF_AX + 2 * AX_BYTES;
+    static constexpr uint32_t OFF_X = OFF_W + WSTAGES * SLAB_B;
+    static constexpr uint32_t OFF_WO = OFF_X + XSTAGES * XCHUNK;
+    static constexpr uint32_t OFF_DOT = OFF_WO + N * 4;
+    static constexpr uint32_t OFF_BAR = OFF_DOT + 2 * PARTS * TM * 4;
+    static constexpr uint32_t SMEM = OFF_BAR + 256;
+    static_assert(SMEM <= 232448, "shared memory budget");
+};
 
 __device__ __forceinline__ uint32_t pack2(float lo, float hi) {
     const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
@@ -77,6 +86,7 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 
 // 32 columns of one row: activation (+ Fig. 2 affine/residual) then bf16 store or output dot
 // (accumulated in four partial sums so the 128-column dot is not one dependent FMA chain).
+template <int TM>
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
                                       uint8_t* A, const float* wo_s, float4& dot) {
     const int fl = ld.flags;
@@ -201,9 +211,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+template <int TMR>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     fused_bf16_pp_kernel(const __grid_constant__ FusedArgs a) {
     using namespace pp;
+    using C = Cfg<TMR>;
+    constexpr int TM = C::TM, COLS = C::COLS, PARTS = C::PARTS, RQ = C::RQ;
+    constexpr uint32_t A_SLAB = C::A_SLAB, A_BYTES = C::A_BYTES, AX_BYTES = C::AX_BYTES;
+    constexpr uint32_t OFF_AX = C::OFF_AX, OFF_W = C::OFF_W, OFF_X = C::OFF_X, OFF_WO = C::OFF_WO,
+                       OFF_DOT = C::OFF_DOT, OFF_BAR = C::OFF_BAR;
 #ifdef SVN_CTA_TIMES
     if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_times[4 * blockIdx.x] = gtimer();
 #endif
@@ -398,7 +414,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
         const int e = warp - 2;
         const uint32_t quad = static_cast<uint32_t>(warp & 3);
         const int ch = e >> 2;
-        const uint32_t row = quad * 32 + lane;
+        // TM=128: lane quadrant = 32 rows, all columns; TM=64 ("2x2"): quadrants 0/1 = rows
+        // 0-31/32-63 of columns 0-127, 2/3 = the same rows of columns 128-255
+        const uint32_t row = (TM == 128 ? quad : (quad & 1u)) * 32 + lane;
+        const int cq = TM == 128 ? 0 : static_cast<int>(quad >> 1) * 128;
+        const int part = (TM == 128 ? 0 : static_cast<int>(quad >> 1) * 2) + ch;
         const uint32_t t_lane = (quad * 32u) << 16;
         const uint32_t a_ready0 = mapa_shared(smem_u32(a_ready), 0);
         uint32_t dp[2] = {0u, 0u}, oe_ph[2] = {0u, 0u};
@@ -436,7 +456,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
                             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
                             if (q + 1 < NCH) tmem_ld32_async(tbase + static_cast<uint32_t>(c0c + 32 * (q + 1)), nxt);
-                            epi32(ld, l, last, reinterpret_cast<float*>(cur), c0c + 32 * q, row, A, wo_s, dot[s]);
+                            epi32<TM>(ld, l, last, reinterpret_cast<float*>(cur), cq + c0c + 32 * q, row, A, wo_s, dot[s]);
                             if (q + 1 < NCH) tmem_wait_tied(nxt);
                         }
                     }
@@ -456,7 +476,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             mbar_wait(&out_empty[s], oe_ph[s]);
                             oe_ph[s] ^= 1u;
                         }
-                        dotbuf[(s * 2 + ch) * TM + row] = (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
+                        dotbuf[(s * PARTS + part) * TM + row] = (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
                         dot[s] = make_float4(0.f, 0.f, 0.f, 0.f);
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&out_full[s]);
@@ -482,13 +502,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
         const int s = warp - OUT_WARP;
         const uint32_t ax_ready0 = mapa_shared(smem_u32(ax_ready), 0);
         uint32_t of_ph = 0u;
-        float px[4][3];
+        float px[RQ][3];
         auto load_points = [&](int64_t t) {
             int32_t motion, nrows;
             int64_t pbase, obase;
             tile_decode(a, t, 2 * TM, motion, pbase, obase, nrows);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < RQ; ++k) {
                 const int32_t r = static_cast<int32_t>(rank * TM + k * 32 + lane);
                 const float* xp = a.points + (pbase + (r < nrows ? r : 0)) * a.point_stride;
                 px[k][0] = xp[0];
@@ -498,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
         };
         auto store_ax = [&]() {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+            for (int k = 0; k < RQ; ++k)
                 write_ax(AX + s * AX_BYTES, static_cast<uint32_t>(k * 32) + lane, (px[k][0] - a.shift[0]) * a.scale[0],
                          (px[k][1] - a.shift[1]) * a.scale[1], (px[k][2] - a.shift[2]) * a.scale[2]);
             fence_proxy_async_smem();
@@ -523,17 +543,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                 store_ax();
                 if (has(j + 2, s)) load_points(tile_of(j + 2, s));
             }
-            float delta[4];
+            float delta[RQ];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < RQ; ++k) {
                 const int r = k * 32 + static_cast<int>(lane);
-                delta[k] = (dotbuf[(s * 2) * TM + r] + dotbuf[(s * 2 + 1) * TM + r]) + a.bo;
+                const float* d = dotbuf + (s * PARTS) * TM + r;
+                delta[k] = (PARTS == 2 ? d[0] + d[TM] : (d[0] + d[TM]) + (d[2 * TM] + d[3 * TM])) + a.bo;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_empty[s]);
             unsigned long long key = ~0ull;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < RQ; ++k) {
                 const int32_t rr = static_cast<int32_t>(rank * TM + k * 32 + lane);
                 if (rr < nrows) {
                     if (a.per_point) a.per_point[obase + rr] = delta[k];
@@ -582,9 +603,11 @@ extern "C" __attribute__((visibility("default"))) int svn_debug_cta_times(unsign
 }
 #endif
 
-cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t st) {
+template <int TM>
+static cudaError_t launch_pp_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
     static SmemOptIn opt;
-    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pp_kernel), (int)pp::SMEM);
+    constexpr uint32_t smem = pp::Cfg<TM>::SMEM;
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pp_kernel<TM>), (int)smem);
     if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     // two tiles in flight per pair, unless there are too few tiles to fill the SMs that way:
@@ -592,9 +615,14 @@ cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t s
     const int64_t need = a.n_tiles <= pairs ? a.n_tiles : (a.n_tiles + 1) / 2;
     if (need < pairs) pairs = need;
     if (pairs < 1) return cudaSuccess;
-    const cudaError_t le = launch_fused_pdl(fused_bf16_pp_kernel, static_cast<unsigned>(2 * pairs), pp::THREADS,
-                                            pp::SMEM, st, a);
+    const cudaError_t le = launch_fused_pdl(fused_bf16_pp_kernel<TM>, static_cast<unsigned>(2 * pairs), pp::THREADS,
+                                            smem, st, a);
     return le != cudaSuccess ? le : cudaGetLastError();
+}
+
+cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t st) {
+    // 128-row pair tiles for launches with fewer 256-row tiles than pairs (abi tile_rows_for)
+    return a.tile_rows == 128 ? launch_pp_n<64>(a, num_sms, st) : launch_pp_n<128>(a, num_sms, st);
 }
 
 }  // namespace svn
