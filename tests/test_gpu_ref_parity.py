@@ -123,6 +123,12 @@ def test_baseline_nets_with_normaliser_and_biases(key, M, P):
         assert np.array_equal(r.free[~amb], ofree[~amb])
         d_at = opp[np.arange(M), r.argmin]
         assert np.all((r.argmin == oarg) | (d_at - omin <= bound))
-    # rows of mixed motions through forward_eval (the a-8 path) with the same model
+    # rows of mixed motions through forward_eval (the a-8 path) with the same model: every row a
+    # different motion than its neighbour, so the FP32 path reads q per row and bf16 at width 512
+    # runs the mixed-motion kernel (the normaliser and the layers' biases on that path too)
     rows = np.concatenate([pts[:200], q[np.arange(200) % M]], axis=1).astype(np.float32)
-    assert np.array_equal(bits(model.forward_eval(rows, precision="fp32_exact")), bits(O.forward_eval(w.program, p, rows)))
+    ref_rows = O.forward_eval(w.program, p, rows)
+    assert np.array_equal(bits(model.forward_eval(rows, precision="fp32_exact")), bits(ref_rows))
+    for prec, bound in precs:
+        err = np.abs(model.forward_eval(rows, precision=prec).astype(np.float64) - ref_rows).max()
+        assert err <= bound, (prec, err)
