@@ -78,10 +78,10 @@ __host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
 }
 
 // |x| >= 65520 rounds to an fp16 infinity: such an activation cannot be held in the
-// (hi, lo') planes.  The row is then reported as delta = -inf (OVERFLOW_DELTA): its
-// motion's min is -inf and its class "not free", i.e. it is handed to the exact checker
-// (the safe side of collision.cpp:68) instead of silently dropping out of the min as a NaN.
-constexpr float kF16Overflow = 65520.f;
+// (hi, lo') planes.  The row is then reported as delta = -inf: its motion's min is -inf and
+// its class "not free", i.e. it is handed to the exact checker (the safe side of
+// collision.cpp:68) instead of silently dropping out of the min as a NaN.  The epilogue keeps
+// the running max of |hi| per row (packed half2) and checks it once per tile.
 
 __device__ __forceinline__ void split(float x, __half& hi, __half& lo) {
     hi = __float2half_rn(x);
@@ -130,7 +130,8 @@ __device__ __forceinline__ void combine32(const uint32_t* m, const uint32_t* c, 
 // residual -> next layer's (hi, lo') planes, or the output dot on the last layer.
 template <int TM>
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot, bool& ovf) {
+                                      uint8_t* Ahi, uint8_t* Alo, const float* wo_s, float4& dot, bool& ovf,
+                                      __half2& hmax) {
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
 #ifndef SVN_SPLIT_NO_NANCHECK  // A/B build without the non-finite input check
@@ -141,10 +142,16 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         // the layer's K=16 extension carries z_x (and b_m) as fp16 splits: an input beyond the
         // fp16 range arrives as inf / NaN, which the ReLU below would turn into 0.  v * 0 is
         // NaN exactly for a non-finite v.
-        float nf = 0.f;
+        unsigned long long nf = 0ull, z2 = 0ull;  // (0, 0) pairs; v * 0 + nf on packed fp32 pairs
 #pragma unroll
-        for (int i = 0; i < 32; ++i) nf = fmaf(v[i], 0.f, nf);
-        ovf |= nf != nf;
+        for (int i = 0; i < 32; i += 2) {
+            unsigned long long vv;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(vv) : "f"(v[i]), "f"(v[i + 1]));
+            asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(nf) : "l"(vv), "l"(z2));
+        }
+        float n0, n1;
+        asm("mov.b64 {%0, %1}, %2;" : "=f"(n0), "=f"(n1) : "l"(nf));
+        ovf |= (n0 != n0) || (n1 != n1);
     }
     if (act) {
 #pragma unroll
@@ -188,17 +195,28 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         }
         return;
     }
+    unsigned long long s2;  // (2^11, 2^11) for the packed fp32 pair ops
+    asm("mov.b64 %0, {%1, %1};" : "=l"(s2) : "f"(LO_SCALE));
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
         uint32_t hw[4], lw[4];
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
-            // paired split: hi = f16x2(x0, x1); lo' = f16x2((x - hi) * 2^11)
+            // paired split: hi = f16x2(x0, x1); lo' = f16x2((x - hi) * 2^11), the difference and
+            // the power-of-two scaling exact, on packed fp32 pairs
             const float x0 = v[8 * u + 2 * p], x1 = v[8 * u + 2 * p + 1];
-            ovf |= !(fabsf(x0) < kF16Overflow && fabsf(x1) < kF16Overflow);  // fp16(x) would be +-inf
             const __half2 h = __floats2half2_rn(x0, x1);
+            // |hi| >= 65520 rounds to inf: the running max of |hi| tells the tile (checked once)
+            hmax = __hmax2(hmax, __habs2(h));
             const float2 hf = __half22float2(h);
-            const __half2 lo = __floats2half2_rn((x0 - hf.x) * LO_SCALE, (x1 - hf.y) * LO_SCALE);
+            unsigned long long xx, hh, d;
+            asm("mov.b64 %0, {%1, %2};" : "=l"(xx) : "f"(x0), "f"(x1));
+            asm("mov.b64 %0, {%1, %2};" : "=l"(hh) : "f"(hf.x), "f"(hf.y));
+            asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(xx), "l"(hh));
+            asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(d) : "l"(s2));
+            float d0, d1;
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+            const __half2 lo = __floats2half2_rn(d0, d1);
             hw[p] = *reinterpret_cast<const uint32_t*>(&h);
             lw[p] = *reinterpret_cast<const uint32_t*>(&lo);
         }
@@ -429,6 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS,
         for (int64_t t = pair; t < a.n_tiles; t += npairs, ++k) {
             float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
             bool ovf = false;
+            __half2 hmax = __float2half2_rn(0.f);
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
@@ -458,11 +477,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS,
                     uint32_t rm2[32], rc2[32];
                     tmem_ld32_async(tb + 32, rm2);
                     tmem_ld32_async(tb + 128 + 32, rc2);
-                    epi32<TM>(ld, l, last, v, col0, row, Ahi, Alo, wo_s, dot, ovf);
+                    epi32<TM>(ld, l, last, v, col0, row, Ahi, Alo, wo_s, dot, ovf, hmax);
                     tmem_wait_tied(rm2);
                     tmem_wait_tied(rc2);
                     combine32(rm2, rc2, kmul, v);
-                    epi32<TM>(ld, l, last, v, col0 + 32, row, Ahi, Alo, wo_s, dot, ovf);
+                    epi32<TM>(ld, l, last, v, col0 + 32, row, Ahi, Alo, wo_s, dot, ovf, hmax);
                     pe_w += prof_clock() - c1;
                     tc_fence_before();
                     if (!last) fence_proxy_async_smem();
@@ -477,6 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(sp::Cfg<N>::THREADS,
                 mbar_wait(&out_empty[b], oe_ph[b]);
                 oe_ph[b] ^= 1u;
             }
+            ovf |= __hisinf(__low2half(hmax)) || __hisinf(__high2half(hmax));  // an activation beyond fp16
             dotbuf[(b * PARTS + part) * TM + row] = ovf ? -INFINITY : (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
