@@ -101,6 +101,26 @@ def test_full_size_bf16_properties(key):
         d_at = O.forward_eval(w.program, params, np.concatenate([pts[r.argmin[m]], q[m]])[None, :])[0]
         assert r.argmin[m] == oarg or float(d_at) - omin <= bound
 
+    # the same check over many motions x the full cloud, against the FP32 path (bit-identical to
+    # the oracle and the reference build: test_c2_full_size_bit_identical, test_gpu_ref_parity),
+    # at the workload's own margin and at a margin placed at the median min (about half the
+    # motions free, so the class check is not vacuous on a workload that is mostly in collision)
+    ms = np.sort(rng.choice(M, size=96, replace=False))
+    exact = model.query_min(pts, q[ms], w.margin, precision="fp32")
+    assert np.abs(r.min[ms].astype(np.float64) - exact.min.astype(np.float64)).max() <= bound
+    for margin in (w.margin, float(np.median(exact.min))):
+        free16 = r.min[ms].astype(np.float64) > margin
+        free32 = exact.min.astype(np.float64) > margin
+        outside = np.abs(exact.min.astype(np.float64) - margin) > bound
+        assert np.array_equal(free16[outside], free32[outside])
+    assert 0.3 <= (exact.min > np.median(exact.min)).mean() <= 0.7
+    # argmin: the same point, or a point whose exact delta is within the bound of the exact min
+    diff = np.nonzero(r.argmin[ms] != exact.argmin)[0]
+    if diff.size:
+        raw = np.concatenate([pts[r.argmin[ms][diff]], q[ms][diff]], axis=1).astype(np.float32)
+        d_at = model.forward_eval(raw, precision="fp32").astype(np.float64)
+        assert np.all(d_at - exact.min[diff].astype(np.float64) <= bound)
+
     # lower bound over the whole workload: min_gpu[m] <= delta_oracle(m, p) + bound
     n = 4000
     ms, ps = rng.integers(0, M, n), rng.integers(0, P, n)
