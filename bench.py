@@ -191,6 +191,48 @@ def run_cpu(w, params, seed, threads, lib, steps, warmup, seconds=10.0):
             (pts, q), res)
 
 
+def reference_build_leg(w, seed, threads, seconds=8.0, repeats=1):
+    """The reference's OWN nn.cpp (oracle/_ref/libref_nn.so: compiled unmodified here against the
+    Eigen-API subset, -O3 -march=x86-64-v3) on the same cloud and motions, one
+    predict_min_distance call per motion from `threads` worker threads (bench.cpp:156,193).  The
+    reference implements the Fig. 2 architecture only (nn.hpp:16-42), so it runs the Fig. 2
+    twin of the workload's network (same width and dof, hidden - 1 blocks; SURVEY.md 8a-0);
+    the port runs the same twin next to it, and their bits are compared.  None when the
+    prebuilt library did not travel with the repo."""
+    try:
+        from oracle import oracle as O
+        from oracle import ref_oracle as R
+        from paper_2402_15281_b200 import program as PR
+        if not R.available():
+            return None
+        prog = w.program
+        twin = prog if prog.name.startswith("fig2") else PR.fig2(len(prog.layers) - 1, prog.width, prog.dof)
+        M, P = cpu_sample(w, threads, seconds)
+        pts, q = w.make(seed=seed, motions=M, points=P)
+        with tempfile.TemporaryDirectory(prefix="svn_ref_") as d:
+            ck = str(Path(d) / "twin.ckpt")
+            params = R.init_model(len(twin.layers) - 1, twin.width, twin.dof, seed, ck)
+            secs = []
+            for _ in range(max(1, repeats)):
+                mn, idx, sec = R.time_predict_min_distance(ck, pts, q, threads)
+                secs.append(sec)
+            sec = statistics.median(secs)
+        t0 = time.perf_counter()
+        omin, oarg, _, _ = O.query_min(twin, params, pts, q, w.margin, threads=threads)
+        port_sec = time.perf_counter() - t0
+        return {"value": M * P / sec, "unit": UNIT, "cores": threads, "kind": "reference", "ms_per_sample": sec * 1e3,
+                "network": f"{twin.name} (Fig. 2 twin of {prog.name})" if twin is not prog else twin.name,
+                "flop_per_query": twin.flops_per_query(),
+                "sample": f"{M} motions x {P} points ({M * P} queries), predict_min_distance per motion "
+                          f"(nn.cpp:460-480) on {threads} threads; reference nn.cpp built -O3 -march=x86-64-v3 "
+                          f"against the Eigen-API subset (oracle/ref)",
+                "port_on_same_network": {"value": M * P / port_sec, "unit": UNIT,
+                                         "bits_equal": bool(np.array_equal(omin.astype(np.float64), mn)
+                                                            and np.array_equal(oarg, idx))}}
+    except Exception as e:  # the baseline leg must not take the bench line down
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+
+
 def bounds_for(network: str, prec: str):
     g = ROOT / "tests" / "golden"
     f = g / ("bf16_bounds.json" if prec == "bf16" else "fp32_split_bounds.json")
@@ -223,16 +265,25 @@ def reference_arm(args, w):
     med_ms = getattr(run_cpu, "last_ms", None)
     # the reference's own call is single-threaded (nn.cpp:116): one thread, ~5 s sample
     v1, s1, _, _ = run_cpu(w, params, args.seed, 1, lib, 1, 0, 5.0)
-    line = {"metric": METRIC, "value": val, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": med_ms,
+    ref_build = reference_build_leg(w, args.seed, threads, per_step, repeats=min(steps, 3))
+    port = {"value": val, "unit": UNIT, "cores": threads, "kind": "port", "network": w.program.name,
+            "sample": sample + f"; oracle restatement of nn.cpp:95-130 (-O3 -march={march}), "
+                               f"{threads} threads on {cpu_model()}",
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": s1}}
+    if ref_build and "value" in ref_build:
+        # the reference's own code compiled here is the arm's number (on the Fig. 2 twin, the only
+        # architecture it implements); the port on the config's own network rides along
+        head, head_ms = dict(ref_build, port=port), ref_build["ms_per_sample"]
+    else:
+        head, head_ms = dict(port, reference_build=ref_build), med_ms
+    line = {"metric": METRIC, "value": head["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head_ms,
             "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded)",
-            "config": {"workload": w.key, "description": w.description, "network": w.program.name},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": sample + f"; oracle restatement of nn.cpp:95-130 (-O3 -march={march}), "
-                                                f"{threads} threads on {cpu_model()}",
-                             "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "sample": s1}},
-            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": w.key, "description": w.description, "network": w.program.name,
+                       "reference_network": head.get("network", w.program.name)},
+            "cpu_baseline": head,
+            "e2e": {"value": head["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -436,7 +487,8 @@ def main():
         lib, march = build_native_oracle()
         val, sample, (spts, sq), ores = run_cpu(w, params, args.seed, threads, lib, 1, 0)
         cpu = {"value": val, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": sample + f"; oracle restatement of nn.cpp:95-130 (-O3 -march={march}) on {cpu_model()}"}
+               "sample": sample + f"; oracle restatement of nn.cpp:95-130 (-O3 -march={march}) on {cpu_model()}",
+               "reference_build": reference_build_leg(w, args.seed, threads, 5.0)}
         if not args.no_parity:
             parity = {"bound": bounds_for(w.program.name, prec), "precision": prec}
             g = model.query_min(spts, sq, w.margin, precision=prec)

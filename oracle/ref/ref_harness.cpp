@@ -1,17 +1,22 @@
 // ref_harness.cpp — TEST INFRASTRUCTURE ONLY.  A C entry layer over the reference's OWN
 // inference code (/root/reference/proj/src/nn.cpp, robot.cpp, geometry.cpp compiled
 // unmodified against oracle/ref/eigen_subset by oracle/ref/Makefile into oracle/_ref/).
-// Only tests/ and tests/golden/make_ref_golden.py load it, as the checker of the C oracle
-// (oracle/sweptnet_oracle.c) and of the CUDA path; nothing in the product links it.
+// tests/ and tests/golden/make_ref_golden.py load it as the checker of the C oracle
+// (oracle/sweptnet_oracle.c) and of the CUDA path, and bench.py's CPU legs (--impl reference,
+// cpu_baseline) time it as the reference's own CPU path; nothing in the product links it.
 //
 // Every entry returns 0 on success or an error kind (1 IoError, 2 FormatError,
 // 3 TruncationError, 4 VersionError, 5 std::invalid_argument, 6 other) with the reference's
 // exception text in ref_last_error().  Models travel as SVCKPT01 files, read and written by
 // the reference's own load_checkpoint / save_checkpoint (nn.cpp:499-576).
+#include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "sweptnet/errors.hpp"
 #include "sweptnet/nn.hpp"
@@ -155,6 +160,54 @@ __attribute__((visibility("default"))) int ref_make_normalizer(int dof, const fl
             shift[k] = sh[k];
             scale[k] = sc[k];
         }
+    });
+}
+
+// The reference's per-motion call pattern, timed (bench.py --impl reference and its cpu_baseline
+// leg): one model, one cloud, M motions, each a predict_min_distance call (nn.cpp:460-480) issued
+// from `threads` worker threads that claim motions from a shared counter — run_box_world's
+// parallel_for over motions (bench.cpp:156,193).  `seconds` covers the calls only (model load and
+// cloud conversion are outside, as they are per scene in the reference).
+__attribute__((visibility("default"))) int ref_time_predict_min_distance(const char* ckpt, const double* cloud, long P,
+                                                                         const double* q01, long M, int dof,
+                                                                         int threads, double* min_out, int* idx_out,
+                                                                         double* seconds) {
+    return guarded([&] {
+        const sweptnet::Mlp m = sweptnet::load_checkpoint(ckpt);
+        std::vector<sweptnet::Vec3> pts(static_cast<size_t>(P));
+        for (long i = 0; i < P; ++i) pts[static_cast<size_t>(i)] = sweptnet::Vec3(cloud[3 * i], cloud[3 * i + 1], cloud[3 * i + 2]);
+        std::vector<sweptnet::Motion> motions(static_cast<size_t>(M));
+        for (long j = 0; j < M; ++j) {
+            sweptnet::Motion& mo = motions[static_cast<size_t>(j)];
+            mo.q0.resize(dof);
+            mo.q1.resize(dof);
+            for (int k = 0; k < dof; ++k) {
+                mo.q0[k] = q01[j * 2 * dof + k];
+                mo.q1[k] = q01[j * 2 * dof + dof + k];
+            }
+        }
+        std::atomic<long> next{0};
+        std::string first_error;
+        std::atomic<bool> failed{false};
+        auto work = [&] {
+            try {
+                for (long j = next.fetch_add(1); j < M; j = next.fetch_add(1)) {
+                    const auto r = sweptnet::predict_min_distance(m, pts, motions[static_cast<size_t>(j)]);
+                    min_out[j] = r.first;
+                    idx_out[j] = r.second;
+                }
+            } catch (const std::exception& e) {
+                if (!failed.exchange(true)) first_error = e.what();
+            }
+        };
+        const int T = threads < 1 ? 1 : threads;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::vector<std::thread> pool;
+        for (int t = 1; t < T; ++t) pool.emplace_back(work);
+        work();
+        for (std::thread& t : pool) t.join();
+        *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (failed) throw std::runtime_error(first_error);
     });
 }
 

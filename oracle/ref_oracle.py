@@ -2,7 +2,8 @@
 geometry.cpp compiled unmodified against oracle/ref/eigen_subset (recipe: oracle/ref/Makefile).
 
 TEST INFRASTRUCTURE ONLY: the checker of the C restatement (oracle/sweptnet_oracle.c) and of
-the CUDA path.  Only tests/ and tests/golden/make_ref_golden.py use it.  Building needs the
+the CUDA path (tests/, tests/golden/make_ref_golden.py), and the reference's own CPU path timed
+by bench.py's CPU legs (--impl reference, cpu_baseline).  Building needs the
 reference sources (/root/reference, present in the build container only); the built .so
 travels to the GPU box with the repo snapshot, where available() tells the tests whether it
 came along.
@@ -57,6 +58,8 @@ def lib(variant: str = "") -> C.CDLL:
     L.ref_forward_eval.argtypes = [C.c_char_p, VP, L64, L64, VP]
     L.ref_forward_eval_f64.argtypes = [C.c_char_p, VP, L64, L64, VP]
     L.ref_predict_min_distance.argtypes = [C.c_char_p, VP, L64, VP, VP, I, VP, VP]
+    if hasattr(L, "ref_time_predict_min_distance"):
+        L.ref_time_predict_min_distance.argtypes = [C.c_char_p, VP, L64, VP, L64, I, I, VP, VP, VP]
     L.ref_make_normalizer.argtypes = [I, VP, L64, VP, VP]
     L.ref_load_checkpoint.argtypes = [C.c_char_p, VP, VP, VP]
     L.ref_uniform_stream.argtypes = [C.c_uint64, L64, C.c_double, C.c_double, VP]
@@ -125,6 +128,19 @@ def predict_min_distance(ckpt, cloud, q0, q1, variant: str = "") -> tuple[float,
     _check(L, L.ref_predict_min_distance(str(ckpt).encode(), _p(cloud), cloud.shape[0], _p(q0), _p(q1), q0.size,
                                          _p(mn), _p(idx)))
     return float(mn[0]), int(idx[0])
+
+
+def time_predict_min_distance(ckpt, cloud, q01, threads: int, variant: str = ""):
+    """M predict_min_distance calls (one per motion, nn.cpp:460-480) from `threads` worker threads,
+    the reference's own per-motion pattern (bench.cpp:156,193); returns (min[M], argmin[M], seconds)."""
+    L = lib(variant)
+    cloud = np.ascontiguousarray(cloud, np.float64).reshape(-1, 3)
+    q01 = np.ascontiguousarray(q01, np.float64)
+    M, dof = q01.shape[0], q01.shape[1] // 2
+    mn, idx, sec = np.zeros(M, np.float64), np.zeros(M, np.int32), np.zeros(1, np.float64)
+    _check(L, L.ref_time_predict_min_distance(str(ckpt).encode(), _p(cloud), cloud.shape[0], _p(q01), M, dof,
+                                              int(threads), _p(mn), _p(idx), _p(sec)))
+    return mn, idx, float(sec[0])
 
 
 def make_normalizer(dof: int, train_x: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
