@@ -23,9 +23,12 @@ time from CUDA events on the launching stream, max over ranks.  L2 is flushed
 (a 256 MiB write, outside the per-step events) before every timed step.  Clocks are
 sampled by nvidia-smi every 100 ms over the timed region, extended with untimed steps
 to at least 1 s when the K steps are shorter.
-`--impl reference` times the reference CPU path (the C restatement of nn.cpp built
--O3 -march=native, all host threads) on a bounded sample of the same workload; it
-loads nothing from the product package's native library.
+`--impl reference` times the reference CPU path on a bounded sample of the same workload,
+on all host threads: the reference's own nn.cpp as built by oracle/ref into oracle/_ref
+(predict_min_distance per motion from worker threads) on the Fig. 2 twin of the config's
+network — the only architecture the reference implements — with the C restatement on the
+config's own network alongside (and alone when oracle/_ref is absent); it loads nothing
+from the product package's native library.
 """
 from __future__ import annotations
 
