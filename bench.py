@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5")
-    ap.add_argument("--precision", default=None, help="override: bf16 | fp32 | fp32_exact | fp32_split")
+    ap.add_argument("--precision", default=None, help="override: bf16 | fp16 | fp32 | fp32_exact | fp32_split")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -238,8 +238,8 @@ def reference_build_leg(w, seed, threads, seconds=8.0, repeats=1):
 
 def bounds_for(network: str, prec: str):
     g = ROOT / "tests" / "golden"
-    f = g / ("bf16_bounds.json" if prec == "bf16" else "fp32_split_bounds.json")
-    if prec not in ("bf16", "fp32_split") or not f.exists():
+    f = g / f"{prec}_bounds.json"
+    if prec not in ("bf16", "fp16", "fp32_split") or not f.exists():
         return 0.0
     d = json.loads(f.read_text())
     return float(d[network]["bound"]) if network in d else None
@@ -417,7 +417,7 @@ def main():
     # ---- roofline of the dominant kernel (the fused MLP) ----------------------
     flop_q = w.program.flops_per_query()
     achieved_tf = M * (pe - pb) * flop_q / (kernel_ms * 1e-3) / 1e12
-    if prec == "bf16":
+    if prec in ("bf16", "fp16"):  # fp16 operands run at the same kind::f16 instruction rate
         peak = float(peaks["bf16_tflops"])
         roof = {"bound": "tensor", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved_tf / peak, "traffic": None,
@@ -504,7 +504,7 @@ def main():
                              library=lib)[3]
             parity["vs_oracle_on_cpu_sample"]["per_point_max_abs_err"] = float(np.max(np.abs(gp - op)))
             parity["vs_oracle_on_cpu_sample"]["per_point_checked"] = int(gp.size)
-    if rank == 0 and not args.no_parity and mode == "motion" and prec in ("bf16", "fp32_split"):
+    if rank == 0 and not args.no_parity and mode == "motion" and prec in ("bf16", "fp16", "fp32_split"):
         # bf16 (or split) against the bit-identical FP32 path over >= 256 motions x the full cloud,
         # as measured (seeded net) and with the output bias calibrated so the median per-motion
         # min sits on the margin (the seeded nets are nearly all in collision)

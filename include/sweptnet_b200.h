@@ -76,12 +76,20 @@ typedef enum {
  *              hidden activation reaches the fp16 range
  *              (|h| >= 65520) or whose input is not finite is reported as delta = -inf: its
  *              motion's min is -inf and its class "not free" (handed to the exact checker),
- *              never dropped. */
+ *              never dropped.
+ *  FP16        the BF16 kernels on fp16 operands (width 256 and 512): the same tcgen05
+ *              instruction rate with 11 significant bits instead of 8, so the per-network
+ *              bound is about 8 times tighter (tests/golden/fp16_bounds.json; DeepSDF 8x512:
+ *              0.012 against 0.089, i.e. inside the 0.02 m margin).  UNSUPPORTED when a
+ *              (BN-folded) weight is outside the fp16 range; a row whose activations leave
+ *              it at run time is reported as delta = -inf (class "not free"), as in
+ *              FP32_SPLIT. */
 typedef enum {
     SVN_PREC_BF16 = 0,
     SVN_PREC_FP32 = 1,
     SVN_PREC_FP32_EXACT = 2,
-    SVN_PREC_FP32_SPLIT = 3
+    SVN_PREC_FP32_SPLIT = 3,
+    SVN_PREC_FP16 = 4
 } svn_precision;
 
 /* One hidden layer of a layer program.  Layer 0 reads the

@@ -62,7 +62,8 @@ enum class Precision {
     BF16 = SVN_PREC_BF16,
     FP32 = SVN_PREC_FP32,
     FP32_EXACT = SVN_PREC_FP32_EXACT,
-    FP32_SPLIT = SVN_PREC_FP32_SPLIT
+    FP32_SPLIT = SVN_PREC_FP32_SPLIT,
+    FP16 = SVN_PREC_FP16
 };
 
 // A layer program; fig2() is the reference network (nn.hpp:11-15).

@@ -18,8 +18,9 @@ LIB_PATH = _build.LIB
 OK, INVALID_ARGUMENT, CUDA_ERROR, OUT_OF_MEMORY, UNSUPPORTED, IO, FORMAT, TRUNCATION, VERSION, NCCL_ERROR, HOST_ERROR = range(11)
 SHARD_MODES = {"auto": 0, "motions": 1, "points": 2}
 # svn_precision
-PREC_BF16, PREC_FP32, PREC_FP32_EXACT, PREC_FP32_SPLIT = 0, 1, 2, 3
-PRECISIONS = {"bf16": PREC_BF16, "fp32": PREC_FP32, "fp32_exact": PREC_FP32_EXACT, "fp32_split": PREC_FP32_SPLIT}
+PREC_BF16, PREC_FP32, PREC_FP32_EXACT, PREC_FP32_SPLIT, PREC_FP16 = 0, 1, 2, 3, 4
+PRECISIONS = {"bf16": PREC_BF16, "fp32": PREC_FP32, "fp32_exact": PREC_FP32_EXACT, "fp32_split": PREC_FP32_SPLIT,
+              "fp16": PREC_FP16}
 
 
 class SvnLayer(C.Structure):

@@ -89,6 +89,8 @@ struct svn_model {
     bool has_bf16 = false;
     bool has_mixed = false;   // width-512 bf16: rows of mixed motions without per-motion folding
     svn::FusedArgs base_bf16{};       // bf16 kernels: base with the BN affine folded (see fold_affine_bf16)
+    svn::FusedArgs base_f16{};        // the same kernels on fp16 operands (precision fp16): own weight / extension images
+    bool has_f16 = false;             // every folded parameter fits the fp16 range
     float* d_wq_bf = nullptr;     // K0 inputs of the bf16 kernels, from the folded parameters
     float* d_mbbase_bf = nullptr;
     float* d_wxslots_bf = nullptr;

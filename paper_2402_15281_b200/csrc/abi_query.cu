@@ -12,6 +12,9 @@ namespace abi {
 svn_status check_prec(const svn_model* m, svn_precision prec) {
     if (prec == SVN_PREC_BF16) {
         if (!m->has_bf16) return fail(SVN_ERR_UNSUPPORTED, "bf16 path needs width 256 or 512");
+    } else if (prec == SVN_PREC_FP16) {
+        if (!m->has_f16)
+            return fail(SVN_ERR_UNSUPPORTED, "fp16 path needs width 256 or 512 and every weight inside the fp16 range");
     } else if (prec == SVN_PREC_FP32 || prec == SVN_PREC_FP32_EXACT) {
         if (m->N != 128 && m->N != 256 && m->N != 512)
             return fail(SVN_ERR_UNSUPPORTED, "fp32 path needs width 128, 256 or 512");
@@ -27,7 +30,7 @@ svn_status check_prec(const svn_model* m, svn_precision prec) {
 // Which fused kernel serves a (model, precision): bf16 tensor cores; fp32-grade split-fp16
 // tensor cores (fp32_split, width 256); or SIMT FFMA in the oracle's order (fp32, fp32_exact).
 Kind kernel_kind(const svn_model*, svn_precision prec) {
-    if (prec == SVN_PREC_BF16) return Kind::BF16;
+    if (prec == SVN_PREC_BF16 || prec == SVN_PREC_FP16) return Kind::BF16;  // one kernel family, two operand formats
     if (prec == SVN_PREC_FP32_SPLIT) return Kind::SPLIT;
     return Kind::SIMT;
 }
@@ -205,7 +208,8 @@ svn_status motion_ext(const svn_model* m, FusedArgs& a, int64_t M, unsigned long
         a.ext_ring = ext;
         a.xq_wq = m->d_wq_bf;
         a.xq_base = m->d_mbbase_bf;
-        SVN_CUDA(launch_ext_ring_init(ext, ctas, m->n_mb ? m->n_mb : 1, m->N, m->d_wxslots_bf, st), "ext ring init");
+        SVN_CUDA(launch_ext_ring_init(ext, ctas, m->n_mb ? m->n_mb : 1, m->N, m->d_wxslots_bf, a.f16, st),
+                 "ext ring init");
         ++g_launches;
         SVN_CUDA(launch_motion_ext(a, m->d_wq_bf, m->d_mbbase_bf, m->d_wxslots_bf, nullptr, keys, counters, n_keys,
                                    sched, st),
@@ -263,7 +267,9 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     DeviceGuard guard(m->device);
     ensure_pool(m->device);
     const Kind kind0 = kernel_kind(m, prec);
-    FusedArgs a = kind0 == Kind::SPLIT ? m->base_split : kind0 == Kind::BF16 ? m->base_bf16 : m->base;
+    FusedArgs a = kind0 == Kind::SPLIT  ? m->base_split
+                  : kind0 == Kind::BF16 ? (prec == SVN_PREC_FP16 ? m->base_f16 : m->base_bf16)
+                                        : m->base;
     // fp32 on the SIMT kernel runs in the oracle's order (no q-fold): at width 512 that costs
     // nothing measurable (c3/c4: 12.0/16.8 M q/s either way) and makes it bit-identical
     const bool exact = kind0 == Kind::SIMT;
@@ -453,7 +459,7 @@ svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw
         tiles.clear();
         for (int64_t t0 = 0; t0 < B; t0 += 128)
             tiles.push_back(TileDesc{t0, t0, 0, static_cast<int32_t>(std::min<int64_t>(128, B - t0))});
-        FusedArgs a = m->base_bf16;
+        FusedArgs a = prec == SVN_PREC_FP16 ? m->base_f16 : m->base_bf16;
         a.mixed = 1;
         a.points = raw_dev;
         a.point_stride = cols;
@@ -485,7 +491,9 @@ svn_status forward_rows(const svn_model* m, svn_precision prec, const float* raw
         SVN_CUDA(cudaStreamSynchronize(st), "forward kernels");
         return SVN_OK;
     }
-    FusedArgs a = kind == Kind::SPLIT ? m->base_split : kind == Kind::BF16 ? m->base_bf16 : m->base;
+    FusedArgs a = kind == Kind::SPLIT  ? m->base_split
+                  : kind == Kind::BF16 ? (prec == SVN_PREC_FP16 ? m->base_f16 : m->base_bf16)
+                                       : m->base;
     a.exact = kind == Kind::SIMT ? 1 : 0;
     a.points = raw_dev;
     a.point_stride = cols;

@@ -73,6 +73,7 @@ struct FusedArgs {
     int tile_rows;             // rows per work item the host cut the tiles with (SIMT: 128/64, or 32)
     unsigned int* sched;       // width-512 bf16 kernel: dynamic tile counter (zeroed by K0)
     int tile_group;            // width-512 bf16 kernel: tiles per claimed chunk (1: per tile)
+    int f16;                   // single-pass tensor-core kernels: operands in fp16 (precision fp16) instead of bf16
     // width-512 bf16 kernel: the per-motion K=16 extension rows (folded bias + x-part splits)
     // are built inside the fused kernel, by each CTA's output warp for the tile two ahead, into a
     // per-CTA ring of two tile slots (L2-resident) that tmap_xq views; null = the K0-built stream
@@ -250,7 +251,7 @@ cudaError_t launch_fused_split(const FusedArgs& a, int num_sms, cudaStream_t st)
 cudaError_t launch_split_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
                              uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init, int64_t n_keys,
                              cudaStream_t st);
-cudaError_t launch_ext_ring_init(uint8_t* ring, int64_t ctas, int n_mb, int N, const float* wx_slots,
+cudaError_t launch_ext_ring_init(uint8_t* ring, int64_t ctas, int n_mb, int N, const float* wx_slots, int f16,
                                  cudaStream_t st);
 cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* mb_base_bias, const float* wx_slots,
                               uint8_t* ext, unsigned long long* keys_init, unsigned int* counters_init,

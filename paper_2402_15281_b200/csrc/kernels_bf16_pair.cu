@@ -70,46 +70,33 @@ struct PairCfg {
     static_assert(COLS % 32 == 0, "epilogue works in 32-column TMEM loads");
 };
 
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-    const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<const uint32_t*>(&p);
-}
-
-__device__ __forceinline__ float bflo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bfhi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
-
-// bf16 hi/lo split of x: hi = bf16(x), lo = bf16(x - hi).
-__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
-    hi = __float2bfloat16_rn(x);
-    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-}
-
-// Write this row's A extension: (1, 1, z0h, z0h, z0l, z1h, z1h, z1l, z2h, z2h, z2l, 0...).
+// The A extension row of a point: (1, 1, z_x splits) against the B rows (b_hi, b_lo, W_x splits).
+template <class F>
 __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, float z1, float z2) {
-    __nv_bfloat16 h0, l0, h1, l1, h2, l2;
-    split_bf16(z0, h0, l0);
-    split_bf16(z1, h1, l1);
-    split_bf16(z2, h2, l2);
-    const __nv_bfloat16 one = __float2bfloat16_rn(1.0f), zero = __float2bfloat16_rn(0.0f);
-    __align__(16) __nv_bfloat16 v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
+    uint16_t h0, l0, h1, l1, h2, l2;
+    F::split(z0, h0, l0);
+    F::split(z1, h1, l1);
+    F::split(z2, h2, l2);
+    constexpr uint16_t one = F::kOne, zero = F::kZero;
+    __align__(16) uint16_t v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
 }
 
-// Rows of mixed motions: the row's q-part as three more K=16 A slabs, z_k = (q_k - shift) * scale
+// Rows of mixed motions (FusedArgs::mixed): the row's own z_q as three more K=16 A slabs, z_q
 // (motion_ext_kernel's arithmetic) in (hi, hi, lo) triples against the model's (hi, lo, hi) W_q
-// triples — the same three-product bf16 split as the x-part.
+// triples — the same three-product split as the x-part.
+template <class F>
 __device__ __forceinline__ void write_axq(uint8_t* axq, uint32_t slab_bytes, uint32_t row, const float* q,
                                           const FusedArgs& a) {
-    __align__(16) __nv_bfloat16 v[48];
-    const __nv_bfloat16 zero = __float2bfloat16_rn(0.0f);
+    __align__(16) uint16_t v[48];
 #pragma unroll
-    for (int i = 0; i < 48; ++i) v[i] = zero;
+    for (int i = 0; i < 48; ++i) v[i] = F::kZero;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         if (k < 2 * a.dof) {
-            __nv_bfloat16 h, l;
-            split_bf16(__fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]), h, l);
+            uint16_t h, l;
+            F::split(__fmul_rn(__fsub_rn(q[k], a.shift[3 + k]), a.scale[3 + k]), h, l);
             v[3 * k] = h;
             v[3 * k + 1] = h;
             v[3 * k + 2] = l;
@@ -124,9 +111,14 @@ __device__ __forceinline__ void write_axq(uint8_t* axq, uint32_t slab_bytes, uin
 }
 
 // Epilogue of 32 columns of one row (the MMA already added bias and x-part).
-template <int N, int TM>
+template <int N, int TM, class F>
 __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                           uint8_t* A, const float* wo_s, float4& dot) {
+                                           uint8_t* A, const float* wo_s, float4& dot, bool& ovf) {
+    // fp16 operands: an activation (or input) beyond the fp16 range is stored as an infinity, and
+    // every accumulator of that row in the next layer is then inf or NaN — which the ReLU pack
+    // would turn into 0.  Two accumulators per 32-column chunk are tested; the row is reported
+    // as delta = -inf (see the output warp).
+    if (F::kHalf) ovf |= !(fabsf(v[0]) <= 3.0e38f) || !(fabsf(v[21]) <= 3.0e38f);
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (!aff && !res && last) {  // plain last layer: straight-line ReLU + output dot (four partial sums)
@@ -156,15 +148,15 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
         for (int u = 0; u < 4; ++u) {
             uint4 p;
             if (act) {
-                p.x = pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]);
-                p.y = pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]);
-                p.z = pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]);
-                p.w = pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]);
+                p.x = F::pack_relu(v[8 * u + 0], v[8 * u + 1]);
+                p.y = F::pack_relu(v[8 * u + 2], v[8 * u + 3]);
+                p.z = F::pack_relu(v[8 * u + 4], v[8 * u + 5]);
+                p.w = F::pack_relu(v[8 * u + 6], v[8 * u + 7]);
             } else {
-                p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
-                p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
-                p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
-                p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+                p.x = F::pack(v[8 * u + 0], v[8 * u + 1]);
+                p.y = F::pack(v[8 * u + 2], v[8 * u + 3]);
+                p.z = F::pack(v[8 * u + 4], v[8 * u + 5]);
+                p.w = F::pack(v[8 * u + 6], v[8 * u + 7]);
             }
             *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
         }
@@ -176,10 +168,10 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
             uint4* slot = reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
             const uint4 o = *slot;
             uint4 p;
-            p.x = add_bf16x2(pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
-            p.y = add_bf16x2(pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]), o.y);
-            p.z = add_bf16x2(pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]), o.z);
-            p.w = add_bf16x2(pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]), o.w);
+            p.x = F::add2(F::pack_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
+            p.y = F::add2(F::pack_relu(v[8 * u + 2], v[8 * u + 3]), o.y);
+            p.z = F::add2(F::pack_relu(v[8 * u + 4], v[8 * u + 5]), o.z);
+            p.w = F::add2(F::pack_relu(v[8 * u + 6], v[8 * u + 7]), o.w);
             *slot = p;
         }
         return;
@@ -203,14 +195,14 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const uint4 o = *reinterpret_cast<const uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
-            v[8 * u + 0] += bflo(o.x);
-            v[8 * u + 1] += bfhi(o.x);
-            v[8 * u + 2] += bflo(o.y);
-            v[8 * u + 3] += bfhi(o.y);
-            v[8 * u + 4] += bflo(o.z);
-            v[8 * u + 5] += bfhi(o.z);
-            v[8 * u + 6] += bflo(o.w);
-            v[8 * u + 7] += bfhi(o.w);
+            v[8 * u + 0] += F::lo(o.x);
+            v[8 * u + 1] += F::hi(o.x);
+            v[8 * u + 2] += F::lo(o.y);
+            v[8 * u + 3] += F::hi(o.y);
+            v[8 * u + 4] += F::lo(o.z);
+            v[8 * u + 5] += F::hi(o.z);
+            v[8 * u + 6] += F::lo(o.w);
+            v[8 * u + 7] += F::hi(o.w);
         }
     }
     if (last) {
@@ -226,10 +218,10 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             uint4 p;
-            p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
-            p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
-            p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
-            p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+            p.x = F::pack(v[8 * u + 0], v[8 * u + 1]);
+            p.y = F::pack(v[8 * u + 2], v[8 * u + 3]);
+            p.z = F::pack(v[8 * u + 4], v[8 * u + 5]);
+            p.w = F::pack(v[8 * u + 6], v[8 * u + 7]);
             *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
         }
     }
@@ -240,7 +232,7 @@ __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last,
 // motion_ext_kernel's arithmetic (z_q = (q - shift) * scale; bias first, then q0, q1 in order),
 // then its bf16 hi/lo split into the row's first word.  NQ = 2 * dof at compile time
 // (0: runtime), so all 4 x NQ weight loads of an n-half are independent and issued together.
-template <int BR, int NH, int NQ>
+template <int BR, int NH, int NQ, class F>
 __device__ __noinline__ void build_ext(const FusedArgs& a, int32_t motion, uint8_t* ring, uint32_t rank, uint32_t lane) {
     const int N = 2 * NH;
     const int nq = NQ > 0 ? NQ : 2 * a.dof;
@@ -276,17 +268,17 @@ __device__ __noinline__ void build_ext(const FusedArgs& a, int32_t motion, uint8
             uint8_t* blob = ring + (sl * 2 + nh) * BR * 32;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                __nv_bfloat16 bh, bl;
-                split_bf16(acc[j], bh, bl);
-                const __nv_bfloat162 w2 = __halves2bfloat162(bh, bl);
+                uint16_t bh, bl;
+                F::split(acc[j], bh, bl);
                 const uint32_t rr = static_cast<uint32_t>(j * 32) + lane;
-                *reinterpret_cast<uint32_t*>(blob + ext_offset(rr, 0)) = *reinterpret_cast<const uint32_t*>(&w2);
+                *reinterpret_cast<uint32_t*>(blob + ext_offset(rr, 0)) =
+                    static_cast<uint32_t>(bh) | (static_cast<uint32_t>(bl) << 16);
             }
         }
     }
 }
 
-template <int N, int TMR>
+template <int N, int TMR, class F>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THREADS, 1)
     fused_bf16_pair_kernel(const __grid_constant__ FusedArgs a) {
     using C = PairCfg<N, TMR>;
@@ -430,7 +422,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
     } else if (warp == 1) {
         // -------------------------------------------------------------- MMA issuer --
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = idesc_bf16(2 * C::TM, C::NH);
+            constexpr uint32_t idesc = F::idesc(2 * C::TM, C::NH);
             const uint32_t a_base = smem_u32(A), s_base = smem_u32(stages), ax_base = smem_u32(AX);
             int stage = 0;
             uint32_t phase = 0;
@@ -528,6 +520,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
         for (int64_t k = 0;; ++k) {
             if (tile_at(k) >= a.n_tiles) break;
             float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
+            bool ovf = false;  // fp16 operands: this row left the fp16 range (pair_epi32)
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
@@ -551,9 +544,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                         tmem_wait_tied2(ra, rb);
 #pragma unroll
                         for (int q = 0; q < NCH; q += 2) {
-                            pair_epi32<N, C::TM>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot);
+                            pair_epi32<N, C::TM, F>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot, ovf);
                             if (q + 2 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32 * (q + 2)), ra);
-                            pair_epi32<N, C::TM>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot);
+                            pair_epi32<N, C::TM, F>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot, ovf);
                             if (q + 3 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32 * (q + 3)), rb);
                             if (q + 2 < NCH) tmem_wait_tied2(ra, rb);
                         }
@@ -574,7 +567,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                 mbar_wait(&out_empty[b], oe_ph[b]);
                 oe_ph[b] ^= 1u;
             }
-            dotbuf[(b * C::PARTS + part) * C::TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
+            dotbuf[(b * C::PARTS + part) * C::TM + row] =
+                (F::kHalf && ovf) ? -INFINITY : (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
             pe_o += prof_clock() - c3;
@@ -617,12 +611,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
         auto store_ax = [&](int b) {
 #pragma unroll
             for (int q = 0; q < C::RQ; ++q) {
-                write_ax(AX + b * C::AXP, static_cast<uint32_t>(q * 32) + lane,
+                write_ax<F>(AX + b * C::AXP, static_cast<uint32_t>(q * 32) + lane,
                          (px[q][0] - a.shift[0]) * a.scale[0], (px[q][1] - a.shift[1]) * a.scale[1],
                          (px[q][2] - a.shift[2]) * a.scale[2]);
                 if constexpr (C::TM == 64) {
                     if (a.mixed)
-                        write_axq(AX + b * C::AXP + C::AX_BYTES, C::AX_BYTES, static_cast<uint32_t>(q * 32) + lane, pq[q], a);
+                        write_axq<F>(AX + b * C::AXP + C::AX_BYTES, C::AX_BYTES, static_cast<uint32_t>(q * 32) + lane, pq[q], a);
                 }
             }
             fence_proxy_async_smem();
@@ -645,13 +639,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                 ring_motion[b] = motion;
                 uint8_t* ring = a.ext_ring + (static_cast<int64_t>(blockIdx.x) * C::XR + b) * a.n_mb * 2 * C::BR * 32;
                 switch (2 * a.dof) {  // compile-time q width: every load of a slot in flight at once
-                    case 12: build_ext<C::BR, C::NH, 12>(a, motion, ring, rank, lane); break;
-                    case 14: build_ext<C::BR, C::NH, 14>(a, motion, ring, rank, lane); break;
-                    case 4: build_ext<C::BR, C::NH, 4>(a, motion, ring, rank, lane); break;
-                    case 6: build_ext<C::BR, C::NH, 6>(a, motion, ring, rank, lane); break;
-                    case 8: build_ext<C::BR, C::NH, 8>(a, motion, ring, rank, lane); break;
-                    case 10: build_ext<C::BR, C::NH, 10>(a, motion, ring, rank, lane); break;
-                    default: build_ext<C::BR, C::NH, 0>(a, motion, ring, rank, lane); break;
+                    case 12: build_ext<C::BR, C::NH, 12, F>(a, motion, ring, rank, lane); break;
+                    case 14: build_ext<C::BR, C::NH, 14, F>(a, motion, ring, rank, lane); break;
+                    case 4: build_ext<C::BR, C::NH, 4, F>(a, motion, ring, rank, lane); break;
+                    case 6: build_ext<C::BR, C::NH, 6, F>(a, motion, ring, rank, lane); break;
+                    case 8: build_ext<C::BR, C::NH, 8, F>(a, motion, ring, rank, lane); break;
+                    case 10: build_ext<C::BR, C::NH, 10, F>(a, motion, ring, rank, lane); break;
+                    default: build_ext<C::BR, C::NH, 0, F>(a, motion, ring, rank, lane); break;
                 }
                 fence_proxy_async_global();  // generic-proxy writes -> the producer's TMA reads
                 __threadfence();
@@ -728,6 +722,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                 const int r = q * 32 + static_cast<int>(lane);
                 const float* d = dotbuf + (b * C::PARTS) * C::TM + r;
                 delta[q] = (C::PARTS == 2 ? d[0] + d[C::TM] : (d[0] + d[C::TM]) + (d[2 * C::TM] + d[3 * C::TM])) + a.bo;
+                // fp16 operands: an activation beyond the fp16 range is an infinity that spreads over
+                // the row's later layers and arrives here as inf or NaN.  Such a row is reported as
+                // -inf (its motion: min -inf, class "not free", handed to the exact checker — the safe
+                // side of collision.cpp:68) instead of dropping out of the min as a NaN.
+                if (F::kHalf && !(fabsf(delta[q]) <= 3.0e38f)) delta[q] = -INFINITY;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_empty[b]);
@@ -774,17 +773,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
     if (warp == 1) tmem_dealloc_pair(tmem, N);
 }
 
-template <int N, int TM>
+template <int N, int TM, class F>
 static cudaError_t launch_pair_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
     using C = PairCfg<N, TM>;
     static SmemOptIn opt;
-    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pair_kernel<N, TM>), (int)C::SMEM);
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pair_kernel<N, TM, F>), (int)C::SMEM);
     if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     if (a.n_tiles < pairs) pairs = a.n_tiles;
     if (pairs < 1) return cudaSuccess;
-    const cudaError_t le = launch_fused_pdl(fused_bf16_pair_kernel<N, TM>, static_cast<unsigned>(2 * pairs), C::THREADS,
-                                            C::SMEM, st, a);
+    const cudaError_t le = launch_fused_pdl(fused_bf16_pair_kernel<N, TM, F>, static_cast<unsigned>(2 * pairs),
+                                            C::THREADS, C::SMEM, st, a);
     return le != cudaSuccess ? le : cudaGetLastError();
 }
 
@@ -792,7 +791,11 @@ cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t
     switch (a.N) {
         case 256: return launch_fused_bf16_pp(a, num_sms, st);  // two tiles in flight (kernels_bf16_pp.cu)
         case 512:  // 128-row pair tiles for launches with fewer 256-row tiles than pairs (abi tile_rows_for)
-            return a.tile_rows == 128 ? launch_pair_n<512, 64>(a, num_sms, st) : launch_pair_n<512, 128>(a, num_sms, st);
+            if (a.f16)  // fp16 operands (precision fp16): the same kernel on the other 16-bit format
+                return a.tile_rows == 128 ? launch_pair_n<512, 64, FmtF16>(a, num_sms, st)
+                                          : launch_pair_n<512, 128, FmtF16>(a, num_sms, st);
+            return a.tile_rows == 128 ? launch_pair_n<512, 64, FmtBf16>(a, num_sms, st)
+                                      : launch_pair_n<512, 128, FmtBf16>(a, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -801,6 +804,7 @@ cudaError_t launch_fused_bf16_pair(const FusedArgs& a, int num_sms, cudaStream_t
 // slots 0..1, the b_m word, are written by the fused kernel per motion).  One thread per row of
 // the ring [cta slot][mb slot][n-half] blobs of N/4 rows; column n of a row follows the pair
 // kernel's blob order (n-half, CTA rank within the pair).
+template <class F>
 __global__ void ext_ring_init_kernel(uint8_t* __restrict__ ring, int64_t n_blobs, int n_mb, int N,
                                      const float* __restrict__ wx_slots, int xr) {
     const int BR = N / 4, NH = N / 2;
@@ -813,22 +817,27 @@ __global__ void ext_ring_init_kernel(uint8_t* __restrict__ ring, int64_t n_blobs
     const int64_t cta = blob / (2 * n_mb) / xr;
     const int n = nh * NH + static_cast<int>(cta & 1) * BR + static_cast<int>(rr);
     const float* wx = wx_slots + static_cast<int64_t>(sl) * 3 * N;
-    __nv_bfloat16 h0, l0, h1, l1, h2, l2;
-    split_bf16(wx[n], h0, l0);
-    split_bf16(wx[N + n], h1, l1);
-    split_bf16(wx[2 * N + n], h2, l2);
-    const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
-    __align__(16) __nv_bfloat16 v[16] = {z, z, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
+    uint16_t h0, l0, h1, l1, h2, l2;
+    F::split(wx[n], h0, l0);
+    F::split(wx[N + n], h1, l1);
+    F::split(wx[2 * N + n], h2, l2);
+    constexpr uint16_t z = F::kZero;
+    __align__(16) uint16_t v[16] = {z, z, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
     uint8_t* base = ring + blob * BR * 32;
     *reinterpret_cast<uint4*>(base + ext_offset(rr, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
     *reinterpret_cast<uint4*>(base + ext_offset(rr, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
 }
 
-cudaError_t launch_ext_ring_init(uint8_t* ring, int64_t ctas, int n_mb, int N, const float* wx_slots, cudaStream_t st) {
+cudaError_t launch_ext_ring_init(uint8_t* ring, int64_t ctas, int n_mb, int N, const float* wx_slots, int f16,
+                                 cudaStream_t st) {
     constexpr int xr = PairCfg<512>::XR;
     const int64_t n_blobs = ctas * xr * n_mb * 2;
     const int64_t rows = n_blobs * (N / 4);
-    ext_ring_init_kernel<<<static_cast<unsigned>((rows + 255) / 256), 256, 0, st>>>(ring, n_blobs, n_mb, N, wx_slots, xr);
+    const unsigned grid = static_cast<unsigned>((rows + 255) / 256);
+    if (f16)
+        ext_ring_init_kernel<FmtF16><<<grid, 256, 0, st>>>(ring, n_blobs, n_mb, N, wx_slots, xr);
+    else
+        ext_ring_init_kernel<FmtBf16><<<grid, 256, 0, st>>>(ring, n_blobs, n_mb, N, wx_slots, xr);
     return cudaGetLastError();
 }
 
@@ -840,6 +849,7 @@ struct QNormX {
     float shift[kMaxIn], scale[kMaxIn];
 };
 
+template <class F>
 __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N, int n_mb,
                                   const float* __restrict__ wq, const float* __restrict__ base_bias,
                                   const float* __restrict__ wx_slots, uint8_t* __restrict__ ext, const QNormX qn,
@@ -867,13 +877,13 @@ __global__ void motion_ext_kernel(const float* __restrict__ q01, int dof, int N,
     for (int n = threadIdx.x; n < N; n += blockDim.x) {
         float acc = base_bias[slot * N + n];
         for (int k = 0; k < nq; ++k) acc = __fmaf_rn(zq[k], w[k * N + n], acc);
-        __nv_bfloat16 bh, bl, h0, l0, h1, l1, h2, l2;
-        split_bf16(acc, bh, bl);
-        split_bf16(wx[n], h0, l0);
-        split_bf16(wx[N + n], h1, l1);
-        split_bf16(wx[2 * N + n], h2, l2);
-        const __nv_bfloat16 z = __float2bfloat16_rn(0.0f);
-        __align__(16) __nv_bfloat16 v[16] = {bh, bl, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
+        uint16_t bh, bl, h0, l0, h1, l1, h2, l2;
+        F::split(acc, bh, bl);
+        F::split(wx[n], h0, l0);
+        F::split(wx[N + n], h1, l1);
+        F::split(wx[2 * N + n], h2, l2);
+        constexpr uint16_t z = F::kZero;
+        __align__(16) uint16_t v[16] = {bh, bl, h0, l0, h0, h1, l1, h1, h2, l2, h2, z, z, z, z, z};
         uint8_t* base;
         int rr;
         if (pp_layout) {  // width-256 ping-pong kernel: blobs [r] of N/2 rows
@@ -904,8 +914,14 @@ cudaError_t launch_motion_ext(const FusedArgs& a, const float* wq, const float* 
         qn.scale[k] = a.scale[3 + k];
     }
     dim3 grid(static_cast<unsigned>(a.M), (a.n_mb > 0 && ext) ? a.n_mb : 1);
-    motion_ext_kernel<<<grid, ext ? 256 : 32, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots, ext, qn,
-                                             keys_init, counters_init, n_keys, a.N == 256 ? 1 : 0, sched_reset);
+    if (a.f16)
+        motion_ext_kernel<FmtF16><<<grid, ext ? 256 : 32, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots,
+                                                                  ext, qn, keys_init, counters_init, n_keys,
+                                                                  a.N == 256 ? 1 : 0, sched_reset);
+    else
+        motion_ext_kernel<FmtBf16><<<grid, ext ? 256 : 32, 0, st>>>(a.q01, a.dof, a.N, a.n_mb, wq, mb_base_bias, wx_slots,
+                                                                   ext, qn, keys_init, counters_init, n_keys,
+                                                                   a.N == 256 ? 1 : 0, sched_reset);
     return cudaGetLastError();
 }
 

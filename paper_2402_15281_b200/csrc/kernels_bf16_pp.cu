@@ -61,34 +61,26 @@ struct Cfg {
     static_assert(SMEM <= 232448, "shared memory budget");
 };
 
-__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
-    const __nv_bfloat162 p = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<const uint32_t*>(&p);
-}
-__device__ __forceinline__ float bflo(uint32_t u) { return __uint_as_float(u << 16); }
-__device__ __forceinline__ float bfhi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
-
-__device__ __forceinline__ void split(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
-    hi = __float2bfloat16_rn(x);
-    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
-}
-
+template <class F>
 __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, float z1, float z2) {
-    __nv_bfloat16 h0, l0, h1, l1, h2, l2;
-    split(z0, h0, l0);
-    split(z1, h1, l1);
-    split(z2, h2, l2);
-    const __nv_bfloat16 one = __float2bfloat16_rn(1.0f), zero = __float2bfloat16_rn(0.0f);
-    __align__(16) __nv_bfloat16 v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
+    uint16_t h0, l0, h1, l1, h2, l2;
+    F::split(z0, h0, l0);
+    F::split(z1, h1, l1);
+    F::split(z2, h2, l2);
+    constexpr uint16_t one = F::kOne, zero = F::kZero;
+    __align__(16) uint16_t v[16] = {one, one, h0, h0, l0, h1, h1, l1, h2, h2, l2, zero, zero, zero, zero, zero};
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 0)) = *reinterpret_cast<const uint4*>(&v[0]);
     *reinterpret_cast<uint4*>(ax + ext_offset(row, 8)) = *reinterpret_cast<const uint4*>(&v[8]);
 }
 
 // 32 columns of one row: activation (+ Fig. 2 affine/residual) then bf16 store or output dot
 // (accumulated in four partial sums so the 128-column dot is not one dependent FMA chain).
-template <int TM>
+template <int TM, class F>
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                      uint8_t* A, const float* wo_s, float4& dot) {
+                                      uint8_t* A, const float* wo_s, float4& dot, bool& ovf) {
+    // fp16 operands: a value beyond the fp16 range is stored as an infinity and makes every
+    // accumulator of its row inf or NaN in the next layer (kernels_bf16_pair.cu: pair_epi32)
+    if (F::kHalf) ovf |= !(fabsf(v[0]) <= 3.0e38f) || !(fabsf(v[21]) <= 3.0e38f);
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (!aff && !res && last) {
@@ -119,15 +111,15 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
         for (int u = 0; u < 4; ++u) {
             uint4 p;
             if (act) {
-                p.x = pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]);
-                p.y = pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]);
-                p.z = pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]);
-                p.w = pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]);
+                p.x = F::pack_relu(v[8 * u + 0], v[8 * u + 1]);
+                p.y = F::pack_relu(v[8 * u + 2], v[8 * u + 3]);
+                p.z = F::pack_relu(v[8 * u + 4], v[8 * u + 5]);
+                p.w = F::pack_relu(v[8 * u + 6], v[8 * u + 7]);
             } else {
-                p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
-                p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
-                p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
-                p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+                p.x = F::pack(v[8 * u + 0], v[8 * u + 1]);
+                p.y = F::pack(v[8 * u + 2], v[8 * u + 3]);
+                p.z = F::pack(v[8 * u + 4], v[8 * u + 5]);
+                p.w = F::pack(v[8 * u + 6], v[8 * u + 7]);
             }
             *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
         }
@@ -139,10 +131,10 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
             uint4* slot = reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
             const uint4 o = *slot;
             uint4 p;
-            p.x = add_bf16x2(pack_bf16_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
-            p.y = add_bf16x2(pack_bf16_relu(v[8 * u + 2], v[8 * u + 3]), o.y);
-            p.z = add_bf16x2(pack_bf16_relu(v[8 * u + 4], v[8 * u + 5]), o.z);
-            p.w = add_bf16x2(pack_bf16_relu(v[8 * u + 6], v[8 * u + 7]), o.w);
+            p.x = F::add2(F::pack_relu(v[8 * u + 0], v[8 * u + 1]), o.x);
+            p.y = F::add2(F::pack_relu(v[8 * u + 2], v[8 * u + 3]), o.y);
+            p.z = F::add2(F::pack_relu(v[8 * u + 4], v[8 * u + 5]), o.z);
+            p.w = F::add2(F::pack_relu(v[8 * u + 6], v[8 * u + 7]), o.w);
             *slot = p;
         }
         return;
@@ -166,14 +158,14 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const uint4 o = *reinterpret_cast<const uint4*>(A + sw128_offset(row, c0 + 8 * u, TM));
-            v[8 * u + 0] += bflo(o.x);
-            v[8 * u + 1] += bfhi(o.x);
-            v[8 * u + 2] += bflo(o.y);
-            v[8 * u + 3] += bfhi(o.y);
-            v[8 * u + 4] += bflo(o.z);
-            v[8 * u + 5] += bfhi(o.z);
-            v[8 * u + 6] += bflo(o.w);
-            v[8 * u + 7] += bfhi(o.w);
+            v[8 * u + 0] += F::lo(o.x);
+            v[8 * u + 1] += F::hi(o.x);
+            v[8 * u + 2] += F::lo(o.y);
+            v[8 * u + 3] += F::hi(o.y);
+            v[8 * u + 4] += F::lo(o.z);
+            v[8 * u + 5] += F::hi(o.z);
+            v[8 * u + 6] += F::lo(o.w);
+            v[8 * u + 7] += F::hi(o.w);
         }
     }
     if (last) {
@@ -189,10 +181,10 @@ __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, floa
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             uint4 p;
-            p.x = pack2(v[8 * u + 0], v[8 * u + 1]);
-            p.y = pack2(v[8 * u + 2], v[8 * u + 3]);
-            p.z = pack2(v[8 * u + 4], v[8 * u + 5]);
-            p.w = pack2(v[8 * u + 6], v[8 * u + 7]);
+            p.x = F::pack(v[8 * u + 0], v[8 * u + 1]);
+            p.y = F::pack(v[8 * u + 2], v[8 * u + 3]);
+            p.z = F::pack(v[8 * u + 4], v[8 * u + 5]);
+            p.w = F::pack(v[8 * u + 6], v[8 * u + 7]);
             *reinterpret_cast<uint4*>(A + sw128_offset(row, c0 + 8 * u, TM)) = p;
         }
     }
@@ -211,7 +203,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int TMR>
+template <int TMR, class F>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     fused_bf16_pp_kernel(const __grid_constant__ FusedArgs a) {
     using namespace pp;
@@ -334,7 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer --
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t idesc = idesc_bf16(2 * TM, N);
+            constexpr uint32_t idesc = F::idesc(2 * TM, N);
             const uint32_t a_base = smem_u32(Abuf), ax_base = smem_u32(AX), w_base = smem_u32(wring);
             const uint32_t x_base = smem_u32(xring);
             int ws = 0, xs = 0;
@@ -428,6 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
             if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
         }
         float4 dot[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+        bool ovf[2] = {false, false};  // fp16 operands: the slot's row left the fp16 range
         unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0;
         for (int64_t j = 0; j < R; ++j) {
             const int nslots = has(j, 1) ? 2 : 1;
@@ -456,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
                             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
                             if (q + 1 < NCH) tmem_ld32_async(tbase + static_cast<uint32_t>(c0c + 32 * (q + 1)), nxt);
-                            epi32<TM>(ld, l, last, reinterpret_cast<float*>(cur), cq + c0c + 32 * q, row, A, wo_s, dot[s]);
+                            epi32<TM, F>(ld, l, last, reinterpret_cast<float*>(cur), cq + c0c + 32 * q, row, A, wo_s, dot[s], ovf[s]);
                             if (q + 1 < NCH) tmem_wait_tied(nxt);
                         }
                     }
@@ -476,8 +469,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             mbar_wait(&out_empty[s], oe_ph[s]);
                             oe_ph[s] ^= 1u;
                         }
-                        dotbuf[(s * PARTS + part) * TM + row] = (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
+                        dotbuf[(s * PARTS + part) * TM + row] =
+                            (F::kHalf && ovf[s]) ? -INFINITY : (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
                         dot[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        ovf[s] = false;
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&out_full[s]);
                     }
@@ -519,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
         auto store_ax = [&]() {
 #pragma unroll
             for (int k = 0; k < RQ; ++k)
-                write_ax(AX + s * AX_BYTES, static_cast<uint32_t>(k * 32) + lane, (px[k][0] - a.shift[0]) * a.scale[0],
+                write_ax<F>(AX + s * AX_BYTES, static_cast<uint32_t>(k * 32) + lane, (px[k][0] - a.shift[0]) * a.scale[0],
                          (px[k][1] - a.shift[1]) * a.scale[1], (px[k][2] - a.shift[2]) * a.scale[2]);
             fence_proxy_async_smem();
             __syncwarp();
@@ -549,6 +544,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                 const int r = k * 32 + static_cast<int>(lane);
                 const float* d = dotbuf + (s * PARTS) * TM + r;
                 delta[k] = (PARTS == 2 ? d[0] + d[TM] : (d[0] + d[TM]) + (d[2 * TM] + d[3 * TM])) + a.bo;
+                // fp16 operands: a row that left the fp16 range arrives as inf / NaN and is reported as
+                // -inf (class "not free") instead of dropping out of the min (kernels_bf16_pair.cu)
+                if (F::kHalf && !(fabsf(delta[k]) <= 3.0e38f)) delta[k] = -INFINITY;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_empty[s]);
@@ -603,11 +601,11 @@ extern "C" __attribute__((visibility("default"))) int svn_debug_cta_times(unsign
 }
 #endif
 
-template <int TM>
+template <int TM, class F>
 static cudaError_t launch_pp_n(const FusedArgs& a, int num_sms, cudaStream_t st) {
     static SmemOptIn opt;
     constexpr uint32_t smem = pp::Cfg<TM>::SMEM;
-    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pp_kernel<TM>), (int)smem);
+    cudaError_t e = opt.ensure(reinterpret_cast<const void*>(fused_bf16_pp_kernel<TM, F>), (int)smem);
     if (e != cudaSuccess) return e;
     int64_t pairs = num_sms / 2;
     // two tiles in flight per pair, unless there are too few tiles to fill the SMs that way:
@@ -615,14 +613,15 @@ static cudaError_t launch_pp_n(const FusedArgs& a, int num_sms, cudaStream_t st)
     const int64_t need = a.n_tiles <= pairs ? a.n_tiles : (a.n_tiles + 1) / 2;
     if (need < pairs) pairs = need;
     if (pairs < 1) return cudaSuccess;
-    const cudaError_t le = launch_fused_pdl(fused_bf16_pp_kernel<TM>, static_cast<unsigned>(2 * pairs), pp::THREADS,
+    const cudaError_t le = launch_fused_pdl(fused_bf16_pp_kernel<TM, F>, static_cast<unsigned>(2 * pairs), pp::THREADS,
                                             smem, st, a);
     return le != cudaSuccess ? le : cudaGetLastError();
 }
 
 cudaError_t launch_fused_bf16_pp(const FusedArgs& a, int num_sms, cudaStream_t st) {
     // 128-row pair tiles for launches with fewer 256-row tiles than pairs (abi tile_rows_for)
-    return a.tile_rows == 128 ? launch_pp_n<64>(a, num_sms, st) : launch_pp_n<128>(a, num_sms, st);
+    if (a.f16) return a.tile_rows == 128 ? launch_pp_n<64, FmtF16>(a, num_sms, st) : launch_pp_n<128, FmtF16>(a, num_sms, st);
+    return a.tile_rows == 128 ? launch_pp_n<64, FmtBf16>(a, num_sms, st) : launch_pp_n<128, FmtBf16>(a, num_sms, st);
 }
 
 }  // namespace svn

@@ -1,8 +1,8 @@
 #!/usr/bin/env python3
-"""Freeze the bf16 per-point bound per network: bound = 2 x the max
-|delta_bf16 - delta_oracle| over a fixed calibration subset (seed 100, 8 motions x
-4096 points), rounded up to 2 significant digits.  Writes gpurun_out/bf16_bounds.json;
-the committed copy is tests/golden/bf16_bounds.json."""
+"""Freeze the per-point bound of a 16-bit tensor-core precision (bf16 default, or fp16: argv[1])
+per network: bound = 2 x the max |delta_gpu - delta_oracle| over a fixed
+calibration subset (seed 100, 8 motions x 4096 points), rounded up to 2 significant digits.
+Writes gpurun_out/<prec>_bounds.json; the committed copy is tests/golden/<prec>_bounds.json."""
 import json
 import math
 import sys
@@ -30,16 +30,17 @@ def up2(x):
     return math.ceil(x / 10 ** (e - 1)) * 10 ** (e - 1)
 
 
-out = {"method": "2 x max |bf16 - oracle fp32| on seed 100, 8 motions x 4096 points, rounded up (2 s.f.)"}
+PREC = sys.argv[1] if len(sys.argv) > 1 else "bf16"
+out = {"method": f"2 x max |{PREC} - oracle fp32| on seed 100, 8 motions x 4096 points, rounded up (2 s.f.)"}
 for name, (prog, bound, wkey) in NETS.items():
     w = WORKLOADS[wkey]
     pts, q = w.make(seed=100, motions=8, points=4096)
     params = S.init_params(prog, 100, bound)
-    r = S.Model(prog, params).query_min(pts, q, w.margin, precision="bf16", per_point=True)
+    r = S.Model(prog, params).query_min(pts, q, w.margin, precision=PREC, per_point=True)
     _, _, _, opp = O.query_min(prog, params, pts, q, w.margin, per_point=True, threads=32)
     err = float(np.abs(r.per_point.astype(np.float64) - opp).max())
     scale = float(np.abs(opp).max())
     out[name] = {"max_err": err, "bound": up2(2 * err), "max_abs_delta": scale}
     print(name, out[name], flush=True)
 (ROOT / "gpurun_out").mkdir(exist_ok=True)
-(ROOT / "gpurun_out" / "bf16_bounds.json").write_text(json.dumps(out, indent=1))
+(ROOT / "gpurun_out" / f"{PREC}_bounds.json").write_text(json.dumps(out, indent=1))

@@ -32,21 +32,25 @@ from paper_2402_15281_b200.workloads import WORKLOADS  # noqa: E402
 
 _B = json.loads((ROOT / "tests" / "golden" / "bf16_bounds.json").read_text())
 BF16_BOUND = {k: v["bound"] for k, v in _B.items() if isinstance(v, dict)}
+_H = json.loads((ROOT / "tests" / "golden" / "fp16_bounds.json").read_text())
+FP16_BOUND = {k: v["bound"] for k, v in _H.items() if isinstance(v, dict)}
 _F = json.loads((ROOT / "tests" / "golden" / "fp32_split_bounds.json").read_text())
 FP32_SPLIT_BOUND = {k: v["bound"] for k, v in _F.items() if isinstance(v, dict)}
 
 # (config, motions, points, precisions): samples sized so the oracle takes seconds
 CASES = [
-    ("c1", 1, 4096, ["fp32", "fp32_split", "bf16"]),
-    ("c2", 64, 2048, ["fp32", "fp32_split", "bf16"]),
-    ("c3", 16, 2048, ["bf16", "fp32", "fp32_split"]),
-    ("c4", 16, 2048, ["bf16", "fp32", "fp32_split"]),
+    ("c1", 1, 4096, ["fp32", "fp32_split", "bf16", "fp16"]),
+    ("c2", 64, 2048, ["fp32", "fp32_split", "bf16", "fp16"]),
+    ("c3", 16, 2048, ["bf16", "fp16", "fp32", "fp32_split"]),
+    ("c4", 16, 2048, ["bf16", "fp16", "fp32", "fp32_split"]),
 ]
 
 
 def tol(prec: str, program) -> float:
     if prec == "fp32_split":
         return FP32_SPLIT_BOUND[program.name]
+    if prec == "fp16":
+        return FP16_BOUND.get(program.name, float("nan"))
     return {"fp32_exact": 0.0, "fp32": 1e-5}.get(prec, BF16_BOUND.get(program.name, float("nan")))
 
 

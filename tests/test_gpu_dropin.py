@@ -63,7 +63,7 @@ def test_reference_api_with_dropin_matches_unpatched_reference(name, tmp_path):
 
 
 @pytest.mark.skipif(not EXE.exists(), reason="oracle/_ref/ref_dropin_driver not built (needs /root/reference)")
-@pytest.mark.parametrize("prec", ["fp32_split", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32_split", "bf16", "fp16"])
 @pytest.mark.parametrize("name", [n for n in NAMES if int(G.case(Z, n)[2]) in (256, 512)])
 def test_dropin_tensor_core_precisions_within_bounds(prec, name, tmp_path):
     """SWEPTNET_B200_PRECISION selects the drop-in's arithmetic (integration/nn_b200.cpp): the
@@ -73,7 +73,7 @@ def test_dropin_tensor_core_precisions_within_bounds(prec, name, tmp_path):
     import os
     g, prog, _, p = G.params(Z, name)
     key = f"fig2_{prog.n_layers - 1}x{prog.width}"
-    f = ROOT / "tests" / "golden" / ("bf16_bounds.json" if prec == "bf16" else "fp32_split_bounds.json")
+    f = ROOT / "tests" / "golden" / f"{prec}_bounds.json"
     bound = json.loads(f.read_text())[key]["bound"]
     ck = tmp_path / "m.ckpt"
     G.write_checkpoint(ck, prog, p)
