@@ -30,7 +30,9 @@ case "$task" in
     for a in "--config c1" "--config c2" "--config c3" "--config c4" "--config c5single" \
              "--config c1 --precision fp32_split" "--config c2 --precision fp32_split" \
              "--config c1 --precision bf16" "--config c2 --precision bf16" "--config paper" \
-             "--config c3 --precision fp32_split" "--config c4 --precision fp32_split" "--config c3 --precision fp32"; do
+             "--config c3 --precision fp32_split" "--config c4 --precision fp32_split" "--config c3 --precision fp32" \
+             "--config c3 --precision fp16" "--config c4 --precision fp16" "--config c2 --precision fp16" \
+             "--config c1 --precision fp16" "--config paper --precision fp16"; do
       n=$(echo "$a" | tr -d ' -'); timeout 900 python bench.py $a --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/cfg_$n.log 2>&1
       line gpurun_out/cfg_$n.log "$a"
     done ;;
