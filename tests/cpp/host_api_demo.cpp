@@ -1,5 +1,6 @@
 // Compiles the C++ host API against the C-ABI library and runs the reference-shaped
 // calls.  Built and run by tests/test_cpp_host_api.py (GPU); compiled-only on CPU.
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -26,6 +27,11 @@ int main() {
     for (int i = 1; i < static_cast<int>(d.size()); ++i)
         if (d[i] < d[best]) best = i;
     auto proxy = batched_proxy(m, cloud, {mo, mo}, Precision::FP32_EXACT);
+    // the tensor-core precisions through the same call: fp16 within its frozen bound of the exact
+    // path (tests/golden/fp16_bounds.json: fig2_3x256 0.0019), bf16 within its own (0.013)
+    const double mn16 = predict_min_distance(m, cloud, mo, Precision::FP16).first;
+    const double mnbf = predict_min_distance(m, cloud, mo, Precision::BF16).first;
+    const bool tc_ok = std::fabs(mn16 - mn) <= 0.0019 && std::fabs(mnbf - mn) <= 0.013;
     bool threw = false;
     try {
         predict_min_distance(m, {}, mo);
@@ -64,8 +70,10 @@ int main() {
                          mc.program().layers[0].act == 0 && mc.program().layers[3].residual == 1 && mn_c == mn &&
                          idx_c == idx;
     std::printf("min %.9g idx %d | forward argmin %d %.9g | proxy %.9g | empty-cloud error %d | multi %.9g %d | "
-                "checkpoint dof %d ok %d\n", mn, idx, best, static_cast<double>(d[best]), proxy(1), threw ? 1 : 0,
-                static_cast<double>(r.min[0]), multi_ok ? 1 : 0, mc.dof(), ckpt_ok ? 1 : 0);
-    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw && multi_ok && ckpt_ok) ? 0
-                                                                                                               : 1;
+                "checkpoint dof %d ok %d | fp16 %.9g bf16 %.9g ok %d\n", mn, idx, best, static_cast<double>(d[best]),
+                proxy(1), threw ? 1 : 0, static_cast<double>(r.min[0]), multi_ok ? 1 : 0, mc.dof(), ckpt_ok ? 1 : 0, mn16,
+                mnbf, tc_ok ? 1 : 0);
+    return (idx == best && mn == static_cast<double>(d[best]) && proxy(1) == mn && threw && multi_ok && ckpt_ok && tc_ok)
+               ? 0
+               : 1;
 }
