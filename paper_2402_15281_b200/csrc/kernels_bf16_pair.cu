@@ -113,12 +113,13 @@ __device__ __forceinline__ void write_axq(uint8_t* axq, uint32_t slab_bytes, uin
 // Epilogue of 32 columns of one row (the MMA already added bias and x-part).
 template <int N, int TM, class F>
 __device__ __forceinline__ void pair_epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                           uint8_t* A, const float* wo_s, float4& dot, bool& ovf) {
+                                           uint8_t* A, const float* wo_s, float4& dot) {
     // fp16 operands: an activation (or input) beyond the fp16 range is stored as an infinity, and
     // every accumulator of that row in the next layer is then inf or NaN — which the ReLU pack
-    // would turn into 0.  Two accumulators per 32-column chunk are tested; the row is reported
-    // as delta = -inf (see the output warp).
-    if (F::kHalf) ovf |= !(fabsf(v[0]) <= 3.0e38f) || !(fabsf(v[21]) <= 3.0e38f);
+    // would turn into 0.  Two accumulators per 32-column chunk are tested; a hit poisons the
+    // row's output dot (-inf, or NaN once the last layer adds to it), and the output warp
+    // reports any non-finite delta as -inf.
+    if (F::kHalf && (!(fabsf(v[0]) <= 3.0e38f) || !(fabsf(v[21]) <= 3.0e38f))) dot.x = -INFINITY;
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (!aff && !res && last) {  // plain last layer: straight-line ReLU + output dot (four partial sums)
@@ -520,7 +521,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
         for (int64_t k = 0;; ++k) {
             if (tile_at(k) >= a.n_tiles) break;
             float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
-            bool ovf = false;  // fp16 operands: this row left the fp16 range (pair_epi32)
             for (int l = 0; l < L; ++l) {
                 const LayerDev& ld = a.layer[l];
                 const bool last = (l == L - 1);
@@ -544,9 +544,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                         tmem_wait_tied2(ra, rb);
 #pragma unroll
                         for (int q = 0; q < NCH; q += 2) {
-                            pair_epi32<N, C::TM, F>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot, ovf);
+                            pair_epi32<N, C::TM, F>(ld, l, last, reinterpret_cast<float*>(ra), c0 + 32 * q, row, A, wo_s, dot);
                             if (q + 2 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32 * (q + 2)), ra);
-                            pair_epi32<N, C::TM, F>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot, ovf);
+                            pair_epi32<N, C::TM, F>(ld, l, last, reinterpret_cast<float*>(rb), c0 + 32 * (q + 1), row, A, wo_s, dot);
                             if (q + 3 < NCH) tmem_ld32_async(tb + static_cast<uint32_t>(tc0 + 32 * (q + 3)), rb);
                             if (q + 2 < NCH) tmem_wait_tied2(ra, rb);
                         }
@@ -567,8 +567,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairCfg<N, TMR>::THR
                 mbar_wait(&out_empty[b], oe_ph[b]);
                 oe_ph[b] ^= 1u;
             }
-            dotbuf[(b * C::PARTS + part) * C::TM + row] =
-                (F::kHalf && ovf) ? -INFINITY : (dot.x + dot.y) + (dot.z + dot.w);
+            dotbuf[(b * C::PARTS + part) * C::TM + row] = (dot.x + dot.y) + (dot.z + dot.w);
             __syncwarp();
             if (lane == 0) mbar_arrive(&out_full[b]);
             pe_o += prof_clock() - c3;

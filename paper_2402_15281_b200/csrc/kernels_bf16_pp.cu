@@ -77,10 +77,11 @@ __device__ __forceinline__ void write_ax(uint8_t* ax, uint32_t row, float z0, fl
 // (accumulated in four partial sums so the 128-column dot is not one dependent FMA chain).
 template <int TM, class F>
 __device__ __forceinline__ void epi32(const LayerDev& ld, int l, bool last, float* v, int c0, uint32_t row,
-                                      uint8_t* A, const float* wo_s, float4& dot, bool& ovf) {
+                                      uint8_t* A, const float* wo_s, float4& dot) {
     // fp16 operands: a value beyond the fp16 range is stored as an infinity and makes every
-    // accumulator of its row inf or NaN in the next layer (kernels_bf16_pair.cu: pair_epi32)
-    if (F::kHalf) ovf |= !(fabsf(v[0]) <= 3.0e38f) || !(fabsf(v[21]) <= 3.0e38f);
+    // accumulator of its row inf or NaN in the next layer; a hit poisons the row's output dot
+    // (kernels_bf16_pair.cu: pair_epi32)
+    if (F::kHalf && (!(fabsf(v[0]) <= 3.0e38f) || !(fabsf(v[21]) <= 3.0e38f))) dot.x = -INFINITY;
     const int fl = ld.flags;
     const bool act = fl & kAct, aff = fl & kAffine, res = (l > 0) && (fl & kResidual);
     if (!aff && !res && last) {
@@ -420,7 +421,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
             if (lane == 0) mbar_arrive_remote(a_ready0 + s * 8u);
         }
         float4 dot[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
-        bool ovf[2] = {false, false};  // fp16 operands: the slot's row left the fp16 range
         unsigned long long pe_d = 0, pe_w = 0, pe_a = 0, pe_o = 0;
         for (int64_t j = 0; j < R; ++j) {
             const int nslots = has(j, 1) ? 2 : 1;
@@ -449,7 +449,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             uint32_t(&cur)[32] = (q & 1) ? rb : ra;
                             uint32_t(&nxt)[32] = (q & 1) ? ra : rb;
                             if (q + 1 < NCH) tmem_ld32_async(tbase + static_cast<uint32_t>(c0c + 32 * (q + 1)), nxt);
-                            epi32<TM, F>(ld, l, last, reinterpret_cast<float*>(cur), cq + c0c + 32 * q, row, A, wo_s, dot[s], ovf[s]);
+                            epi32<TM, F>(ld, l, last, reinterpret_cast<float*>(cur), cq + c0c + 32 * q, row, A, wo_s, dot[s]);
                             if (q + 1 < NCH) tmem_wait_tied(nxt);
                         }
                     }
@@ -469,10 +469,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pp::THREADS, 1)
                             mbar_wait(&out_empty[s], oe_ph[s]);
                             oe_ph[s] ^= 1u;
                         }
-                        dotbuf[(s * PARTS + part) * TM + row] =
-                            (F::kHalf && ovf[s]) ? -INFINITY : (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
+                        dotbuf[(s * PARTS + part) * TM + row] = (dot[s].x + dot[s].y) + (dot[s].z + dot[s].w);
                         dot[s] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        ovf[s] = false;
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&out_full[s]);
                     }
