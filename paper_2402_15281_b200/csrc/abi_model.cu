@@ -365,154 +365,155 @@ SVN_API svn_status svn_model_create(const svn_model_desc* d, const float* params
             // parameter fits its range, fp16 (precision fp16: same kernels and instruction rate,
             // 11 significant bits instead of 8).  Elements are written as raw 16-bit patterns.
             auto build16 = [&](FusedArgs& a, bool half) -> svn_status {
-            auto cvt16 = [half](float x) -> uint16_t {
-                return half ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
-            };
-            auto split16 = [half](float x, uint16_t& hi, uint16_t& lo) {
-                if (half) {
-                    const __half h = __float2half_rn(x);
-                    hi = __half_as_ushort(h);
-                    lo = __half_as_ushort(__float2half_rn(x - __half2float(h)));
-                } else {
-                    __nv_bfloat16 h, l;
-                    split_bf16_host(x, h, l);
-                    hi = __bfloat16_as_ushort(h);
-                    lo = __bfloat16_as_ushort(l);
+                auto cvt16 = [half](float x) -> uint16_t {
+                    return half ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
+                };
+                auto split16 = [half](float x, uint16_t& hi, uint16_t& lo) {
+                    if (half) {
+                        const __half h = __float2half_rn(x);
+                        hi = __half_as_ushort(h);
+                        lo = __half_as_ushort(__float2half_rn(x - __half2float(h)));
+                    } else {
+                        __nv_bfloat16 h, l;
+                        split_bf16_host(x, h, l);
+                        hi = __bfloat16_as_ushort(h);
+                        lo = __bfloat16_as_ushort(l);
+                    }
+                };
+                svn_status st = SVN_OK;
+                const int NH = N / 2, KSL = NH / 64;
+                const size_t chunk_elems = static_cast<size_t>(NH) * 64;
+                std::vector<uint16_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * N * N);
+                const float* Wl = pbf.data() + 2 * in;
+                size_t pos = 0;
+                for (int l = 0; l < L; ++l) {
+                    const int K = layer_k(d->layers, l, N, in);
+                    if (l > 0 && N == 256) {
+                        // ping-pong kernel (width 256): per layer 4 K slabs, each [CTA r: 128 rows] x 64 k
+                        for (int ks = 0; ks < N / 64; ++ks)
+                            for (int r = 0; r < 2; ++r) {
+                                uint8_t* blob = reinterpret_cast<uint8_t*>(ws.data() + pos);
+                                for (int nr = 0; nr < 128; ++nr)
+                                    for (int kc = 0; kc < 64; ++kc) {
+                                        const int n = r * 128 + nr, k = ks * 64 + kc;
+                                        *reinterpret_cast<uint16_t*>(blob + sw128_offset(nr, kc, 128)) =
+                                            cvt16(Wl[static_cast<int64_t>(k) * N + n]);
+                                    }
+                                pos += 128 * 64;
+                            }
+                    } else if (l > 0) {
+                        for (int step = 0; step < 4; ++step) {
+                            const int nh = step & 1, kh = step >> 1;
+                            for (int ks = 0; ks < KSL; ++ks) {
+                                uint8_t* chunk = reinterpret_cast<uint8_t*>(ws.data() + pos);
+                                for (int nr = 0; nr < NH; ++nr)
+                                    for (int kc = 0; kc < 64; ++kc) {
+                                        const int n = nh * NH + nr, k = (kh * KSL + ks) * 64 + kc;
+                                        const float w = Wl[static_cast<int64_t>(k) * N + n];
+                                        *reinterpret_cast<uint16_t*>(chunk + sw128_offset(nr, kc, NH)) = cvt16(w);
+                                    }
+                                pos += chunk_elems;
+                            }
+                        }
+                    }
+                    Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
                 }
-            };
-            svn_status st = SVN_OK;
-            const int NH = N / 2, KSL = NH / 64;
-            const size_t chunk_elems = static_cast<size_t>(NH) * 64;
-            std::vector<uint16_t> ws(static_cast<size_t>(L > 1 ? L - 1 : 1) * N * N);
-            const float* Wl = pbf.data() + 2 * in;
-            size_t pos = 0;
-            for (int l = 0; l < L; ++l) {
-                const int K = layer_k(d->layers, l, N, in);
-                if (l > 0 && N == 256) {
-                    // ping-pong kernel (width 256): per layer 4 K slabs, each [CTA r: 128 rows] x 64 k
-                    for (int ks = 0; ks < N / 64; ++ks)
-                        for (int r = 0; r < 2; ++r) {
-                            uint8_t* blob = reinterpret_cast<uint8_t*>(ws.data() + pos);
-                            for (int nr = 0; nr < 128; ++nr)
-                                for (int kc = 0; kc < 64; ++kc) {
-                                    const int n = r * 128 + nr, k = ks * 64 + kc;
-                                    *reinterpret_cast<uint16_t*>(blob + sw128_offset(nr, kc, 128)) =
-                                        cvt16(Wl[static_cast<int64_t>(k) * N + n]);
-                                }
-                            pos += 128 * 64;
+                uint16_t* dws = nullptr;
+                if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return st;
+                a.wstream = dws;
+                // CTA-pair kernel: TMA views of the weight stream and of the model-constant
+                // K=16 extension rows (bias hi/lo of non-concat layers with a nonzero bias).
+                const int BR = N == 256 ? N / 2 : N / 4;  // B rows per CTA per TMA box (128 for both kernels)
+                if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return st;
+                std::vector<uint8_t> xm;
+                const float* Wb = pbf.data() + 2 * in;
+                const bool fill_k0 = wq_bf.empty() && mbbase_bf.empty();  // first pass only
+                for (int l = 0; l < L; ++l) {
+                    const int K = layer_k(d->layers, l, N, in);
+                    const float* Wfull = Wb;
+                    const float* b = Wb + static_cast<int64_t>(N) * K;
+                    LayerDev& ld = a.layer[l];
+                    ld.ext = 0;
+                    ld.ext_row = 0;
+                    bool bias_zero = true;
+                    for (int n = 0; n < N; ++n)
+                        if (b[n] != 0.0f) bias_zero = false;
+                    if (ld.mb_slot >= 0) {
+                        ld.ext = 2;
+                        const int xoff = (l == 0) ? 0 : N;
+                        if (fill_k0) {
+                            wq_bf.insert(wq_bf.end(), Wfull + static_cast<int64_t>(xoff + 3) * N,
+                                         Wfull + static_cast<int64_t>(xoff + 3 + nq) * N);
+                            wx_bf.insert(wx_bf.end(), Wfull + static_cast<int64_t>(xoff) * N,
+                                         Wfull + static_cast<int64_t>(xoff + 3) * N);
+                            mbbase_bf.insert(mbbase_bf.end(), b, b + N);
                         }
-                } else if (l > 0) {
-                    for (int step = 0; step < 4; ++step) {
-                        const int nh = step & 1, kh = step >> 1;
-                        for (int ks = 0; ks < KSL; ++ks) {
-                            uint8_t* chunk = reinterpret_cast<uint8_t*>(ws.data() + pos);
-                            for (int nr = 0; nr < NH; ++nr)
-                                for (int kc = 0; kc < 64; ++kc) {
-                                    const int n = nh * NH + nr, k = (kh * KSL + ks) * 64 + kc;
-                                    const float w = Wl[static_cast<int64_t>(k) * N + n];
-                                    *reinterpret_cast<uint16_t*>(chunk + sw128_offset(nr, kc, NH)) = cvt16(w);
-                                }
-                            pos += chunk_elems;
+                    } else if (!bias_zero) {
+                        ld.ext = 1;
+                        ld.ext_row = static_cast<int64_t>(xm.size() / 32);
+                        const size_t base = xm.size();
+                        xm.resize(base + static_cast<size_t>(N) * 32, 0);
+                        for (int n = 0; n < N; ++n) {
+                            int blob_i, rr;
+                            if (N == 256) {  // ping-pong layout: blobs [r] of N/2 rows
+                                blob_i = n / BR;
+                                rr = n % BR;
+                            } else {         // pair layout: blobs [n-half][r] of N/4 rows
+                                const int nh = n / (N / 2), wi = n % (N / 2);
+                                blob_i = nh * 2 + wi / BR;
+                                rr = wi % BR;
+                            }
+                            uint8_t* blob = xm.data() + base + static_cast<size_t>(blob_i * BR) * 32;
+                            uint16_t hi, lo;
+                            split16(b[n], hi, lo);
+                            *reinterpret_cast<uint16_t*>(blob + ext_offset(rr, 0)) = hi;
+                            *reinterpret_cast<uint16_t*>(blob + ext_offset(rr, 1)) = lo;
                         }
                     }
+                    Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
                 }
-                Wl += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
-            }
-            uint16_t* dws = nullptr;
-            if ((st = m->upload(ws.data(), ws.size(), &dws)) != SVN_OK) return st;
-            a.wstream = dws;
-            // CTA-pair kernel: TMA views of the weight stream and of the model-constant
-            // K=16 extension rows (bias hi/lo of non-concat layers with a nonzero bias).
-            const int BR = N == 256 ? N / 2 : N / 4;  // B rows per CTA per TMA box (128 for both kernels)
-            if ((st = encode_blob_map(&a.tmap_w, dws, 128, ws.size() * 2 / 128, BR)) != SVN_OK) return st;
-            std::vector<uint8_t> xm;
-            const float* Wb = pbf.data() + 2 * in;
-            const bool fill_k0 = wq_bf.empty() && mbbase_bf.empty();  // first pass only
-            for (int l = 0; l < L; ++l) {
-                const int K = layer_k(d->layers, l, N, in);
-                const float* Wfull = Wb;
-                const float* b = Wb + static_cast<int64_t>(N) * K;
-                LayerDev& ld = a.layer[l];
-                ld.ext = 0;
-                ld.ext_row = 0;
-                bool bias_zero = true;
-                for (int n = 0; n < N; ++n)
-                    if (b[n] != 0.0f) bias_zero = false;
-                if (ld.mb_slot >= 0) {
-                    ld.ext = 2;
-                    const int xoff = (l == 0) ? 0 : N;
-                    if (fill_k0) {
-                    wq_bf.insert(wq_bf.end(), Wfull + static_cast<int64_t>(xoff + 3) * N,
-                                 Wfull + static_cast<int64_t>(xoff + 3 + nq) * N);
-                    wx_bf.insert(wx_bf.end(), Wfull + static_cast<int64_t>(xoff) * N, Wfull + static_cast<int64_t>(xoff + 3) * N);
-                    mbbase_bf.insert(mbbase_bf.end(), b, b + N);
-                    }
-                } else if (!bias_zero) {
-                    ld.ext = 1;
-                    ld.ext_row = static_cast<int64_t>(xm.size() / 32);
-                    const size_t base = xm.size();
-                    xm.resize(base + static_cast<size_t>(N) * 32, 0);
-                    for (int n = 0; n < N; ++n) {
-                        int blob_i, rr;
-                        if (N == 256) {  // ping-pong layout: blobs [r] of N/2 rows
-                            blob_i = n / BR;
-                            rr = n % BR;
-                        } else {         // pair layout: blobs [n-half][r] of N/4 rows
-                            const int nh = n / (N / 2), wi = n % (N / 2);
-                            blob_i = nh * 2 + wi / BR;
-                            rr = wi % BR;
+                if (xm.empty()) xm.resize(static_cast<size_t>(BR) * 32, 0);
+                uint8_t* dxm = nullptr;
+                if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return st;
+                if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return st;
+                if (N == 512 && !wq_bf.empty()) {
+                    // rows of mixed motions (forward_eval batches whose rows all differ in q): per
+                    // (concat slot, n-half, CTA half r) four K=16 slabs of BR rows — [b hi, b lo, W_x
+                    // splits] as in motion_ext_kernel but with the model bias, then W_q in (hi, lo, hi)
+                    // triples matching the per-row A slabs (z_q hi, z_q hi, z_q lo) of the kernel
+                    const int NH = N / 2, n_slots = static_cast<int>(mbbase_bf.size() / N);
+                    std::vector<uint8_t> mix(static_cast<size_t>(n_slots) * 2 * 2 * 4 * BR * 32, 0);
+                    for (int sl = 0; sl < n_slots; ++sl)
+                        for (int n = 0; n < N; ++n) {
+                            const int nh = n / NH, wi = n % NH, r = wi / BR, rr = wi % BR;
+                            uint8_t* blob = mix.data() + static_cast<size_t>(((sl * 2 + nh) * 2 + r) * 4) * BR * 32;
+                            auto put = [&](int sub, int k, uint16_t v) {
+                                *reinterpret_cast<uint16_t*>(blob + sub * BR * 32 + ext_offset(rr, k)) = v;
+                            };
+                            uint16_t hi, lo;
+                            split16(mbbase_bf[static_cast<size_t>(sl) * N + n], hi, lo);
+                            put(0, 0, hi);
+                            put(0, 1, lo);
+                            for (int c = 0; c < 3; ++c) {
+                                split16(wx_bf[(static_cast<size_t>(sl) * 3 + c) * N + n], hi, lo);
+                                put(0, 2 + 3 * c, hi);
+                                put(0, 3 + 3 * c, lo);
+                                put(0, 4 + 3 * c, hi);
+                            }
+                            for (int k = 0; k < nq; ++k) {
+                                split16(wq_bf[(static_cast<size_t>(sl) * nq + k) * N + n], hi, lo);
+                                const int q0 = 3 * k;
+                                put(1 + q0 / 16, q0 % 16, hi);
+                                put(1 + (q0 + 1) / 16, (q0 + 1) % 16, lo);
+                                put(1 + (q0 + 2) / 16, (q0 + 2) % 16, hi);
+                            }
                         }
-                        uint8_t* blob = xm.data() + base + static_cast<size_t>(blob_i * BR) * 32;
-                        uint16_t hi, lo;
-                        split16(b[n], hi, lo);
-                        *reinterpret_cast<uint16_t*>(blob + ext_offset(rr, 0)) = hi;
-                        *reinterpret_cast<uint16_t*>(blob + ext_offset(rr, 1)) = lo;
-                    }
+                    uint8_t* dmix = nullptr;
+                    if ((st = m->upload(mix.data(), mix.size(), &dmix)) != SVN_OK) return st;
+                    if ((st = encode_blob_map(&a.tmap_xmix, dmix, 128, mix.size() / 128, 128)) != SVN_OK) return st;
+                    m->has_mixed = 3 * nq <= 48;
                 }
-                Wb += static_cast<int64_t>(N) * K + N + (d->layers[l].affine ? 4 * N : 0);
-            }
-            if (xm.empty()) xm.resize(static_cast<size_t>(BR) * 32, 0);
-            uint8_t* dxm = nullptr;
-            if ((st = m->upload(xm.data(), xm.size(), &dxm)) != SVN_OK) return st;
-            if ((st = encode_blob_map(&a.tmap_xm, dxm, 32, xm.size() / 32, BR)) != SVN_OK) return st;
-            if (N == 512 && !wq_bf.empty()) {
-                // rows of mixed motions (forward_eval batches whose rows all differ in q): per
-                // (concat slot, n-half, CTA half r) four K=16 slabs of BR rows — [b hi, b lo, W_x
-                // splits] as in motion_ext_kernel but with the model bias, then W_q in (hi, lo, hi)
-                // triples matching the per-row A slabs (z_q hi, z_q hi, z_q lo) of the kernel
-                const int NH = N / 2, n_slots = static_cast<int>(mbbase_bf.size() / N);
-                std::vector<uint8_t> mix(static_cast<size_t>(n_slots) * 2 * 2 * 4 * BR * 32, 0);
-                for (int sl = 0; sl < n_slots; ++sl)
-                    for (int n = 0; n < N; ++n) {
-                        const int nh = n / NH, wi = n % NH, r = wi / BR, rr = wi % BR;
-                        uint8_t* blob = mix.data() + static_cast<size_t>(((sl * 2 + nh) * 2 + r) * 4) * BR * 32;
-                        auto put = [&](int sub, int k, uint16_t v) {
-                            *reinterpret_cast<uint16_t*>(blob + sub * BR * 32 + ext_offset(rr, k)) = v;
-                        };
-                        uint16_t hi, lo;
-                        split16(mbbase_bf[static_cast<size_t>(sl) * N + n], hi, lo);
-                        put(0, 0, hi);
-                        put(0, 1, lo);
-                        for (int c = 0; c < 3; ++c) {
-                            split16(wx_bf[(static_cast<size_t>(sl) * 3 + c) * N + n], hi, lo);
-                            put(0, 2 + 3 * c, hi);
-                            put(0, 3 + 3 * c, lo);
-                            put(0, 4 + 3 * c, hi);
-                        }
-                        for (int k = 0; k < nq; ++k) {
-                            split16(wq_bf[(static_cast<size_t>(sl) * nq + k) * N + n], hi, lo);
-                            const int q0 = 3 * k;
-                            put(1 + q0 / 16, q0 % 16, hi);
-                            put(1 + (q0 + 1) / 16, (q0 + 1) % 16, lo);
-                            put(1 + (q0 + 2) / 16, (q0 + 2) % 16, hi);
-                        }
-                    }
-                uint8_t* dmix = nullptr;
-                if ((st = m->upload(mix.data(), mix.size(), &dmix)) != SVN_OK) return st;
-                if ((st = encode_blob_map(&a.tmap_xmix, dmix, 128, mix.size() / 128, 128)) != SVN_OK) return st;
-                m->has_mixed = 3 * nq <= 48;
-            }
-            return SVN_OK;
+                return SVN_OK;
             };  // build16
             if ((st = build16(a, false)) != SVN_OK) return cleanup_fail(st);
             if ((st = m->upload(wq_bf.data(), wq_bf.size(), &m->d_wq_bf)) != SVN_OK) return cleanup_fail(st);
