@@ -89,7 +89,9 @@ class Model:
                   per_point: bool = False) -> QueryResult:
         """Every (point x motion) pair -> per-motion min, argmin, `min > margin`.
         points float [P, 3]; q01 float [M, 2*dof] = (q0 | q1).
-        precision: "bf16" (tcgen05, per-network stated bound), "fp32" / "fp32_exact" (the FP32
+        precision: "bf16" (tcgen05, per-network stated bound), "fp16" (the same kernels on fp16
+        operands: ~9x tighter bound at ~0.95x the throughput; rows leaving the fp16 range are
+        reported as -inf), "fp32" / "fp32_exact" (the FP32
         path: FFMA in the reference's order, bit-identical to the oracle), "fp32_split"
         (width 256/512: fp32-grade split-fp16 on tcgen05; 1e-5 at width 256, a stated bound at
         width 512)."""
