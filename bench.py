@@ -458,7 +458,9 @@ def main():
     if not args.no_e2e and mode == "motion":
         hp = torch.from_numpy(pts_np).pin_memory().numpy()
         hq = torch.from_numpy(q_np).pin_memory().numpy()
-        model.query_min(hp, hq[: min(M, 8)], w.margin, precision=prec)  # warm the host path (staging)
+        # warm the host path (staging block, scratch arena sized by the previous call): the full batch
+        # when a step is short, a few motions of it when a step takes seconds
+        model.query_min(hp, hq if ms < 100 else hq[: min(M, 8)], w.margin, precision=prec)
         n_e = 1 if ms > 2000 else max(1, min(args.steps, 3))
         if world > 1:
             dist.barrier()
