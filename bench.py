@@ -523,6 +523,20 @@ def main():
         gc = cm.query_min(pts_np, q_np[:nm], w.margin, precision=prec)
         parity["calibrated_output_bias"] = class_compare(gc.min, gc.free, gc.argmin, rc.min, rc.free, rc.argmin,
                                                          w.margin, bnd)
+        if prec in ("bf16", "fp16") and bounds_for(w.program.name, "fp32_split"):
+            # the exact-for-every-motion classification on the same calibrated case: this precision
+            # for the batch, fp32_split / the FP32 path for the motions near the margin
+            # (svn_query_min_cascade); class mismatches against the FP32 path must be 0
+            t0 = time.perf_counter()
+            cr, st = cm.query_min_cascade(pts_np, q_np[:nm], w.margin, bnd, bounds_for(w.program.name, "fp32_split"),
+                                          coarse=prec)
+            t_c = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            cm.query_min(pts_np, q_np[:nm], w.margin, precision=prec)
+            t_p = time.perf_counter() - t0
+            parity["cascade_on_calibrated"] = {"motions": nm, "stage_motions": list(st),
+                                               "class_mismatches": int((cr.free != rc.free).sum()),
+                                               "ms": t_c * 1e3, "ms_coarse_alone": t_p * 1e3}
         cm.close()
 
     if rank == 0:

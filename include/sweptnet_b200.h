@@ -166,6 +166,22 @@ SVN_API svn_status svn_query_min(const svn_model* model, svn_precision prec, con
                                  const float* q01, int64_t M, double margin, float* min_out,
                                  int32_t* argmin_out, uint8_t* free_out, float* per_point);
 
+/* svn_query_min with a margin classification that is exact for EVERY motion (new; the
+ * classification step of collision.cpp:68 / bench.cpp:108): the batch runs on `coarse` (a
+ * tensor-core precision: FP16 or BF16); the motions whose min lies within band_coarse of the
+ * margin — the precision's stated bound, tests/golden/{fp16,bf16}_bounds.json — or is not finite
+ * (FP16's range report) run again on FP32_SPLIT (when the model has it), and those still within
+ * band_split of the margin on the FP32 path, whose min, argmin and class are the reference's bit
+ * for bit.  Outside the bands the coarse class already equals the reference's, so free_out equals
+ * the FP32 path's for all M motions, at the coarse path's cost plus the few re-evaluated
+ * motions.  min_out / argmin_out hold the finest stage evaluated per motion.  stage_motions
+ * (int64 [3], or NULL) receives the motions evaluated per stage {coarse, FP32_SPLIT, FP32}.
+ * HOST buffers, synchronous. */
+SVN_API svn_status svn_query_min_cascade(const svn_model* model, svn_precision coarse, double band_coarse,
+                                         double band_split, const float* points, int64_t P, const float* q01,
+                                         int64_t M, double margin, float* min_out, int32_t* argmin_out,
+                                         uint8_t* free_out, int64_t* stage_motions);
+
 /* Point-sharded partial (device pointers): folds min over this shard's points
  * into keys[M] with atomicMin.  key = (orderable(delta) << 32) | (index_offset + p);
  * the caller initialises keys to UINT64_MAX (svn_keys_init_device) and reduces

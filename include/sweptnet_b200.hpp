@@ -176,6 +176,30 @@ inline std::function<double(int)> batched_proxy(const Model& m, const std::vecto
     return [mins](int j) { return static_cast<double>((*mins)[static_cast<size_t>(j)]); };
 }
 
+// The classification step of the callers (collision.cpp:68, bench.cpp:108) for a batch of motions,
+// exact for every motion (svn_query_min_cascade): `coarse` (FP16 or BF16) for the batch, FP32_SPLIT
+// for the motions within band_coarse of the margin, the FP32 path for those within band_split.
+struct CascadeResult {
+    std::vector<float> min;
+    std::vector<int32_t> argmin;
+    std::vector<uint8_t> free;   // == the reference's double(min) > margin, motion by motion
+    int64_t stage_motions[3];    // motions evaluated on {coarse, FP32_SPLIT, FP32}
+};
+inline CascadeResult classify_motions(const Model& m, const std::vector<float>& points_xyz,
+                                      const std::vector<float>& q01, double margin, double band_coarse,
+                                      double band_split, Precision coarse = Precision::FP16) {
+    const int64_t P = static_cast<int64_t>(points_xyz.size() / 3);
+    const int64_t M = m.dof() > 0 ? static_cast<int64_t>(q01.size()) / (2 * m.dof()) : 0;
+    CascadeResult r;
+    r.min.resize(static_cast<size_t>(M));
+    r.argmin.resize(static_cast<size_t>(M));
+    r.free.resize(static_cast<size_t>(M));
+    check(svn_query_min_cascade(m.handle(), static_cast<svn_precision>(coarse), band_coarse, band_split,
+                                points_xyz.data(), P, q01.data(), M, margin, r.min.data(), r.argmin.data(),
+                                r.free.data(), r.stage_motions));
+    return r;
+}
+
 // Several GPUs of this box from one process (svn_multi_*): one model copy and one worker
 // thread per device.  query_min shards motions (no communication) or, for batches with
 // fewer motions than devices, points (one NCCL u64 MIN all-reduce); bit-identical to Model.

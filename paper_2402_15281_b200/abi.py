@@ -106,6 +106,7 @@ def _finish(L):
         "svn_model_get_program": (C.c_int, [VP, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), P, I32]),
         "svn_query_min_device": (C.c_int, [VP, C.c_int, P, I64, P, I64, D, P, P, P, P, VP]),
         "svn_query_min": (C.c_int, [VP, C.c_int, P, I64, P, I64, D, P, P, P, P]),
+        "svn_query_min_cascade": (C.c_int, [VP, C.c_int, D, D, P, I64, P, I64, D, P, P, P, P]),
         "svn_keys_init_device": (C.c_int, [P, I64, VP]),
         "svn_query_min_keys_device": (C.c_int, [VP, C.c_int, P, I64, I64, P, I64, P, VP]),
         "svn_keys_finalize_device": (C.c_int, [P, I64, D, P, P, P, VP]),
@@ -139,7 +140,7 @@ def _finish(L):
 
 EXPORTED = ("svn_param_count", "svn_trainable_param_count", "svn_init_params", "svn_model_create",
             "svn_model_load_checkpoint", "svn_model_destroy", "svn_model_get_program", "svn_query_min_device", "svn_query_min",
-            "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
+            "svn_query_min_cascade", "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
             "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_gcc_min_distance",
             "svn_gcc_min_distance_device", "svn_gcc_nn_search", "svn_multi_create", "svn_multi_destroy",
             "svn_multi_device_count", "svn_query_min_multi", "svn_launch_count",

@@ -106,6 +106,23 @@ class Model:
                                           float(margin), abi.ptr(mn), abi.ptr(am), abi.ptr(fr), abi.ptr(pp)))
         return QueryResult(mn, am, fr.astype(bool), pp)
 
+    def query_min_cascade(self, points: np.ndarray, q01: np.ndarray, margin: float, band_coarse: float,
+                          band_split: float, coarse: str = "fp16") -> tuple[QueryResult, tuple[int, int, int]]:
+        """query_min whose class `free` equals the FP32 path's (the reference's, collision.cpp:68)
+        for EVERY motion: the batch on `coarse` ("fp16" | "bf16"), the motions within band_coarse
+        of the margin (the precision's stated bound) or not finite again on fp32_split, those
+        within band_split of it on the FP32 path.  Returns the result (min/argmin of the finest
+        stage evaluated per motion) and the motions evaluated per stage."""
+        pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+        q = np.ascontiguousarray(q01, dtype=np.float32).reshape(-1, 2 * self.program.dof)
+        P, M = pts.shape[0], q.shape[0]
+        mn, am, fr = np.empty(M, np.float32), np.empty(M, np.int32), np.empty(M, np.uint8)
+        stages = np.zeros(3, np.int64)
+        abi.check(abi.lib().svn_query_min_cascade(self._h, abi.PRECISIONS[coarse], float(band_coarse),
+                                                  float(band_split), abi.ptr(pts), P, abi.ptr(q), M, float(margin),
+                                                  abi.ptr(mn), abi.ptr(am), abi.ptr(fr), abi.ptr(stages)))
+        return QueryResult(mn, am, fr.astype(bool)), (int(stages[0]), int(stages[1]), int(stages[2]))
+
     def forward_eval(self, raw: np.ndarray, precision: str = "fp32_exact") -> np.ndarray:
         """forward_eval<float> (nn.cpp:95-130): raw [B, 3 + 2*dof] rows [x, q0, q1]."""
         raw = np.ascontiguousarray(raw, dtype=np.float32)

@@ -797,6 +797,68 @@ SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const f
     }
 }
 
+// Margin classification that is exact for every motion at close to the coarse path's cost: the
+// whole batch on a fast tensor-core precision, then only the motions whose min lies within that
+// precision's stated band of the margin (or is not finite: an fp16 range report) again on
+// fp32_split, and what is still within fp32_split's band of the margin on the FP32 path, whose
+// class is the reference's bit for bit (collision.cpp:68 on nn.cpp:460-480's result).
+SVN_API svn_status svn_query_min_cascade(const svn_model* m, svn_precision coarse, double band_coarse,
+                                         double band_split, const float* points, int64_t P, const float* q01,
+                                         int64_t M, double margin, float* min_out, int32_t* argmin_out,
+                                         uint8_t* free_out, int64_t* stage_motions) {
+    try {
+        if (!m) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+        if (!(band_coarse >= 0.0) || !(band_split >= 0.0))
+            return fail(SVN_ERR_INVALID_ARGUMENT, "cascade: bands must be non-negative");
+        if (kernel_kind(m, coarse) == Kind::SIMT)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "cascade: the coarse stage must be a tensor-core precision");
+        svn_status s = svn_query_min(m, coarse, points, P, q01, M, margin, min_out, argmin_out, free_out, nullptr);
+        if (s != SVN_OK) return s;
+        if (stage_motions) stage_motions[0] = M, stage_motions[1] = 0, stage_motions[2] = 0;
+        const int nq = 2 * m->dof;
+        std::vector<int64_t> idx;
+        auto near_margin = [&](int64_t i, double band) {
+            const double v = static_cast<double>(min_out[i]);
+            return !std::isfinite(v) || std::fabs(v - margin) <= band;  // NaN / -inf: a range report, look again
+        };
+        for (int64_t i = 0; i < M; ++i)
+            if (near_margin(i, band_coarse)) idx.push_back(i);
+        // one finer stage over the motions in idx, results scattered back
+        auto refine = [&](svn_precision prec) -> svn_status {
+            const int64_t n = static_cast<int64_t>(idx.size());
+            std::vector<float> q(static_cast<size_t>(n) * nq), mn(static_cast<size_t>(n));
+            std::vector<int32_t> am(static_cast<size_t>(n));
+            std::vector<uint8_t> fr(static_cast<size_t>(n));
+            for (int64_t k = 0; k < n; ++k)
+                std::memcpy(q.data() + k * nq, q01 + idx[static_cast<size_t>(k)] * nq, sizeof(float) * nq);
+            const svn_status r = svn_query_min(m, prec, points, P, q.data(), n, margin, mn.data(), am.data(), fr.data(), nullptr);
+            if (r != SVN_OK) return r;
+            for (int64_t k = 0; k < n; ++k) {
+                const int64_t i = idx[static_cast<size_t>(k)];
+                min_out[i] = mn[static_cast<size_t>(k)];
+                argmin_out[i] = am[static_cast<size_t>(k)];
+                free_out[i] = fr[static_cast<size_t>(k)];
+            }
+            return SVN_OK;
+        };
+        if (!idx.empty() && m->has_split && coarse != SVN_PREC_FP32_SPLIT) {
+            if ((s = refine(SVN_PREC_FP32_SPLIT)) != SVN_OK) return s;
+            if (stage_motions) stage_motions[1] = static_cast<int64_t>(idx.size());
+            std::vector<int64_t> rest;
+            for (int64_t i : idx)
+                if (near_margin(i, band_split)) rest.push_back(i);
+            idx.swap(rest);
+        }
+        if (!idx.empty()) {
+            if ((s = refine(SVN_PREC_FP32_EXACT)) != SVN_OK) return s;
+            if (stage_motions) stage_motions[2] = static_cast<int64_t>(idx.size());
+        }
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
+}
+
 SVN_API svn_status svn_forward_eval(const svn_model* m, svn_precision prec, const float* raw, int64_t B, int64_t cols,
                                     float* out) {
     try {
