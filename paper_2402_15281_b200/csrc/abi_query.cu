@@ -353,6 +353,37 @@ cudaStream_t thread_stream(int device) {
     return ts.s[device];
 }
 
+// A second stream per (thread, device) for the host->device copies of a large cloud, and a few
+// events to hand its chunks to the compute stream (query_min_host's pipelined path).
+struct ThreadCopy {
+    static constexpr int kEvents = 8;
+    cudaStream_t s[64] = {};
+    cudaEvent_t ev[64][kEvents] = {};
+    ~ThreadCopy() {
+        for (int d = 0; d < 64; ++d)
+            if (s[d]) {
+                int prev = 0;
+                cudaGetDevice(&prev);
+                cudaSetDevice(d);
+                for (cudaEvent_t e : ev[d])
+                    if (e) cudaEventDestroy(e);
+                cudaStreamDestroy(s[d]);
+                cudaSetDevice(prev);
+            }
+    }
+};
+
+ThreadCopy* thread_copy(int device) {
+    thread_local ThreadCopy tc;
+    if (device < 0 || device >= 64) return nullptr;
+    if (!tc.s[device]) {
+        if (cudaStreamCreateWithFlags(&tc.s[device], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        for (cudaEvent_t& e : tc.ev[device])
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    return &tc;
+}
+
 }  // namespace abi
 }  // namespace svn
 
@@ -673,9 +704,70 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
     if (g_trace_on) g_trace.start();
     const bool direct = pinned(points) && pinned(q01);
     SVN_TRACE(8);
+    Arena& arena = thread_arena(m->device);
+    // A large cloud (>= 2^21 points, 24 MB) given as float arrays: the points travel in chunks on a
+    // second stream while the compute stream folds the chunks already on the device into the
+    // per-motion keys (the point-sharding identity: atomicMin over (delta, index) keys, bit-identical
+    // to one launch) — pageable callers' staging copy, the H2D and the kernels overlap instead of
+    // running one after the other.  SVN_PIPELINE=0 turns it off (A/B hook).
+    static const bool pipeline_on = [] {
+        const char* e = std::getenv("SVN_PIPELINE");
+        return !(e && e[0] == '0');
+    }();
+    constexpr int64_t kChunkPoints = int64_t(1) << 20;
+    ThreadCopy* tc = nullptr;
+    if (pipeline_on && points && q01 && !per_point && P >= 2 * kChunkPoints && !g_timing && !prof_enabled())
+        tc = thread_copy(m->device);
+    if (tc) {
+        cudaStream_t cs = tc->s[m->device];
+        ArenaScope as(&arena);
+        Scratch sc(st);
+        unsigned long long* keys = nullptr;
+        SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&keys), sizeof(unsigned long long) * M), "cudaMallocAsync(keys)");
+        if (!direct) std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
+        SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, direct ? reinterpret_cast<const uint8_t*>(q01) : sg.host + o_q,
+                                 sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),
+                 "H2D motions");
+        SVN_CUDA(launch_keys_init(keys, M, st), "keys_init kernel");
+        ++g_launches;
+        int k = 0;
+        for (int64_t p0 = 0; p0 < P; p0 += kChunkPoints, ++k) {
+            const int64_t n = std::min(kChunkPoints, P - p0);
+            const size_t off = sizeof(float) * 3 * static_cast<size_t>(p0), bytes = sizeof(float) * 3 * static_cast<size_t>(n);
+            const uint8_t* src = reinterpret_cast<const uint8_t*>(points) + off;
+            if (!direct) {  // pageable: through the chunk's own part of the pinned block
+                std::memcpy(sg.host + off, src, bytes);
+                src = sg.host + off;
+            }
+            cudaEvent_t ev = tc->ev[m->device][k % ThreadCopy::kEvents];
+            SVN_CUDA(cudaMemcpyAsync(sg.dev + off, src, bytes, cudaMemcpyHostToDevice, cs), "H2D point chunk");
+            SVN_CUDA(cudaEventRecord(ev, cs), "cudaEventRecord");
+            SVN_CUDA(cudaStreamWaitEvent(st, ev, 0), "cudaStreamWaitEvent");
+            const svn_status s = query_dense(m, prec, reinterpret_cast<const float*>(sg.dev + off), n, p0,
+                                             reinterpret_cast<const float*>(sg.dev + o_q), M, margin, nullptr, nullptr,
+                                             nullptr, nullptr, reinterpret_cast<uint64_t*>(keys), st);
+            if (s != SVN_OK) {
+                cudaStreamSynchronize(cs);
+                cudaStreamSynchronize(st);
+                return s;
+            }
+        }
+        SVN_CUDA(launch_keys_finalize(keys, M, margin, reinterpret_cast<float*>(sg.dev + o_min),
+                                      reinterpret_cast<int32_t*>(sg.dev + o_arg), sg.dev + o_free, st),
+                 "keys_finalize kernel");
+        ++g_launches;
+        SVN_CUDA(cudaMemcpyAsync(sg.host + o_min, sg.dev + o_min, total - o_min, cudaMemcpyDeviceToHost, st),
+                 "D2H min/argmin/free");
+        SVN_CUDA(cudaStreamSynchronize(st), "query kernels");
+        SVN_CUDA(arena.grow_to_need(), "scratch arena");
+        std::memcpy(min_out, sg.host + o_min, sizeof(float) * M);
+        std::memcpy(argmin_out, sg.host + o_arg, sizeof(int32_t) * M);
+        std::memcpy(free_out, sg.host + o_free, M);
+        g_trace_on = false;
+        return SVN_OK;
+    }
     if (!direct) fill(reinterpret_cast<float*>(sg.host), reinterpret_cast<float*>(sg.host + o_q));
     SVN_TRACE(0);
-    Arena& arena = thread_arena(m->device);
     const bool small = !direct && !per_point && P <= kSmallStagingPoints && M <= 64 && small_staging_enabled();
     if (small && arena.cap > 0 && graphs_enabled() && !g_timing && !prof_enabled() &&
         small_graph(m, prec, P, M, margin, sg, arena, o_q, o_min, o_arg, o_free, st)) {

@@ -336,3 +336,29 @@ def test_small_calls_read_each_calls_inputs(prec):
             else:
                 assert abs(got[0] - ref[0]) <= tol
         del m
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_large_cloud_host_call_is_pipelined_and_bit_identical(prec):
+    """A cloud of >= 2^21 points given as host float arrays travels in 2^20-point chunks on a second
+    stream while the chunks already on the device are folded into the per-motion keys
+    (query_min_host); the result equals one launch over the device-resident cloud bit for bit,
+    for pageable and for pinned host arrays, including a ragged last chunk."""
+    import torch
+    w = WORKLOADS["c2"]
+    params = S.init_params(w.program, 12, w.bound)
+    P = (1 << 21) + 12345
+    pts, q = w.make(seed=12, motions=3, points=P)
+    model = S.Model(w.program, params)
+    dev = torch.device("cuda:0")
+    tp, tq = torch.from_numpy(pts).to(dev), torch.from_numpy(q).to(dev)
+    mn = torch.empty(3, dtype=torch.float32, device=dev)
+    am = torch.empty(3, dtype=torch.int32, device=dev)
+    fr = torch.empty(3, dtype=torch.uint8, device=dev)
+    model.query_min_device(tp, tq, w.margin, mn, am, fr, None, precision=prec)
+    torch.cuda.synchronize()
+    for hp, hq in ((pts, q), (torch.from_numpy(pts).pin_memory().numpy(), torch.from_numpy(q).pin_memory().numpy())):
+        for _ in range(2):  # the second call reuses the staging block and the grown scratch arena
+            r = model.query_min(hp, hq, w.margin, precision=prec)
+            assert np.array_equal(r.min, mn.cpu().numpy()) and np.array_equal(r.argmin, am.cpu().numpy())
+            assert np.array_equal(r.free, fr.cpu().numpy().astype(bool))
