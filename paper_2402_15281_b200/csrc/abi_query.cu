@@ -575,7 +575,8 @@ bool small_staging_enabled() {  // SVN_SMALL_STAGING=0: DMA copies for every cal
 }
 
 // svn_query_min / svn_predict_min_distance: inputs from host memory, outputs to host memory.
-// fill(pts, q) writes the call's float inputs into the pinned staging block; points/q01 are
+// fill(pts, q, p0, n) writes points p0..p0+n-1 (when pts != null) and the motions (when q != null)
+// as floats into the pinned staging block; points/q01 are
 // the caller's float arrays (null for predict_min_distance, whose double inputs are converted
 // by fill), sent to the device directly when they are already pinned.
 // Small staged calls as one CUDA graph (SVN_GRAPH=0 turns it off): the stage-in kernel, K0
@@ -705,7 +706,7 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
     const bool direct = pinned(points) && pinned(q01);
     SVN_TRACE(8);
     Arena& arena = thread_arena(m->device);
-    // A large cloud (>= 2^21 points, 24 MB) given as float arrays: the points travel in chunks on a
+    // A large cloud (>= 2^21 points, 24 MB): the points travel in chunks on a
     // second stream while the compute stream folds the chunks already on the device into the
     // per-motion keys (the point-sharding identity: atomicMin over (delta, index) keys, bit-identical
     // to one launch) — pageable callers' staging copy, the H2D and the kernels overlap instead of
@@ -714,9 +715,14 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         const char* e = std::getenv("SVN_PIPELINE");
         return !(e && e[0] == '0');
     }();
+    static const int fill_threads = [] {
+        const char* e = std::getenv("SVN_FILL_THREADS");
+        const int v = e ? std::atoi(e) : 4;
+        return v < 1 ? 1 : (v > 16 ? 16 : v);
+    }();
     constexpr int64_t kChunkPoints = int64_t(1) << 20;
     ThreadCopy* tc = nullptr;
-    if (pipeline_on && points && q01 && !per_point && P >= 2 * kChunkPoints && !g_timing && !prof_enabled())
+    if (pipeline_on && !per_point && P >= 2 * kChunkPoints && !g_timing && !prof_enabled())
         tc = thread_copy(m->device);
     if (tc) {
         cudaStream_t cs = tc->s[m->device];
@@ -724,7 +730,7 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         Scratch sc(st);
         unsigned long long* keys = nullptr;
         SVN_CUDA(sc.alloc(reinterpret_cast<void**>(&keys), sizeof(unsigned long long) * M), "cudaMallocAsync(keys)");
-        if (!direct) std::memcpy(sg.host + o_q, q01, sizeof(float) * nq * M);
+        if (!direct) fill(nullptr, reinterpret_cast<float*>(sg.host + o_q), 0, 0);
         SVN_CUDA(cudaMemcpyAsync(sg.dev + o_q, direct ? reinterpret_cast<const uint8_t*>(q01) : sg.host + o_q,
                                  sizeof(float) * nq * M, cudaMemcpyHostToDevice, st),
                  "H2D motions");
@@ -734,9 +740,25 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         for (int64_t p0 = 0; p0 < P; p0 += kChunkPoints, ++k) {
             const int64_t n = std::min(kChunkPoints, P - p0);
             const size_t off = sizeof(float) * 3 * static_cast<size_t>(p0), bytes = sizeof(float) * 3 * static_cast<size_t>(n);
-            const uint8_t* src = reinterpret_cast<const uint8_t*>(points) + off;
-            if (!direct) {  // pageable: through the chunk's own part of the pinned block
-                std::memcpy(sg.host + off, src, bytes);
+            const uint8_t* src = direct ? reinterpret_cast<const uint8_t*>(points) + off : nullptr;
+            if (!direct) {  // pageable floats or the reference's double cloud: through the chunk's own
+                // part of the pinned block, the copy / double->float cast of a chunk split over a
+                // few threads (SVN_FILL_THREADS, default 4: one thread casts 2^24 points in ~50 ms,
+                // longer than the GPU needs for them)
+                float* dst = reinterpret_cast<float*>(sg.host + off);
+                const int T = static_cast<int>(std::min<int64_t>(fill_threads, n / 65536 + 1));
+                if (T <= 1) {
+                    fill(dst, nullptr, p0, n);
+                } else {
+                    std::vector<std::thread> pool;
+                    const int64_t per = (n + T - 1) / T;
+                    for (int t = 1; t < T; ++t) {
+                        const int64_t a0 = std::min<int64_t>(n, t * per), a1 = std::min<int64_t>(n, (t + 1) * per);
+                        if (a1 > a0) pool.emplace_back([&, a0, a1] { fill(dst + 3 * a0, nullptr, p0 + a0, a1 - a0); });
+                    }
+                    fill(dst, nullptr, p0, std::min<int64_t>(n, per));
+                    for (std::thread& th : pool) th.join();
+                }
                 src = sg.host + off;
             }
             cudaEvent_t ev = tc->ev[m->device][k % ThreadCopy::kEvents];
@@ -766,7 +788,7 @@ svn_status query_min_host(const svn_model* m, svn_precision prec, int64_t P, int
         g_trace_on = false;
         return SVN_OK;
     }
-    if (!direct) fill(reinterpret_cast<float*>(sg.host), reinterpret_cast<float*>(sg.host + o_q));
+    if (!direct) fill(reinterpret_cast<float*>(sg.host), reinterpret_cast<float*>(sg.host + o_q), 0, P);
     SVN_TRACE(0);
     const bool small = !direct && !per_point && P <= kSmallStagingPoints && M <= 64 && small_staging_enabled();
     if (small && arena.cap > 0 && graphs_enabled() && !g_timing && !prof_enabled() &&
@@ -879,9 +901,9 @@ SVN_API svn_status svn_query_min(const svn_model* m, svn_precision prec, const f
         if (!points || !q01) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
         const int nq = m ? 2 * m->dof : 0;
         return query_min_host(m, prec, P, M, margin, points, q01,
-                              [&](float* hp, float* hq) {
-                                  std::memcpy(hp, points, sizeof(float) * 3 * P);
-                                  std::memcpy(hq, q01, sizeof(float) * nq * M);
+                              [&](float* hp, float* hq, int64_t p0, int64_t n) {
+                                  if (hp) std::memcpy(hp, points + 3 * p0, sizeof(float) * 3 * n);
+                                  if (hq) std::memcpy(hq, q01, sizeof(float) * nq * M);
                               },
                               min_out, argmin_out, free_out, per_point);
     } catch (...) {
@@ -1012,10 +1034,12 @@ SVN_API svn_status svn_predict_min_distance(const svn_model* m, svn_precision pr
         int32_t idx = 0;
         uint8_t fr = 0;
         svn_status s = query_min_host(m, prec, P, 1, 0.0, nullptr, nullptr,
-                                      [&](float* hp, float* hq) {
-                                          cvt_f64_f32(hp, cloud, 3 * P);
-                                          for (int i = 0; i < dof; ++i) hq[i] = static_cast<float>(q0[i]);
-                                          for (int i = 0; i < dof; ++i) hq[dof + i] = static_cast<float>(q1[i]);
+                                      [&](float* hp, float* hq, int64_t p0, int64_t n) {
+                                          if (hp) cvt_f64_f32(hp, cloud + 3 * p0, 3 * n);
+                                          if (hq) {
+                                              for (int i = 0; i < dof; ++i) hq[i] = static_cast<float>(q0[i]);
+                                              for (int i = 0; i < dof; ++i) hq[dof + i] = static_cast<float>(q1[i]);
+                                          }
                                       },
                                       &mn, &idx, &fr, nullptr);
         if (s != SVN_OK) return s;

@@ -362,3 +362,8 @@ def test_large_cloud_host_call_is_pipelined_and_bit_identical(prec):
             r = model.query_min(hp, hq, w.margin, precision=prec)
             assert np.array_equal(r.min, mn.cpu().numpy()) and np.array_equal(r.argmin, am.cpu().numpy())
             assert np.array_equal(r.free, fr.cpu().numpy().astype(bool))
+    # the reference's own entry point (double cloud, one motion): its conversion runs chunk by chunk too
+    dof = w.program.dof
+    d, i = model.predict_min_distance(pts.astype(np.float64), q[1, :dof].astype(np.float64),
+                                      q[1, dof:].astype(np.float64), precision=prec)
+    assert d == float(mn[1].item()) and i == int(am[1].item())
