@@ -95,6 +95,8 @@ def depth_scan_cloud(rng, n, n_ell=20) -> np.ndarray:
     parts.append(plane)
     for e in range(n_ell):
         k = int(counts[e + 1])
+        if k == 0:  # a cloud of a few points: this ellipsoid drew none
+            continue
         got = []
         a, b, c = axes[e]
         wmax = max(b * c, a * c, a * b)
