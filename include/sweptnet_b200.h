@@ -287,13 +287,20 @@ SVN_API svn_status svn_gcc_nn_search(const svn_model* model, svn_precision prec,
  *                      needs distinct devices (UNSUPPORTED otherwise);
  *   SVN_SHARD_AUTO     points when M < G, else motions.
  * Results are bit-identical to one device in every mode.  Calls on one svn_multi are
- * serialised. */
+ * serialised.
+ * svn_multi_set_scene keeps one scene's cloud resident: the whole cloud is copied once to
+ * every device (run_box_world evaluates all of a scene's motions against one cloud,
+ * bench.cpp:185-198), and svn_query_min_multi calls with points == NULL run against it — P
+ * must then be the scene's point count — moving only the motions in and (min, argmin, free)
+ * out per call.  points == NULL, P == 0 drops the scene.  Without a scene, points == NULL is
+ * an argument error as before. */
 typedef struct svn_multi svn_multi;
 typedef enum { SVN_SHARD_AUTO = 0, SVN_SHARD_MOTIONS = 1, SVN_SHARD_POINTS = 2 } svn_shard_mode;
 SVN_API svn_status svn_multi_create(const svn_model_desc* desc, const float* params, int64_t n_params,
                                     const int32_t* devices, int32_t n_devices, svn_multi** out);
 SVN_API svn_status svn_multi_destroy(svn_multi* multi);
 SVN_API int32_t svn_multi_device_count(const svn_multi* multi);
+SVN_API svn_status svn_multi_set_scene(svn_multi* multi, const float* points, int64_t P);
 SVN_API svn_status svn_query_min_multi(svn_multi* multi, svn_precision prec, const float* points, int64_t P,
                                        const float* q01, int64_t M, double margin, svn_shard_mode mode,
                                        float* min_out, int32_t* argmin_out, uint8_t* free_out);

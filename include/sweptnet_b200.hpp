@@ -231,11 +231,28 @@ public:
                                   static_cast<svn_shard_mode>(shard), r.min.data(), r.argmin.data(), r.free.data()));
         return r;
     }
+    // Keep one scene's cloud resident on every device (svn_multi_set_scene); an empty vector
+    // drops it.  query_min_scene then moves only the motions in and the results out.
+    void set_scene(const std::vector<float>& points) {
+        check(svn_multi_set_scene(h_.get(), points.empty() ? nullptr : points.data(), static_cast<int64_t>(points.size() / 3)));
+        scene_points_ = static_cast<int64_t>(points.size() / 3);
+    }
+    MinResult query_min_scene(const std::vector<float>& q01, double margin, Precision prec = Precision::BF16,
+                              Shard shard = Shard::AUTO) const {
+        const int64_t M = static_cast<int64_t>(q01.size() / (2 * prog_.dof));
+        MinResult r{std::vector<float>(static_cast<size_t>(M)), std::vector<int32_t>(static_cast<size_t>(M)),
+                    std::vector<uint8_t>(static_cast<size_t>(M))};
+        check(svn_query_min_multi(h_.get(), static_cast<svn_precision>(prec), nullptr, scene_points_, q01.data(), M,
+                                  margin, static_cast<svn_shard_mode>(shard), r.min.data(), r.argmin.data(),
+                                  r.free.data()));
+        return r;
+    }
     int devices() const { return svn_multi_device_count(h_.get()); }
 
 private:
     Program prog_;
     std::shared_ptr<svn_multi> h_;
+    int64_t scene_points_ = 0;
 };
 
 }  // namespace sweptnet_b200

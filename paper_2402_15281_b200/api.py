@@ -206,15 +206,31 @@ class MultiModel:
         except Exception:
             pass
 
-    def query_min(self, points: np.ndarray, q01: np.ndarray, margin: float, precision: str = "bf16",
-                  shard: str = "auto") -> QueryResult:
+    def set_scene(self, points) -> None:
+        """Keep one scene's cloud resident on every device (svn_multi_set_scene); query_min
+        with points=None then runs against it.  points=None drops the scene."""
+        if points is None:
+            abi.check(abi.lib().svn_multi_set_scene(self._h, None, 0))
+            self._scene_points = 0
+            return
         pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+        abi.check(abi.lib().svn_multi_set_scene(self._h, abi.ptr(pts), pts.shape[0]))
+        self._scene_points = pts.shape[0]
+
+    def query_min(self, points, q01: np.ndarray, margin: float, precision: str = "bf16",
+                  shard: str = "auto") -> QueryResult:
         q = np.ascontiguousarray(q01, dtype=np.float32).reshape(-1, 2 * self.program.dof)
-        P, M = pts.shape[0], q.shape[0]
+        M = q.shape[0]
+        if points is None:  # the resident scene
+            pts, P = None, getattr(self, "_scene_points", 0)
+        else:
+            pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+            P = pts.shape[0]
         mn = np.empty(M, np.float32)
         am = np.empty(M, np.int32)
         fr = np.empty(M, np.uint8)
-        abi.check(abi.lib().svn_query_min_multi(self._h, abi.PRECISIONS[precision], abi.ptr(pts), P, abi.ptr(q), M,
+        abi.check(abi.lib().svn_query_min_multi(self._h, abi.PRECISIONS[precision],
+                                                abi.ptr(pts) if pts is not None else None, P, abi.ptr(q), M,
                                                 float(margin), abi.SHARD_MODES[shard], abi.ptr(mn), abi.ptr(am),
                                                 abi.ptr(fr)))
         return QueryResult(mn, am, fr.astype(bool), None)

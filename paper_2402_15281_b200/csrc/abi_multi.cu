@@ -152,8 +152,20 @@ struct svn_multi {
     std::string no_comm_why;
     std::vector<std::unique_ptr<svn::abi::Worker>> workers;
     std::mutex call_mu;  // one call at a time: collectives of two calls must not interleave
+    std::vector<float*> scene;  // the resident cloud, one whole copy per listed device (svn_multi_set_scene)
+    int64_t scene_points = 0;
+    void drop_scene() {
+        for (size_t d = 0; d < scene.size(); ++d)
+            if (scene[d]) {
+                svn::abi::DeviceGuard guard(models[d]->device);
+                cudaFree(scene[d]);
+            }
+        scene.clear();
+        scene_points = 0;
+    }
     ~svn_multi() {
         workers.clear();
+        drop_scene();
         if (!comms.empty())
             for (ncclComm_t c : comms) svn::abi::nccl_api().comm_destroy(c);
         for (svn_model* m : models) svn_model_destroy(m);
@@ -256,6 +268,35 @@ SVN_API int32_t svn_multi_device_count(const svn_multi* mg) {
     return mg ? static_cast<int32_t>(mg->devices.size()) : 0;
 }
 
+SVN_API svn_status svn_multi_set_scene(svn_multi* mg, const float* points, int64_t P) {
+    try {
+        if (!mg) return fail(SVN_ERR_INVALID_ARGUMENT, "multi: null handle");
+        if (P < 0 || (P > 0 && !points) || (P == 0 && points))
+            return fail(SVN_ERR_INVALID_ARGUMENT, "multi: scene needs points and a point count (NULL, 0 drops it)");
+        std::lock_guard<std::mutex> lock(mg->call_mu);
+        mg->drop_scene();
+        if (P == 0) return SVN_OK;
+        mg->scene.assign(mg->devices.size(), nullptr);
+        mg->scene_points = P;
+        const size_t bytes = sizeof(float) * 3 * static_cast<size_t>(P);
+        // the copies to the devices run side by side, one per worker (one host link each)
+        const svn_status s = run_all(mg, [&](int d, Outcome& o) {
+            DeviceGuard guard(mg->models[d]->device);
+            cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&mg->scene[d]), bytes);
+            if (e == cudaSuccess) e = cudaMemcpy(mg->scene[d], points, bytes, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) record(o, cuda_fail(e, "scene upload"));
+        });
+        if (s != SVN_OK) {
+            const std::string why = svn_last_error();
+            mg->drop_scene();
+            return fail(s, why);
+        }
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
+}
+
 SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const float* points, int64_t P,
                                        const float* q01, int64_t M, double margin, svn_shard_mode mode,
                                        float* min_out, int32_t* argmin_out, uint8_t* free_out) {
@@ -263,14 +304,54 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
         if (!mg) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
         if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
         if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
-        if (!points || !q01 || !min_out || !argmin_out || !free_out)
+        if (!q01 || !min_out || !argmin_out || !free_out)
             return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
         NvtxRange nvtx("svn query_min_multi");
         std::lock_guard<std::mutex> lock(mg->call_mu);
+        const bool resident = points == nullptr;
+        if (resident && mg->scene.empty()) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+        if (resident && P != mg->scene_points)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "multi: P differs from the resident scene's point count");
         const int G = static_cast<int>(mg->devices.size());
         if (mode == SVN_SHARD_AUTO) mode = M < G ? SVN_SHARD_POINTS : SVN_SHARD_MOTIONS;
         const int64_t nq = 2 * static_cast<int64_t>(mg->models[0]->dof);
 
+        if (mode == SVN_SHARD_MOTIONS && resident) {
+            // the cloud is already on every device: per call only this device's motions go in
+            // and its slice of (min, argmin, free) comes out
+            return run_all(mg, [&](int d, Outcome& o) {
+                const int64_t b = d * M / G, e = (d + 1) * M / G, n = e - b;
+                if (n < 1) return;
+                const svn_model* m = mg->models[d];
+                DeviceGuard guard(m->device);
+                ensure_pool(m->device);
+                cudaStream_t st = thread_stream(m->device);
+                auto cu = [&](cudaError_t err, const char* what) {
+                    if (err != cudaSuccess) record(o, cuda_fail(err, what));
+                    return err == cudaSuccess;
+                };
+                // one block: [q | min | argmin | free]
+                const size_t q_bytes = sizeof(float) * static_cast<size_t>(nq * n);
+                const size_t off_min = (q_bytes + 15) & ~size_t(15), off_arg = off_min + sizeof(float) * n,
+                             off_free = off_arg + sizeof(int32_t) * n;
+                char* blk = nullptr;
+                if (!cu(cudaMallocAsync(reinterpret_cast<void**>(&blk), off_free + n, st), "cudaMallocAsync")) return;
+                float* dq = reinterpret_cast<float*>(blk);
+                float* dmin = reinterpret_cast<float*>(blk + off_min);
+                int32_t* darg = reinterpret_cast<int32_t*>(blk + off_arg);
+                uint8_t* dfree = reinterpret_cast<uint8_t*>(blk + off_free);
+                if (cu(cudaMemcpyAsync(dq, q01 + b * nq, q_bytes, cudaMemcpyHostToDevice, st), "H2D motions")) {
+                    record(o, svn_query_min_device(m, prec, mg->scene[d], P, dq, n, margin, dmin, darg, dfree, nullptr, st));
+                    if (o.status == SVN_OK)
+                        cu(cudaMemcpyAsync(min_out + b, dmin, sizeof(float) * n, cudaMemcpyDeviceToHost, st), "D2H min") &&
+                            cu(cudaMemcpyAsync(argmin_out + b, darg, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st),
+                               "D2H argmin") &&
+                            cu(cudaMemcpyAsync(free_out + b, dfree, n, cudaMemcpyDeviceToHost, st), "D2H free");
+                }
+                cudaFreeAsync(blk, st);
+                cu(cudaStreamSynchronize(st), "resident-scene query");
+            });
+        }
         if (mode == SVN_SHARD_MOTIONS) {
             return run_all(mg, [&](int d, Outcome& o) {
                 const int64_t b = d * M / G, e = (d + 1) * M / G;
@@ -298,11 +379,17 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
             };
             bool ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&dq), sizeof(float) * nq * M, st), "cudaMallocAsync") &&
                       cu(cudaMallocAsync(reinterpret_cast<void**>(&keys), sizeof(uint64_t) * M, st), "cudaMallocAsync") &&
-                      cu(cudaMallocAsync(reinterpret_cast<void**>(&dp), sizeof(float) * 3 * (pe > pb ? pe - pb : 1), st),
-                         "cudaMallocAsync") &&
-                      cu(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions") &&
-                      cu(cudaMemcpyAsync(dp, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
-                         "H2D point chunk");
+                      cu(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions");
+            float* chunk = nullptr;  // this device's point chunk, freed below unless it is the resident scene's
+            if (ok && resident) {
+                dp = mg->scene[d] + 3 * pb;
+            } else if (ok) {
+                ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&chunk), sizeof(float) * 3 * (pe > pb ? pe - pb : 1), st),
+                        "cudaMallocAsync") &&
+                     cu(cudaMemcpyAsync(chunk, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
+                        "H2D point chunk");
+                dp = chunk;
+            }
             if (ok) {
                 record(o, svn_keys_init_device(keys, M, st));
                 if (o.status == SVN_OK && pe > pb) record(o, svn_query_min_keys_device(m, prec, dp, pe - pb, pb, dq, M, keys, st));
@@ -331,7 +418,7 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
                 o.status = SVN_ERR_CUDA;
                 o.msg = "multi: another device failed before the all-reduce";
             }
-            for (void* p : {static_cast<void*>(dp), static_cast<void*>(dq), static_cast<void*>(keys),
+            for (void* p : {static_cast<void*>(chunk), static_cast<void*>(dq), static_cast<void*>(keys),
                             static_cast<void*>(dmin), static_cast<void*>(darg), static_cast<void*>(dfree)})
                 if (p) cudaFreeAsync(p, st);
             cudaStreamSynchronize(st);

@@ -51,7 +51,11 @@ int main() {
     check(svn_init_params(&dd, 7, 0, params.data()));
     MultiModel mg(prog, params, {0, 0});
     const MinResult r = mg.query_min(pts, q01, 0.02, Precision::FP32_EXACT, Shard::MOTIONS);
-    const bool multi_ok = mg.devices() == 2 && r.min.size() == 3 && static_cast<double>(r.min[0]) == mn && r.argmin[0] == idx;
+    // the same against the scene kept resident on both devices
+    mg.set_scene(pts);
+    const MinResult rs = mg.query_min_scene(q01, 0.02, Precision::FP32_EXACT, Shard::MOTIONS);
+    const bool multi_ok = mg.devices() == 2 && r.min.size() == 3 && static_cast<double>(r.min[0]) == mn && r.argmin[0] == idx &&
+                          rs.min == r.min && rs.argmin == r.argmin && rs.free == r.free;
     // the same parameters as an SVCKPT01 checkpoint (nn.cpp:482-520): the loaded Model knows its
     // program from the header (dof, width, Fig. 2 layers) and predicts the same bits
     const char* ck = "host_api_demo.svckpt";

@@ -102,3 +102,42 @@ def test_concurrent_callers_serialise():
     assert not errs and len(out) == 20
     for r in out:
         _same(r, ref)
+
+
+@pytest.mark.parametrize("key,prec", [("c3", "bf16"), ("c2", "fp32"), ("c2", "fp32_split")])
+def test_resident_scene_equals_per_call_cloud(key, prec):
+    """svn_multi_set_scene: the cloud uploaded once to every device, later calls pass
+    points=None and move only motions in and results out — same bits as passing the cloud."""
+    w = WORKLOADS[key]
+    params = S.init_params(w.program, 41, w.bound)
+    pts, q = w.make(seed=41, motions=9, points=2100)
+    ref = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec)
+    mg = S.MultiModel(w.program, params, devices=[0, 0, 0])
+    with pytest.raises(ReferenceInvalidArgument, match="null buffer"):  # no scene yet
+        mg.query_min(None, q, w.margin, precision=prec, shard="motions")
+    mg.set_scene(pts)
+    for _ in range(2):
+        _same(mg.query_min(None, q, w.margin, precision=prec, shard="motions"), ref)
+    _same(mg.query_min(None, q[2:3], w.margin, precision=prec, shard="motions"),  # fewer motions than devices
+          S.Model(w.program, params).query_min(pts, q[2:3], w.margin, precision=prec))
+    _same(mg.query_min(pts, q, w.margin, precision=prec, shard="motions"), ref)  # an explicit cloud still works
+    # a second scene replaces the first
+    pts2, _ = w.make(seed=43, motions=1, points=700)
+    mg.set_scene(pts2)
+    _same(mg.query_min(None, q, w.margin, precision=prec, shard="motions"),
+          S.Model(w.program, params).query_min(pts2, q, w.margin, precision=prec))
+    mg.set_scene(None)
+    with pytest.raises(ReferenceInvalidArgument, match="null buffer"):
+        mg.query_min(None, q, w.margin, precision=prec, shard="motions")
+    mg.close()
+
+
+def test_resident_scene_point_shards_one_rank():
+    w = WORKLOADS["c3"]
+    params = S.init_params(w.program, 47, w.bound)
+    pts, q = w.make(seed=47, motions=2, points=3000)
+    ref = S.Model(w.program, params).query_min(pts, q, w.margin, precision="bf16")
+    mg = S.MultiModel(w.program, params, devices=[0])
+    mg.set_scene(pts)
+    _same(mg.query_min(None, q, w.margin, precision="bf16", shard="points"), ref)
+    mg.close()
