@@ -368,14 +368,16 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        if mode == "motion":
-            model.query_min_device(pts, q, w.margin, mn, am, fr, None, precision=prec, stream=stream)
-        else:
-            S.keys_init_device(keys, stream=stream)
-            model.query_keys_device(pts, pb, q, keys, precision=prec, stream=stream)
-            if world > 1:
-                allreduce_keys_min(keys)
-            S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
+        # every rank runs the tile shape of the whole (fixed) workload: the same bits at every N
+        with S.whole_batch(M_total, P):
+            if mode == "motion":
+                model.query_min_device(pts, q, w.margin, mn, am, fr, None, precision=prec, stream=stream)
+            else:
+                S.keys_init_device(keys, stream=stream)
+                model.query_keys_device(pts, pb, q, keys, precision=prec, stream=stream)
+                if world > 1:
+                    allreduce_keys_min(keys)
+                S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
 
     for _ in range(args.warmup):
         step()

@@ -286,8 +286,8 @@ SVN_API svn_status svn_gcc_nn_search(const svn_model* model, svn_precision prec,
  *                      all-reduce of the packed (delta, index) keys, 8 B per motion;
  *                      needs distinct devices (UNSUPPORTED otherwise);
  *   SVN_SHARD_AUTO     points when M < G, else motions.
- * Results are bit-identical to one device in every mode.  Calls on one svn_multi are
- * serialised.
+ * Results are bit-identical to one device in every mode and precision (the shards run the
+ * whole batch's tile shape, svn_set_whole_batch).  Calls on one svn_multi are serialised.
  * svn_multi_set_scene keeps one scene's cloud resident: the whole cloud is copied once to
  * every device (run_box_world evaluates all of a scene's motions against one cloud,
  * bench.cpp:185-198), and svn_query_min_multi calls with points == NULL run against it — P
@@ -304,6 +304,18 @@ SVN_API svn_status svn_multi_set_scene(svn_multi* multi, const float* points, in
 SVN_API svn_status svn_query_min_multi(svn_multi* multi, svn_precision prec, const float* points, int64_t P,
                                        const float* q01, int64_t M, double margin, svn_shard_mode mode,
                                        float* min_out, int32_t* argmin_out, uint8_t* free_out);
+
+/* Shards of one batch.  The tensor-core precisions pick their tile shape from the size of the
+ * launch (a launch with fewer 256-row tiles than CTA pairs runs 128-row tiles, for latency),
+ * and the two shapes sum the output dot in different orders: results ~1e-6 apart, far inside
+ * the precision's bound, but not the same bits.  A caller that evaluates one batch in several
+ * calls — motion ranges or point chunks on other devices or ranks — declares the whole
+ * batch's shape first; every shard then runs the tile shape the whole batch would, and the
+ * results are bit-identical to one call whatever the split, in every precision (the FP32
+ * paths are regardless).  Thread-local, applies to svn_query_min, svn_query_min_device and
+ * svn_query_min_keys_device until cleared with (0, 0).  svn_query_min_multi does this
+ * itself. */
+SVN_API void svn_set_whole_batch(int64_t M_total, int64_t P_total);
 
 /* Kernel launches issued by this thread since the last reset (evidence for bench.py). */
 SVN_API int64_t svn_launch_count(void);

@@ -200,6 +200,16 @@ inline CascadeResult classify_motions(const Model& m, const std::vector<float>& 
     return r;
 }
 
+// The calls made while a WholeBatch is alive are shards (motion ranges or point chunks) of one
+// batch of that shape and take its tile shape: the same bits whatever the split, in every
+// precision (svn_set_whole_batch; thread-local).  MultiModel does this itself.
+struct WholeBatch {
+    WholeBatch(int64_t motions, int64_t points) { svn_set_whole_batch(motions, points); }
+    ~WholeBatch() { svn_set_whole_batch(0, 0); }
+    WholeBatch(const WholeBatch&) = delete;
+    WholeBatch& operator=(const WholeBatch&) = delete;
+};
+
 // Several GPUs of this box from one process (svn_multi_*): one model copy and one worker
 // thread per device.  query_min shards motions (no communication) or, for batches with
 // fewer motions than devices, points (one NCCL u64 MIN all-reduce); bit-identical to Model.

@@ -236,6 +236,23 @@ class MultiModel:
         return QueryResult(mn, am, fr.astype(bool), None)
 
 
+class whole_batch:
+    """`with whole_batch(M_total, P_total): ...` — the calls inside are shards (motion ranges or
+    point chunks) of one batch of that shape and take its tile shape, so the tensor-core
+    precisions give the same bits whatever the split (svn_set_whole_batch; thread-local)."""
+
+    def __init__(self, motions: int, points: int):
+        self.shape = (int(motions), int(points))
+
+    def __enter__(self):
+        abi.lib().svn_set_whole_batch(*self.shape)
+        return self
+
+    def __exit__(self, *exc):
+        abi.lib().svn_set_whole_batch(0, 0)
+        return False
+
+
 def keys_init_device(keys, stream=None) -> None:
     st = C.c_void_p(stream.cuda_stream if stream is not None else 0)
     abi.check(abi.lib().svn_keys_init_device(abi.ptr(keys), keys.numel(), st))

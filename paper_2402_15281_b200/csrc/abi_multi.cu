@@ -3,7 +3,8 @@
 //
 //   motions sharding (default): worker d evaluates motions [d*M/G, (d+1)*M/G) against the
 //     whole cloud through the single-GPU path and writes its slice of the outputs; no
-//     communication, results bit-identical to one GPU.
+//     communication, results bit-identical to one GPU (every shard runs the whole batch's
+//     tile shape, svn_set_whole_batch).
 //   points sharding (single-motion batches, M < G): worker d evaluates the point chunk
 //     [d*P/G, (d+1)*P/G) into packed u64 keys with global point indices, the shards meet in
 //     one NCCL MIN all-reduce of 8 B per motion, and device 0 decodes (min, argmin, class);
@@ -176,6 +177,12 @@ namespace svn {
 namespace abi {
 namespace {
 
+// Worker threads are persistent: the whole-batch shape (svn_set_whole_batch) is set for one job.
+struct WholeBatch {
+    WholeBatch(int64_t M, int64_t P) { svn_set_whole_batch(M, P); }
+    ~WholeBatch() { svn_set_whole_batch(0, 0); }
+};
+
 void record(Outcome& o, svn_status s) {
     if (s != SVN_OK && o.status == SVN_OK) {
         o.status = s;
@@ -322,6 +329,7 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
             return run_all(mg, [&](int d, Outcome& o) {
                 const int64_t b = d * M / G, e = (d + 1) * M / G, n = e - b;
                 if (n < 1) return;
+                WholeBatch whole(M, P);
                 const svn_model* m = mg->models[d];
                 DeviceGuard guard(m->device);
                 ensure_pool(m->device);
@@ -355,6 +363,7 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
         if (mode == SVN_SHARD_MOTIONS) {
             return run_all(mg, [&](int d, Outcome& o) {
                 const int64_t b = d * M / G, e = (d + 1) * M / G;
+                WholeBatch whole(M, P);
                 if (e > b)
                     record(o, svn_query_min(mg->models[d], prec, points, P, q01 + b * nq, e - b, margin, min_out + b,
                                             argmin_out + b, free_out + b, nullptr));
@@ -366,6 +375,7 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
         return run_all(mg, [&](int d, Outcome& o) {
             const svn_model* m = mg->models[d];
             const int64_t pb = d * P / G, pe = (d + 1) * P / G;
+            WholeBatch whole(M, P);
             DeviceGuard guard(m->device);
             ensure_pool(m->device);
             cudaStream_t st = thread_stream(m->device);

@@ -47,6 +47,9 @@ int tile_rows(Kind k, int N) {
 // thousand points — the reference's per-motion predict_min_distance) is latency-bound, so it
 // runs 128-row pair tiles (64 rows per CTA, M=128 MMAs): twice the tiles, each through the
 // network in about half the time.  SVN_PAIR_TILE=128|256 forces one (A/B hook).
+// svn_set_whole_batch: the shape of the batch this thread's calls are shards of (0 = none)
+thread_local int64_t g_whole_M = 0, g_whole_P = 0;
+
 int tile_rows_for(Kind k, int N, int64_t big_tiles, int num_sms) {
     const int t = tile_rows(k, N);
     if (k == Kind::SIMT && big_tiles < num_sms) return kFp32SmallTile;
@@ -281,7 +284,10 @@ svn_status query_dense(const svn_model* m, svn_precision prec, const float* poin
     a.M = M;
     const Kind kind = kernel_kind(m, prec);
     const int TM0 = tile_rows(kind, m->N);
-    const int TM = tile_rows_for(kind, m->N, M * ((P + TM0 - 1) / TM0), m->num_sms);
+    // a shard takes the tile shape of the batch it is a shard of (same bits whatever the split)
+    const bool shard = g_whole_M > 0 && g_whole_P > 0 && kind != Kind::SIMT;
+    const int TM = tile_rows_for(kind, m->N, shard ? g_whole_M * ((g_whole_P + TM0 - 1) / TM0) : M * ((P + TM0 - 1) / TM0),
+                                 m->num_sms);
     a.tile_rows = TM;
     a.tiles_per_motion = (P + TM - 1) / TM;
     a.n_tiles = a.tiles_per_motion * M;
@@ -856,6 +862,11 @@ SVN_API svn_status svn_query_min_device(const svn_model* m, svn_precision prec, 
     } catch (...) {
         return host_exception();
     }
+}
+
+SVN_API void svn_set_whole_batch(int64_t M_total, int64_t P_total) {
+    g_whole_M = M_total > 0 && P_total > 0 ? M_total : 0;
+    g_whole_P = M_total > 0 && P_total > 0 ? P_total : 0;
 }
 
 SVN_API svn_status svn_keys_init_device(uint64_t* keys, int64_t M, void* stream) {

@@ -87,8 +87,10 @@ def motion_sharded_query(model, points, q01, margin, world: int, rank: int, prec
     am = torch.empty(n, dtype=torch.int32, device=dev)
     fr = torch.empty(n, dtype=torch.uint8, device=dev)
     if n:
-        model.query_min_device(points, q01[b:e].contiguous(), margin, mn, am, fr, None, precision=precision,
-                               stream=stream)
+        from .api import whole_batch
+        with whole_batch(M, points.shape[0]):  # the whole batch's tile shape: same bits for every world size
+            model.query_min_device(points, q01[b:e].contiguous(), margin, mn, am, fr, None, precision=precision,
+                                   stream=stream)
     return b, mn, am, fr
 
 
@@ -97,7 +99,7 @@ def point_sharded_query(model, points_full_host: np.ndarray, q01, margin, world:
     """Point-chunk sharding with one NCCL MIN all-reduce of 8 B per motion.
     points_full_host: float32 [P, 3] (each rank uploads only its chunk)."""
     import torch
-    from .api import keys_finalize_device, keys_init_device
+    from .api import keys_finalize_device, keys_init_device, whole_batch
     P = points_full_host.shape[0]
     b, e = shard_range(P, world, rank)
     dev = device or q01.device
@@ -106,7 +108,8 @@ def point_sharded_query(model, points_full_host: np.ndarray, q01, margin, world:
     keys_init_device(keys, stream=stream)
     if e > b:
         pts = torch.from_numpy(np.ascontiguousarray(points_full_host[b:e])).to(dev)
-        model.query_keys_device(pts, b, q01, keys, precision=precision, stream=stream)
+        with whole_batch(M, P):
+            model.query_keys_device(pts, b, q01, keys, precision=precision, stream=stream)
     if world > 1:
         allreduce_keys_min(keys, group)
     mn = torch.empty(M, dtype=torch.float32, device=dev)

@@ -113,7 +113,9 @@ def test_resident_scene_equals_per_call_cloud(key, prec):
     pts, q = w.make(seed=41, motions=9, points=2100)
     ref = S.Model(w.program, params).query_min(pts, q, w.margin, precision=prec)
     mg = S.MultiModel(w.program, params, devices=[0, 0, 0])
-    with pytest.raises(ReferenceInvalidArgument, match="null buffer"):  # no scene yet
+    # 9 x 2100 is 81 big tiles (>= 74 pairs: 256-row tiles) while a 3-motion shard alone would run
+    # 128-row tiles: the shards take the whole batch's shape, so `ref` is matched bit for bit
+    with pytest.raises(ReferenceInvalidArgument):  # no scene yet: an empty cloud (P = 0)
         mg.query_min(None, q, w.margin, precision=prec, shard="motions")
     mg.set_scene(pts)
     for _ in range(2):
@@ -127,7 +129,7 @@ def test_resident_scene_equals_per_call_cloud(key, prec):
     _same(mg.query_min(None, q, w.margin, precision=prec, shard="motions"),
           S.Model(w.program, params).query_min(pts2, q, w.margin, precision=prec))
     mg.set_scene(None)
-    with pytest.raises(ReferenceInvalidArgument, match="null buffer"):
+    with pytest.raises(ReferenceInvalidArgument):
         mg.query_min(None, q, w.margin, precision=prec, shard="motions")
     mg.close()
 
@@ -140,4 +142,44 @@ def test_resident_scene_point_shards_one_rank():
     mg = S.MultiModel(w.program, params, devices=[0])
     mg.set_scene(pts)
     _same(mg.query_min(None, q, w.margin, precision="bf16", shard="points"), ref)
+    mg.close()
+
+
+@pytest.mark.parametrize("key,prec", [("c3", "bf16"), ("c3", "fp16"), ("c2", "bf16"), ("c4", "bf16"), ("c3", "fp32_split")])
+def test_shards_take_the_whole_batch_tile_shape(key, prec):
+    """A launch with fewer 256-row tiles than CTA pairs runs 128-row tiles, whose output dot
+    sums in another order (~1e-6).  Declared as shards of the whole batch (svn_set_whole_batch),
+    motion ranges and point chunks give the whole batch's bits; svn_query_min_multi does so itself."""
+    w = WORKLOADS[key]
+    params = S.init_params(w.program, 41, w.bound)
+    pts, q = w.make(seed=41, motions=9, points=2100)  # 81 big tiles; 3 motions alone: 27
+    m = S.Model(w.program, params)
+    ref = m.query_min(pts, q, w.margin, precision=prec)
+    with S.whole_batch(9, 2100):
+        parts = [m.query_min(pts, q[i:i + 3], w.margin, precision=prec) for i in (0, 3, 6)]
+    assert np.array_equal(np.concatenate([p.min for p in parts]), ref.min)
+    assert np.array_equal(np.concatenate([p.argmin for p in parts]), ref.argmin)
+    # the setting is cleared on exit: a later small call runs its own shape again
+    alone = m.query_min(pts, q[:3], w.margin, precision=prec)
+    bound = 1e-5 if prec == "fp32_split" else 1e-4
+    assert np.abs(alone.min.astype(np.float64) - ref.min[:3]).max() <= bound
+    # point chunks through the keys entry points
+    import torch
+    from paper_2402_15281_b200 import parallel
+    dev = torch.device("cuda", 0)
+    qd = torch.from_numpy(q).to(dev)
+    keys = torch.empty(9, dtype=torch.int64, device=dev)
+    S.keys_init_device(keys)
+    with S.whole_batch(9, 2100):
+        for b in range(0, 2100, 700):
+            m.query_keys_device(torch.from_numpy(np.ascontiguousarray(pts[b:b + 700])).to(dev), b, qd, keys, precision=prec)
+    mn = torch.empty(9, dtype=torch.float32, device=dev)
+    am = torch.empty(9, dtype=torch.int32, device=dev)
+    fr = torch.empty(9, dtype=torch.uint8, device=dev)
+    S.keys_finalize_device(keys, w.margin, mn, am, fr)
+    torch.cuda.synchronize()
+    assert np.array_equal(mn.cpu().numpy(), ref.min) and np.array_equal(am.cpu().numpy(), ref.argmin)
+    # and the box: three workers, three motions each
+    mg = S.MultiModel(w.program, params, devices=[0, 0, 0])
+    _same(mg.query_min(pts, q, w.margin, precision=prec, shard="motions"), ref)
     mg.close()
