@@ -368,16 +368,20 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     def step():
-        # every rank runs the tile shape of the whole (fixed) workload: the same bits at every N
-        with S.whole_batch(M_total, P):
-            if mode == "motion":
-                model.query_min_device(pts, q, w.margin, mn, am, fr, None, precision=prec, stream=stream)
-            else:
-                S.keys_init_device(keys, stream=stream)
-                model.query_keys_device(pts, pb, q, keys, precision=prec, stream=stream)
-                if world > 1:
-                    allreduce_keys_min(keys)
-                S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
+        if mode == "motion":
+            model.query_min_device(pts, q, w.margin, mn, am, fr, None, precision=prec, stream=stream)
+        else:
+            S.keys_init_device(keys, stream=stream)
+            model.query_keys_device(pts, pb, q, keys, precision=prec, stream=stream)
+            if world > 1:
+                allreduce_keys_min(keys)
+            S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
+
+    # every rank runs the tile shape of the whole (fixed) workload — the same bits at every N
+    # (svn_set_whole_batch; set once for the warm-up and timed steps, cleared before the other legs)
+    shards = S.whole_batch(M_total, P)
+    if world > 1:
+        shards.__enter__()
 
     for _ in range(args.warmup):
         step()
@@ -406,6 +410,8 @@ def main():
             step()
             torch.cuda.synchronize(dev)
             extra_steps += 1
+    if world > 1:
+        shards.__exit__(None, None, None)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = sum(step_ms) / len(step_ms)
     kernel_ms = k_ms / max(1, k_n)
@@ -485,6 +491,45 @@ def main():
                "api": "svn_query_min (C-ABI, pinned host buffers)",
                "pageable": {"value": total_queries / (pg_ms * 1e-3), "ms_per_step": pg_ms,
                             "api": "svn_query_min (C-ABI, pageable host buffers: staged copy)"}}
+
+    elif not args.no_e2e:
+        # point mode: every rank copies ITS point chunk and the motions from pinned host memory,
+        # folds the chunk into the keys, the ranks meet in the MIN all-reduce, and rank 0's
+        # (min, argmin, free) come back to the host — all inside the timed region
+        hchunk = torch.from_numpy(np.ascontiguousarray(pts_np[pb:pe])).pin_memory()
+        hq = torch.from_numpy(q_np).pin_memory()
+
+        def e_step():
+            dp = hchunk.to(dev, non_blocking=True)
+            dq = hq.to(dev, non_blocking=True)
+            S.keys_init_device(keys, stream=stream)
+            with S.whole_batch(M_total, P):
+                model.query_keys_device(dp, pb, dq, keys, precision=prec, stream=stream)
+            if world > 1:
+                allreduce_keys_min(keys)
+            S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
+            return mn.cpu(), am.cpu(), fr.cpu()
+
+        e_step()
+        n_e = 1 if ms > 2000 else max(1, min(args.steps, 3))
+        t_e = []
+        for _ in range(n_e):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            e_step()
+            t_e.append(time.perf_counter() - t0)
+        e_ms = statistics.mean(t_e) * 1e3
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": total_queries / (e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(hchunk.numel() * 4 + hq.numel() * 4), "d2h_bytes_per_step": int(M * (4 + 4 + 1)),
+               "ms_per_step": e_ms, "steps": n_e,
+               "api": "svn_query_min_keys_device + u64 MIN all-reduce + svn_keys_finalize_device (C-ABI; each rank's "
+                      "point chunk from pinned host memory, bytes per rank)"}
 
     # ---- CPU baseline + parity (rank 0) ----------------------------------------
     cpu = None
