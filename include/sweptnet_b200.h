@@ -304,6 +304,14 @@ SVN_API svn_status svn_multi_set_scene(svn_multi* multi, const float* points, in
 SVN_API svn_status svn_query_min_multi(svn_multi* multi, svn_precision prec, const float* points, int64_t P,
                                        const float* q01, int64_t M, double margin, svn_shard_mode mode,
                                        float* min_out, int32_t* argmin_out, uint8_t* free_out);
+/* svn_query_min_cascade over the box: device d runs the cascade on motions [d*M/G, (d+1)*M/G)
+ * against the whole cloud (no communication); free_out equals the FP32 path's for every motion
+ * and every output equals one device's.  stage_motions (int64 [3] or NULL) receives the
+ * motions evaluated per stage, summed over the devices.  HOST buffers, synchronous. */
+SVN_API svn_status svn_query_min_cascade_multi(svn_multi* multi, svn_precision coarse, double band_coarse,
+                                               double band_split, const float* points, int64_t P,
+                                               const float* q01, int64_t M, double margin, float* min_out,
+                                               int32_t* argmin_out, uint8_t* free_out, int64_t* stage_motions);
 
 /* Shards of one batch.  The tensor-core precisions pick their tile shape from the size of the
  * launch (a launch with fewer 256-row tiles than CTA pairs runs 128-row tiles, for latency),

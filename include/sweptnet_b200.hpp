@@ -257,6 +257,19 @@ public:
                                   r.free.data()));
         return r;
     }
+    // query_min with the class equal to the FP32 path's for every motion (svn_query_min_cascade_multi):
+    // bands = the stated bounds of `coarse` and of FP32_SPLIT; stage_motions as in the C entry.
+    MinResult query_min_cascade(const std::vector<float>& points, const std::vector<float>& q01, double margin,
+                                double band_coarse, double band_split, Precision coarse = Precision::FP16,
+                                std::array<int64_t, 3>* stage_motions = nullptr) const {
+        const int64_t P = static_cast<int64_t>(points.size() / 3), M = static_cast<int64_t>(q01.size() / (2 * prog_.dof));
+        MinResult r{std::vector<float>(static_cast<size_t>(M)), std::vector<int32_t>(static_cast<size_t>(M)),
+                    std::vector<uint8_t>(static_cast<size_t>(M))};
+        check(svn_query_min_cascade_multi(h_.get(), static_cast<svn_precision>(coarse), band_coarse, band_split,
+                                          points.data(), P, q01.data(), M, margin, r.min.data(), r.argmin.data(),
+                                          r.free.data(), stage_motions ? stage_motions->data() : nullptr));
+        return r;
+    }
     int devices() const { return svn_multi_device_count(h_.get()); }
 
 private:

@@ -123,6 +123,7 @@ def _finish(L):
         "svn_set_whole_batch": (None, [I64, I64]),
         "svn_multi_set_scene": (C.c_int, [VP, P, I64]),
         "svn_query_min_multi": (C.c_int, [VP, C.c_int, P, I64, P, I64, D, C.c_int, P, P, P]),
+        "svn_query_min_cascade_multi": (C.c_int, [VP, C.c_int, D, D, P, I64, P, I64, D, P, P, P, P]),
         "svn_launch_count": (I64, []),
         "svn_launch_count_reset": (None, []),
         "svn_kernel_timing_begin": (None, []),
@@ -145,7 +146,7 @@ EXPORTED = ("svn_param_count", "svn_trainable_param_count", "svn_init_params", "
             "svn_query_min_cascade", "svn_keys_init_device", "svn_query_min_keys_device", "svn_keys_finalize_device", "svn_forward_eval",
             "svn_forward_eval_device", "svn_predict_min_distance", "svn_eval_grid", "svn_gcc_min_distance",
             "svn_gcc_min_distance_device", "svn_gcc_nn_search", "svn_multi_create", "svn_multi_destroy",
-            "svn_multi_device_count", "svn_multi_set_scene", "svn_set_whole_batch", "svn_query_min_multi", "svn_launch_count",
+            "svn_multi_device_count", "svn_multi_set_scene", "svn_set_whole_batch", "svn_query_min_multi", "svn_query_min_cascade_multi", "svn_launch_count",
             "svn_launch_count_reset",
             "svn_kernel_timing_begin", "svn_kernel_timing_end", "svn_last_error", "svn_version")
 

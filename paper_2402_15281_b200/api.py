@@ -235,6 +235,20 @@ class MultiModel:
                                                 abi.ptr(fr)))
         return QueryResult(mn, am, fr.astype(bool), None)
 
+    def query_min_cascade(self, points, q01, margin: float, band_coarse: float, band_split: float,
+                          coarse: str = "fp16"):
+        """Model.query_min_cascade over the box (svn_query_min_cascade_multi): motions split over the
+        devices, the class equal to the FP32 path's for every motion, outputs equal to one device's."""
+        pts = np.ascontiguousarray(points, dtype=np.float32).reshape(-1, 3)
+        q = np.ascontiguousarray(q01, dtype=np.float32).reshape(-1, 2 * self.program.dof)
+        P, M = pts.shape[0], q.shape[0]
+        mn, am, fr = np.empty(M, np.float32), np.empty(M, np.int32), np.empty(M, np.uint8)
+        stages = np.zeros(3, np.int64)
+        abi.check(abi.lib().svn_query_min_cascade_multi(self._h, abi.PRECISIONS[coarse], float(band_coarse),
+                                                        float(band_split), abi.ptr(pts), P, abi.ptr(q), M, float(margin),
+                                                        abi.ptr(mn), abi.ptr(am), abi.ptr(fr), abi.ptr(stages)))
+        return QueryResult(mn, am, fr.astype(bool), None), (int(stages[0]), int(stages[1]), int(stages[2]))
+
 
 class whole_batch:
     """`with whole_batch(M_total, P_total): ...` — the calls inside are shards (motion ranges or

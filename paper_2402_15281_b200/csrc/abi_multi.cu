@@ -438,4 +438,38 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
     }
 }
 
+SVN_API svn_status svn_query_min_cascade_multi(svn_multi* mg, svn_precision coarse, double band_coarse,
+                                               double band_split, const float* points, int64_t P,
+                                               const float* q01, int64_t M, double margin, float* min_out,
+                                               int32_t* argmin_out, uint8_t* free_out, int64_t* stage_motions) {
+    try {
+        if (!mg) return fail(SVN_ERR_INVALID_ARGUMENT, "query: null model");
+        if (P < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "predict_min_distance: empty point cloud");
+        if (M < 1) return fail(SVN_ERR_INVALID_ARGUMENT, "query: no motions");
+        if (!points || !q01 || !min_out || !argmin_out || !free_out)
+            return fail(SVN_ERR_INVALID_ARGUMENT, "query: null buffer");
+        NvtxRange nvtx("svn query_min_cascade_multi");
+        std::lock_guard<std::mutex> lock(mg->call_mu);
+        const int G = static_cast<int>(mg->devices.size());
+        const int64_t nq = 2 * static_cast<int64_t>(mg->models[0]->dof);
+        std::vector<int64_t> stages(static_cast<size_t>(3 * G), 0);
+        const svn_status s = run_all(mg, [&](int d, Outcome& o) {
+            const int64_t b = d * M / G, e = (d + 1) * M / G;
+            if (e <= b) return;
+            WholeBatch whole(M, P);
+            record(o, svn_query_min_cascade(mg->models[d], coarse, band_coarse, band_split, points, P, q01 + b * nq,
+                                            e - b, margin, min_out + b, argmin_out + b, free_out + b, &stages[3 * d]));
+        });
+        if (s != SVN_OK) return s;
+        if (stage_motions)
+            for (int k = 0; k < 3; ++k) {
+                stage_motions[k] = 0;
+                for (int d = 0; d < G; ++d) stage_motions[k] += stages[3 * d + k];
+            }
+        return SVN_OK;
+    } catch (...) {
+        return host_exception();
+    }
+}
+
 }  // extern "C"

@@ -91,3 +91,29 @@ def test_cascade_without_fp32_split_and_argument_checks():
         model.query_min_cascade(pts, q, 0.005, 0.01, 1e-5, coarse="fp32")
     with pytest.raises(abi.SvnError):
         model.query_min_cascade(pts, q, 0.005, -1.0, 1e-5)
+
+
+@pytest.mark.parametrize("coarse", ["fp16", "bf16"])
+def test_cascade_over_the_box_equals_one_device(coarse):
+    """svn_query_min_cascade_multi: motions split over three workers (device 0 three times),
+    every output and the per-stage motion counts equal to one device's cascade."""
+    w = WORKLOADS["c3"]
+    M, P = 301, 3000
+    pts, q, params = _calibrated(w, 43, M, P)
+    name = w.program.name
+    one, st_one = S.Model(w.program, params).query_min_cascade(pts, q, w.margin, BOUNDS[coarse][name],
+                                                               BOUNDS["fp32_split"][name], coarse=coarse)
+    mg = S.MultiModel(w.program, params, devices=[0, 0, 0])
+    box, st_box = mg.query_min_cascade(pts, q, w.margin, BOUNDS[coarse][name], BOUNDS["fp32_split"][name], coarse=coarse)
+    assert np.array_equal(box.free, one.free) and np.array_equal(box.min, one.min) and np.array_equal(box.argmin, one.argmin)
+    assert st_box == st_one and st_box[0] == M and 0 < st_box[1] < M
+    exact = S.Model(w.program, params).query_min(pts, q, w.margin, precision="fp32")
+    assert np.array_equal(box.free, exact.free)
+    # fewer motions than workers, and the argument checks of the single-device entry
+    two, _ = mg.query_min_cascade(pts, q[:2], w.margin, BOUNDS[coarse][name], BOUNDS["fp32_split"][name], coarse=coarse)
+    assert np.array_equal(two.free, exact.free[:2])
+    with pytest.raises(abi.ReferenceInvalidArgument):
+        mg.query_min_cascade(pts, q, w.margin, -1.0, 0.0, coarse=coarse)
+    with pytest.raises(abi.ReferenceInvalidArgument, match="empty point cloud"):
+        mg.query_min_cascade(pts[:0], q, w.margin, 0.1, 0.0, coarse=coarse)
+    mg.close()
