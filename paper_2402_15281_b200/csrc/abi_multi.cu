@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <functional>
 #include <memory>
@@ -391,19 +392,44 @@ SVN_API svn_status svn_query_min_multi(svn_multi* mg, svn_precision prec, const 
                       cu(cudaMallocAsync(reinterpret_cast<void**>(&keys), sizeof(uint64_t) * M, st), "cudaMallocAsync") &&
                       cu(cudaMemcpyAsync(dq, q01, sizeof(float) * nq * M, cudaMemcpyHostToDevice, st), "H2D motions");
             float* chunk = nullptr;  // this device's point chunk, freed below unless it is the resident scene's
+            constexpr int64_t kPiece = int64_t(1) << 20;
+            bool piped = false;
             if (ok && resident) {
                 dp = mg->scene[d] + 3 * pb;
             } else if (ok) {
                 ok = cu(cudaMallocAsync(reinterpret_cast<void**>(&chunk), sizeof(float) * 3 * (pe > pb ? pe - pb : 1), st),
-                        "cudaMallocAsync") &&
-                     cu(cudaMemcpyAsync(chunk, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
-                        "H2D point chunk");
+                        "cudaMallocAsync");
+                // a large chunk travels in pieces on a second stream while this stream folds the
+                // pieces already here into the keys (as svn_query_min does for large clouds)
+                piped = ok && pe - pb >= 2 * kPiece;
+                if (ok && !piped)
+                    ok = cu(cudaMemcpyAsync(chunk, points + 3 * pb, sizeof(float) * 3 * (pe - pb), cudaMemcpyHostToDevice, st),
+                            "H2D point chunk");
                 dp = chunk;
             }
             if (ok) {
                 record(o, svn_keys_init_device(keys, M, st));
-                if (o.status == SVN_OK && pe > pb) record(o, svn_query_min_keys_device(m, prec, dp, pe - pb, pb, dq, M, keys, st));
-                ok = o.status == SVN_OK && cu(cudaStreamSynchronize(st), "point-shard kernels");
+                if (o.status == SVN_OK && piped) {
+                    cudaStream_t cs = nullptr;
+                    cudaEvent_t ev = nullptr;
+                    ok = cu(cudaStreamSynchronize(st), "cudaMallocAsync(point chunk)") &&  // the chunk exists before cs writes it
+                         cu(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate") &&
+                         cu(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+                    for (int64_t p0 = 0; ok && o.status == SVN_OK && p0 < pe - pb; p0 += kPiece) {
+                        const int64_t n = std::min<int64_t>(kPiece, pe - pb - p0);
+                        ok = cu(cudaMemcpyAsync(chunk + 3 * p0, points + 3 * (pb + p0), sizeof(float) * 3 * n,
+                                                cudaMemcpyHostToDevice, cs),
+                                "H2D point piece") &&
+                             cu(cudaEventRecord(ev, cs), "cudaEventRecord") && cu(cudaStreamWaitEvent(st, ev, 0), "cudaStreamWaitEvent");
+                        if (ok) record(o, svn_query_min_keys_device(m, prec, chunk + 3 * p0, n, pb + p0, dq, M, keys, st));
+                    }
+                    if (cs) cudaStreamSynchronize(cs);
+                    if (ev) cudaEventDestroy(ev);
+                    if (cs) cudaStreamDestroy(cs);
+                } else if (o.status == SVN_OK && pe > pb) {
+                    record(o, svn_query_min_keys_device(m, prec, dp, pe - pb, pb, dq, M, keys, st));
+                }
+                ok = ok && o.status == SVN_OK && cu(cudaStreamSynchronize(st), "point-shard kernels");
             }
             if (meet.arrive_all_ok(ok)) {
                 // the one exchange of the path: 8 B per motion, u64 MIN over NVLink

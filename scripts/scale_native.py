@@ -1,7 +1,7 @@
 """Scaling of the single-process multi-GPU path (svn_query_min_multi, one worker thread per
 GPU) over the GPUs of this box: weak scaling of motion shards (c3's per-GPU size per device)
 and strong scaling of point shards (c5single: one motion, 2^24 points, one NCCL MIN
-all-reduce).  Host buffers in, results out (the e2e contract of svn_query_min); wall time of
+all-reduce; also against the resident scene).  Host buffers in, results out (the e2e contract of svn_query_min); wall time of
 the synchronous call, median of a few calls.  python scripts/scale_native.py [--max-gpus N]"""
 import argparse
 import json
@@ -46,7 +46,7 @@ def main():
         print(json.dumps({"mode": "motions (weak)", "n_gpus": n, "queries_per_s": qps, "seconds": sec,
                           "efficiency_vs_1": qps / (base * n)}), flush=True)
         mg.close()
-    base = None
+    base = base_res = None
     for n in counts:
         w = WORKLOADS["c5single"]
         params = S.init_params(w.program, 0, w.bound)
@@ -57,6 +57,12 @@ def main():
         base = base or qps
         print(json.dumps({"mode": "points (strong)", "n_gpus": n, "queries_per_s": qps, "seconds": sec,
                           "speedup_vs_1": qps / base}), flush=True)
+        # the same against the scene kept resident on the devices (svn_multi_set_scene)
+        mg.set_scene(pts)
+        sec = timed(lambda: mg.query_min(None, q, w.margin, precision="bf16", shard="points"), args.reps)
+        base_res = base_res or pts.shape[0] / sec
+        print(json.dumps({"mode": "points (strong), resident scene", "n_gpus": n, "queries_per_s": pts.shape[0] / sec,
+                          "seconds": sec, "speedup_vs_1": pts.shape[0] / sec / base_res}), flush=True)
         mg.close()
 
 

@@ -183,3 +183,17 @@ def test_shards_take_the_whole_batch_tile_shape(key, prec):
     mg = S.MultiModel(w.program, params, devices=[0, 0, 0])
     _same(mg.query_min(pts, q, w.margin, precision=prec, shard="motions"), ref)
     mg.close()
+
+
+def test_point_shard_large_chunk_is_piped_and_bit_identical():
+    """A worker's point chunk of >= 2^21 points travels in 2^20-point pieces on a second stream
+    while the pieces already on the device are folded into the keys: same bits as one device."""
+    w = WORKLOADS["c3"]
+    params = S.init_params(w.program, 53, w.bound)
+    pts, q = w.make(seed=53, motions=2, points=(1 << 21) + 5000)
+    ref = S.Model(w.program, params).query_min(pts, q, w.margin, precision="bf16")
+    mg = S.MultiModel(w.program, params, devices=[0])
+    _same(mg.query_min(pts, q, w.margin, precision="bf16", shard="points"), ref)
+    mg.set_scene(pts)
+    _same(mg.query_min(None, q, w.margin, precision="bf16", shard="points"), ref)
+    mg.close()
