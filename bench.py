@@ -467,8 +467,9 @@ def main():
         hp = torch.from_numpy(pts_np).pin_memory().numpy()
         hq = torch.from_numpy(q_np).pin_memory().numpy()
         # warm the host path (staging block, scratch arena sized by the previous call): the full batch
-        # when a step is short, a few motions of it when a step takes seconds
-        model.query_min(hp, hq if ms < 100 else hq[: min(M, 8)], w.margin, precision=prec)
+        # when a step takes under 2 s (a first full-size call was seen to cost up to ~0.1 s extra), a few
+        # motions of it when a step takes longer
+        model.query_min(hp, hq if ms < 2000 else hq[: min(M, 8)], w.margin, precision=prec)
         n_e = 1 if ms > 2000 else max(1, min(args.steps, 3))
         if world > 1:
             dist.barrier()
@@ -488,6 +489,7 @@ def main():
             e_ms, pg_ms = float(t[0]), float(t[1])
         e2e = {"value": total_queries / (e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(hp.nbytes + hq.nbytes),
                "d2h_bytes_per_step": int(M * (4 + 4 + 1)), "ms_per_step": e_ms, "steps": n_e,
+               "ms_samples": [round(t * 1e3, 3) for t in t_e],
                "api": "svn_query_min (C-ABI, pinned host buffers)",
                "pageable": {"value": total_queries / (pg_ms * 1e-3), "ms_per_step": pg_ms,
                             "api": "svn_query_min (C-ABI, pageable host buffers: staged copy)"}}
@@ -496,19 +498,15 @@ def main():
         # point mode: every rank copies ITS point chunk and the motions from pinned host memory,
         # folds the chunk into the keys, the ranks meet in the MIN all-reduce, and rank 0's
         # (min, argmin, free) come back to the host — all inside the timed region
-        hchunk = torch.from_numpy(np.ascontiguousarray(pts_np[pb:pe])).pin_memory()
+        from paper_2402_15281_b200.parallel import point_sharded_query
+        hfull = torch.from_numpy(pts_np).pin_memory().numpy()  # each rank reads only its chunk of it
         hq = torch.from_numpy(q_np).pin_memory()
+        hchunk = hfull[pb:pe]
 
         def e_step():
-            dp = hchunk.to(dev, non_blocking=True)
             dq = hq.to(dev, non_blocking=True)
-            S.keys_init_device(keys, stream=stream)
-            with S.whole_batch(M_total, P):
-                model.query_keys_device(dp, pb, dq, keys, precision=prec, stream=stream)
-            if world > 1:
-                allreduce_keys_min(keys)
-            S.keys_finalize_device(keys, w.margin, mn, am, fr, stream=stream)
-            return mn.cpu(), am.cpu(), fr.cpu()
+            r = point_sharded_query(model, hfull, dq, w.margin, world, rank, precision=prec, stream=stream, device=dev)
+            return tuple(t.cpu() for t in r)
 
         e_step()
         n_e = 1 if ms > 2000 else max(1, min(args.steps, 3))
@@ -526,10 +524,11 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t[0])
         e2e = {"value": total_queries / (e_ms * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": int(hchunk.numel() * 4 + hq.numel() * 4), "d2h_bytes_per_step": int(M * (4 + 4 + 1)),
+               "h2d_bytes_per_step": int(hchunk.size * 4 + hq.numel() * 4), "d2h_bytes_per_step": int(M * (4 + 4 + 1)),
                "ms_per_step": e_ms, "steps": n_e,
-               "api": "svn_query_min_keys_device + u64 MIN all-reduce + svn_keys_finalize_device (C-ABI; each rank's "
-                      "point chunk from pinned host memory, bytes per rank)"}
+               "api": "parallel.point_sharded_query: svn_query_min_keys_device + u64 MIN all-reduce + "
+                      "svn_keys_finalize_device (each rank's point chunk from pinned host memory, in 2^20-point pieces "
+                      "on a side stream; bytes per rank)"}
 
     # ---- CPU baseline + parity (rank 0) ----------------------------------------
     cpu = None

@@ -75,6 +75,8 @@ def allreduce_keys_min(keys, group=None):
     return keys
 
 
+PIECE_POINTS = 1 << 20  # point_sharded_query: upload granularity of a large chunk
+
 # ------------------------------------------------------------- GPU drivers ---
 def motion_sharded_query(model, points, q01, margin, world: int, rank: int, precision="bf16", stream=None):
     """This rank's motion shard on its GPU; returns (motion_begin, min, argmin, free) device tensors."""
@@ -106,7 +108,25 @@ def point_sharded_query(model, points_full_host: np.ndarray, q01, margin, world:
     M = q01.shape[0]
     keys = torch.empty(M, dtype=torch.int64, device=dev)
     keys_init_device(keys, stream=stream)
-    if e > b:
+    if e - b >= 2 * PIECE_POINTS and torch.device(dev).type == "cuda":
+        # a large chunk travels in pieces on a side stream while the compute stream folds the
+        # pieces already on the device into the keys (bit-identical: min over packed keys)
+        cur = stream if stream is not None else torch.cuda.current_stream(dev)
+        side = torch.cuda.Stream(device=dev)
+        buf = torch.empty((e - b, 3), dtype=torch.float32, device=dev)
+        buf.record_stream(side)
+        side.wait_stream(cur)
+        with whole_batch(M, P):
+            for p0 in range(0, e - b, PIECE_POINTS):
+                n = min(PIECE_POINTS, e - b - p0)
+                src = torch.from_numpy(np.ascontiguousarray(points_full_host[b + p0:b + p0 + n]))
+                with torch.cuda.stream(side):
+                    buf[p0:p0 + n].copy_(src, non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(side)
+                cur.wait_event(ev)
+                model.query_keys_device(buf[p0:p0 + n], b + p0, q01, keys, precision=precision, stream=stream)
+    elif e > b:
         pts = torch.from_numpy(np.ascontiguousarray(points_full_host[b:e])).to(dev)
         with whole_batch(M, P):
             model.query_keys_device(pts, b, q01, keys, precision=precision, stream=stream)

@@ -197,3 +197,22 @@ def test_point_shard_large_chunk_is_piped_and_bit_identical():
     mg.set_scene(pts)
     _same(mg.query_min(None, q, w.margin, precision="bf16", shard="points"), ref)
     mg.close()
+
+
+def test_parallel_point_sharded_query_pipes_a_large_chunk():
+    """parallel.point_sharded_query (the torchrun path): a chunk of >= 2^21 points is uploaded in
+    2^20-point pieces on a side stream and folded piece by piece — same bits as one call."""
+    import torch
+    from paper_2402_15281_b200 import parallel
+    w = WORKLOADS["c3"]
+    params = S.init_params(w.program, 59, w.bound)
+    pts, q = w.make(seed=59, motions=2, points=(1 << 21) + 777)
+    model = S.Model(w.program, params)
+    ref = model.query_min(pts, q, w.margin, precision="bf16")
+    dev = torch.device("cuda", 0)
+    qd = torch.from_numpy(q).to(dev)
+    for host in (pts, torch.from_numpy(pts).pin_memory().numpy()):  # pageable and pinned callers
+        mn, am, fr = parallel.point_sharded_query(model, host, qd, w.margin, 1, 0, precision="bf16", device=dev)
+        torch.cuda.synchronize()
+        assert np.array_equal(mn.cpu().numpy(), ref.min) and np.array_equal(am.cpu().numpy(), ref.argmin)
+        assert np.array_equal(fr.cpu().numpy().astype(bool), ref.free)
