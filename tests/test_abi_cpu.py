@@ -112,3 +112,13 @@ def test_workloads_shapes_and_shard_slices():
         assert np.array_equal(pts, pts2) and np.array_equal(q[2:], q2)
     pts, _ = WORKLOADS["c2"].make(seed=0, motions=1, points=4000)
     assert np.all(pts >= np.array([0, -0.4, 0]) - 1e-6) and np.all(pts <= np.array([1.2, 0.4, 0.5]) + 1e-6)
+
+
+def test_whole_batch_setting_needs_no_device():
+    """svn_set_whole_batch is a thread-local setting (no CUDA call): the context manager sets and
+    clears it without a GPU, and nonsense shapes clear it."""
+    import paper_2402_15281_b200 as S
+    with S.whole_batch(9, 2100) as wb:
+        assert wb.shape == (9, 2100)
+    S.abi.lib().svn_set_whole_batch(-3, 10)
+    S.abi.lib().svn_set_whole_batch(0, 0)
